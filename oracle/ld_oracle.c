@@ -1,0 +1,224 @@
+/*
+ * ld_oracle.c -- plain single-threaded C99 oracle for the lane-detection hot
+ * path of arXiv 2212.09460.  TEST INFRASTRUCTURE ONLY (see ld_oracle.h): it is
+ * written for a reader checking it against the paper by eye, not for speed.
+ * No blocking, fusion, vectorisation or reordering beyond the paper's own
+ * definitions; it shares no code, header or table with the CUDA path.
+ */
+#include "ld_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+/* Fig. 2: the two Sobel kernels, row 0 on top. */
+static const int SOBEL_X[3][3] = {{-1, 0, +1}, {-2, 0, +2}, {-1, 0, +1}};
+static const int SOBEL_Y[3][3] = {{+1, +2, +1}, {0, 0, 0}, {-1, -2, -1}};
+
+int32_t ldo_rho_offset(int32_t width, int32_t height) {
+  if (width < 1 || height < 1) return -1;
+  int64_t d2 = (int64_t)width * width + (int64_t)height * height;
+  int64_t d = 0;
+  while (d * d < d2) d++; /* smallest D with D^2 >= W^2 + H^2 */
+  return (int32_t)d;
+}
+
+static int32_t iabs32(int32_t v) { return v < 0 ? -v : v; }
+
+int ldo_sobel_magnitude(const uint8_t *gray, int32_t width, int32_t height,
+                        int64_t pitch, int32_t *mag) {
+  if (!gray || !mag || width < 1 || height < 1 || pitch < width) return LDO_EARG;
+  for (int32_t y = 0; y < height; y++) {
+    for (int32_t x = 0; x < width; x++) {
+      int border = (x == 0 || x == width - 1 || y == 0 || y == height - 1);
+      if (border) { /* DESIGN R2: 1-px output border forced to 0 */
+        mag[(int64_t)y * width + x] = 0;
+        continue;
+      }
+      int32_t gx = 0, gy = 0; /* Eq. 1: literal multiply-accumulate */
+      for (int i = 0; i < 3; i++) {
+        for (int j = 0; j < 3; j++) {
+          int32_t p = gray[(int64_t)(y - 1 + i) * pitch + (x - 1 + j)];
+          gx += SOBEL_X[i][j] * p;
+          gy += SOBEL_Y[i][j] * p;
+        }
+      }
+      mag[(int64_t)y * width + x] = iabs32(gx) + iabs32(gy);
+    }
+  }
+  return LDO_OK;
+}
+
+int ldo_sobel_binarize(const uint8_t *gray, int32_t width, int32_t height,
+                       int64_t pitch, int32_t threshold, uint8_t *binary) {
+  if (!gray || !binary || width < 1 || height < 1 || pitch < width) return LDO_EARG;
+  int32_t *mag = (int32_t *)malloc(sizeof(int32_t) * (size_t)width * (size_t)height);
+  if (!mag) return LDO_ENOMEM;
+  int rc = ldo_sobel_magnitude(gray, width, height, pitch, mag);
+  if (rc == LDO_OK) {
+    for (int32_t y = 0; y < height; y++) {
+      for (int32_t x = 0; x < width; x++) {
+        int64_t i = (int64_t)y * width + x;
+        int border = (x == 0 || x == width - 1 || y == 0 || y == height - 1);
+        /* P:76 every pixel becomes 255 or 0; comparator sense ">=" (R4) */
+        binary[i] = (!border && mag[i] >= threshold) ? 255 : 0;
+      }
+    }
+  }
+  free(mag);
+  return rc;
+}
+
+int ldo_compact(const uint8_t *binary, int32_t width, int32_t height,
+                uint32_t *edges, int64_t cap, int64_t *n_edges) {
+  if (!binary || !n_edges || width < 1 || height < 1 || width > 65536 ||
+      height > 65536 || cap < 0 || (cap > 0 && !edges))
+    return LDO_EARG;
+  int64_t n = 0;
+  for (int32_t y = 0; y < height; y++) {
+    for (int32_t x = 0; x < width; x++) {
+      if (binary[(int64_t)y * width + x] == 255) {
+        if (n >= cap) return LDO_ECAP;
+        edges[n++] = ((uint32_t)y << 16) | (uint32_t)x;
+      }
+    }
+  }
+  *n_edges = n;
+  return LDO_OK;
+}
+
+/* floor(a / b) for b > 0, written with C division (which truncates toward 0)
+ * and an explicit correction -- deliberately not an arithmetic shift. */
+static int64_t floor_div(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
+  return q;
+}
+
+int ldo_hough_accumulate(const uint32_t *edges, int64_t n_edges, int32_t width,
+                         int32_t height, int32_t n_theta, const int32_t *cos_q15,
+                         const int32_t *sin_q15, uint32_t *acc) {
+  if (!acc || !cos_q15 || !sin_q15 || n_theta < 1 || n_edges < 0 ||
+      (n_edges > 0 && !edges))
+    return LDO_EARG;
+  int32_t d = ldo_rho_offset(width, height);
+  if (d < 0) return LDO_EARG;
+  int64_t n_rho = 2 * (int64_t)d + 1;
+  memset(acc, 0, sizeof(uint32_t) * (size_t)n_theta * (size_t)n_rho);
+  for (int64_t e = 0; e < n_edges; e++) {
+    int64_t x = edges[e] & 0xFFFFu;
+    int64_t y = edges[e] >> 16;
+    if (x >= width || y >= height) return LDO_EARG;
+    for (int32_t t = 0; t < n_theta; t++) {
+      /* Eq. 3: r = x cos(theta) + y sin(theta), Q15, rounded half up */
+      int64_t v = x * cos_q15[t] + y * sin_q15[t] + 16384;
+      int64_t rho = floor_div(v, 32768) + d;
+      if (rho < 0 || rho >= n_rho) return LDO_ERANGE;
+      acc[(int64_t)t * n_rho + rho] += 1;
+    }
+  }
+  return LDO_OK;
+}
+
+/* key(a) > key(b) with key = (votes, -theta, -rho) */
+static int key_greater(uint32_t va, int32_t ta, int32_t ra, uint32_t vb,
+                       int32_t tb, int32_t rb) {
+  if (va != vb) return va > vb;
+  if (ta != tb) return ta < tb;
+  return ra < rb;
+}
+
+static int peak_cmp_desc(const void *pa, const void *pb) {
+  const ldo_peak *a = (const ldo_peak *)pa, *b = (const ldo_peak *)pb;
+  if (key_greater(a->votes, a->theta_bin, a->rho_bin, b->votes, b->theta_bin,
+                  b->rho_bin))
+    return -1;
+  if (key_greater(b->votes, b->theta_bin, b->rho_bin, a->votes, a->theta_bin,
+                  a->rho_bin))
+    return 1;
+  return 0;
+}
+
+int ldo_hough_peaks(const uint32_t *acc, int32_t n_theta, int32_t n_rho,
+                    int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                    int32_t k, ldo_peak *peaks, int32_t *n_peaks) {
+  if (!acc || !peaks || !n_peaks || n_theta < 1 || n_rho < 1 ||
+      half_theta < 0 || half_rho < 0 || k < 1)
+    return LDO_EARG;
+  uint32_t floor_votes = min_votes > 1 ? min_votes : 1;
+  int64_t cap = 1024, count = 0;
+  ldo_peak *cand = (ldo_peak *)malloc(sizeof(ldo_peak) * (size_t)cap);
+  if (!cand) return LDO_ENOMEM;
+  for (int32_t t = 0; t < n_theta; t++) {
+    for (int32_t r = 0; r < n_rho; r++) {
+      uint32_t v = acc[(int64_t)t * n_rho + r];
+      if (v < floor_votes) continue;
+      int is_max = 1;
+      /* window N(t, r), clipped to the accumulator, no theta wrap-around */
+      for (int32_t tt = t - half_theta; tt <= t + half_theta && is_max; tt++) {
+        if (tt < 0 || tt >= n_theta) continue;
+        for (int32_t rr = r - half_rho; rr <= r + half_rho; rr++) {
+          if (rr < 0 || rr >= n_rho || (tt == t && rr == r)) continue;
+          uint32_t w = acc[(int64_t)tt * n_rho + rr];
+          if (!key_greater(v, t, r, w, tt, rr)) { is_max = 0; break; }
+        }
+      }
+      if (!is_max) continue;
+      if (count == cap) {
+        cap *= 2;
+        ldo_peak *grown = (ldo_peak *)realloc(cand, sizeof(ldo_peak) * (size_t)cap);
+        if (!grown) { free(cand); return LDO_ENOMEM; }
+        cand = grown;
+      }
+      cand[count].theta_bin = t;
+      cand[count].rho_bin = r;
+      cand[count].votes = v;
+      count++;
+    }
+  }
+  qsort(cand, (size_t)count, sizeof(ldo_peak), peak_cmp_desc);
+  int32_t m = count < k ? (int32_t)count : k;
+  for (int32_t i = 0; i < k; i++) {
+    if (i < m) {
+      peaks[i] = cand[i];
+    } else {
+      peaks[i].theta_bin = -1;
+      peaks[i].rho_bin = -1;
+      peaks[i].votes = 0;
+    }
+  }
+  *n_peaks = m;
+  free(cand);
+  return LDO_OK;
+}
+
+int ldo_detect(const uint8_t *gray, int32_t width, int32_t height, int64_t pitch,
+               int32_t threshold, int32_t n_theta, const int32_t *cos_q15,
+               const int32_t *sin_q15, int32_t half_theta, int32_t half_rho,
+               uint32_t min_votes, int32_t k, uint8_t *binary, uint32_t *edges,
+               int64_t *n_edges, uint32_t *acc, ldo_peak *peaks,
+               int32_t *n_peaks) {
+  if (!gray || !n_edges || !peaks || !n_peaks || width < 1 || height < 1 ||
+      n_theta < 1)
+    return LDO_EARG;
+  int32_t d = ldo_rho_offset(width, height);
+  int64_t n_rho = 2 * (int64_t)d + 1;
+  size_t npx = (size_t)width * (size_t)height;
+  uint8_t *bin = binary ? binary : (uint8_t *)malloc(npx);
+  uint32_t *edg = edges ? edges : (uint32_t *)malloc(sizeof(uint32_t) * npx);
+  uint32_t *ac = acc ? acc : (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n_theta * (size_t)n_rho);
+  int rc = LDO_ENOMEM;
+  if (bin && edg && ac) {
+    rc = ldo_sobel_binarize(gray, width, height, pitch, threshold, bin);
+    if (rc == LDO_OK) rc = ldo_compact(bin, width, height, edg, (int64_t)npx, n_edges);
+    if (rc == LDO_OK)
+      rc = ldo_hough_accumulate(edg, *n_edges, width, height, n_theta, cos_q15,
+                                sin_q15, ac);
+    if (rc == LDO_OK)
+      rc = ldo_hough_peaks(ac, n_theta, (int32_t)n_rho, half_theta, half_rho,
+                           min_votes, k, peaks, n_peaks);
+  }
+  if (!binary) free(bin);
+  if (!edges) free(edg);
+  if (!acc) free(ac);
+  return rc;
+}

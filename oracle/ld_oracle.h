@@ -1,0 +1,111 @@
+/*
+ * ld_oracle.h -- plain, slow, single-threaded CPU oracle of the lane-detection
+ * hot path of Alshemi, Saif & Taher, "Hardware Acceleration of Lane Detection
+ * Algorithm: a GPU versus FPGA Comparison" (arXiv 2212.09460).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load liboracle.so.  The
+ * product path (libld.so and its Python binding) never links, imports or calls
+ * anything in oracle/, and this file includes no header of the product.
+ *
+ * Citations: "P:n" = line n of the paper text (reference PAPER.md);
+ * "S:n" = line n of the CPU-program SPEC.md; "DESIGN R<k>" = reading k of the
+ * paper listed in DESIGN.md section 3.
+ *
+ * Every function is pure: it reads its inputs, writes only its outputs, keeps
+ * no state, allocates only temporary host memory, and returns 0 on success or a
+ * negative LDO_E* code (outputs then undefined).
+ *
+ * Pins: every function here is pinned by tests/test_oracle_pins.py against
+ * hand-computed values, closed forms, library routines and brute force (see
+ * DESIGN.md section 4).  No function is "parity unpinned".
+ */
+#ifndef LD_ORACLE_H
+#define LD_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LDO_OK 0
+#define LDO_EARG (-1)   /* invalid argument                              */
+#define LDO_ERANGE (-2) /* a vote fell outside [0, n_rho) (table too big) */
+#define LDO_ECAP (-3)   /* output capacity too small                     */
+#define LDO_ENOMEM (-4) /* host malloc failed                            */
+
+typedef struct {
+  int32_t theta_bin; /* t in [0, n_theta)                       */
+  int32_t rho_bin;   /* r in [0, n_rho); signed rho = r - D     */
+  uint32_t votes;    /* acc[t][r]                               */
+} ldo_peak;
+
+/* D = ceil(sqrt(W^2 + H^2)), found as the smallest integer D >= 0 with
+ * D*D >= W*W + H*H by counting up (no floating point).  n_rho = 2D + 1.
+ * DESIGN R10.  Returns -1 for W < 1 or H < 1. */
+int32_t ldo_rho_offset(int32_t width, int32_t height);
+
+/* Eq. 1 with the Fig. 2 kernels as correlation weights
+ * (row 0 of each kernel multiplies image row y-1; DESIGN R1):
+ *   Gx = sum_ij Sx[i][j] * I[y-1+i][x-1+j],  Gy likewise with Sy,
+ *   mag[y][x] = |Gx| + |Gy|                      for interior pixels,
+ *   mag[y][x] = 0  for x in {0, W-1} or y in {0, H-1} (border, DESIGN R2).
+ * gray: [height][pitch] bytes, pitch >= width.  mag: [height][width] int32. */
+int ldo_sobel_magnitude(const uint8_t *gray, int32_t width, int32_t height,
+                        int64_t pitch, int32_t *mag);
+
+/* Sobel magnitude then binarization:
+ *   binary[y][x] = 255 if (interior and |Gx|+|Gy| >= threshold) else 0.
+ * The comparison is ">=" on the raw integer magnitude (DESIGN R3, R4).
+ * binary: [height][width] bytes. */
+int ldo_sobel_binarize(const uint8_t *gray, int32_t width, int32_t height,
+                       int64_t pitch, int32_t threshold, uint8_t *binary);
+
+/* Edge-coordinate list ("threads read the coordinates of input pixels
+ * stored in the global memory"): raster scan (y-major, then x) of binary
+ * [height][width]; appends (y << 16) | x for every pixel equal to 255.
+ * Writes *n_edges.  Returns LDO_ECAP if more than cap edges. */
+int ldo_compact(const uint8_t *binary, int32_t width, int32_t height,
+                uint32_t *edges, int64_t cap, int64_t *n_edges);
+
+/* Hough voting (Eq. 3; DESIGN R8, R9, R11, R12).
+ * acc[n_theta][n_rho] (n_rho = 2D+1) is zeroed, then for every edge (x, y)
+ * and every t in [0, n_theta):
+ *   v   = x*C[t] + y*S[t] + 2^14           (64-bit integer)
+ *   rho = floor(v / 2^15) + D              (explicit floor division)
+ *   acc[t][rho] += 1
+ * i.e. rho - D is r = x cos(theta_t) + y sin(theta_t) in Q15 rounded half up.
+ * Returns LDO_ERANGE (acc undefined) if any rho leaves [0, n_rho). */
+int ldo_hough_accumulate(const uint32_t *edges, int64_t n_edges, int32_t width,
+                         int32_t height, int32_t n_theta, const int32_t *cos_q15,
+                         const int32_t *sin_q15, uint32_t *acc);
+
+/* Hough peaks ("picking the line with the most pixel value"; P:185;
+ * DESIGN R13, R14).  key(t, r) = (acc[t][r], -t, -r), compared
+ * lexicographically.  (t, r) is a candidate iff
+ *   acc[t][r] >= max(1, min_votes)  and
+ *   key(t, r) > key(t', r') for every other (t', r') with |t'-t| <= half_theta,
+ *   |r'-r| <= half_rho, inside the accumulator (no theta wrap-around).
+ * Candidates are sorted by key, descending; the first min(k, #candidates) are
+ * written to peaks[0..), the rest of peaks[0..k) is {-1, -1, 0}.
+ * *n_peaks = min(k, #candidates). */
+int ldo_hough_peaks(const uint32_t *acc, int32_t n_theta, int32_t n_rho,
+                    int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                    int32_t k, ldo_peak *peaks, int32_t *n_peaks);
+
+/* The whole per-frame pipeline (Fig. 1 steps 1-3 plus the peak step):
+ * sobel_binarize -> compact -> hough_accumulate -> hough_peaks.
+ * binary (nullable) [height][width]; acc (nullable) [n_theta][2D+1];
+ * edges (nullable) [width*height], raster order; n_edges required. */
+int ldo_detect(const uint8_t *gray, int32_t width, int32_t height, int64_t pitch,
+               int32_t threshold, int32_t n_theta, const int32_t *cos_q15,
+               const int32_t *sin_q15, int32_t half_theta, int32_t half_rho,
+               uint32_t min_votes, int32_t k, uint8_t *binary, uint32_t *edges,
+               int64_t *n_edges, uint32_t *acc, ldo_peak *peaks,
+               int32_t *n_peaks);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LD_ORACLE_H */

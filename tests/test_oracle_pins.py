@@ -1,0 +1,359 @@
+"""Pins of the CPU oracle against values the paper and mathematics fix (CPU only).
+
+Each test pins one oracle function to something other than itself: a
+hand-computed value (tests/golden, each with its citation), a closed form, a
+library routine (scipy / numpy), exact rational arithmetic, an invariant, or
+brute force on tiny inputs.  DESIGN.md section 4 maps every pin to the paper.
+"""
+from fractions import Fraction
+import itertools
+import math
+
+import numpy as np
+import pytest
+from scipy import signal
+
+from conftest import load_golden
+from paper_2212_09460_b200 import synth
+
+SX = np.array([[-1, 0, 1], [-2, 0, 2], [-1, 0, 1]])   # Fig. 2
+SY = np.array([[1, 2, 1], [0, 0, 0], [-1, -2, -1]])
+
+
+# ----------------------------------------------------------------------------
+# Geometry (DESIGN R10)
+# ----------------------------------------------------------------------------
+def test_rho_offset_golden(oracle):
+    g = load_golden("geometry_pins.json")
+    for case in g["rho_offset"]:
+        assert oracle.rho_offset(case["w"], case["h"]) == case["D"], case
+    for case in g["acc_bytes"]:
+        d = oracle.rho_offset(case["w"], case["h"])
+        assert case["n_theta"] * (2 * d + 1) * 4 == case["bytes"], case
+
+
+def test_rho_offset_is_ceil_sqrt(oracle):
+    # math.isqrt is an exact library integer square root
+    rng = np.random.default_rng(5)
+    for w, h in list(rng.integers(1, 16385, size=(300, 2))) + [(1, 1), (16384, 16384)]:
+        s = int(w) ** 2 + int(h) ** 2
+        r = math.isqrt(s)
+        want = r if r * r == s else r + 1
+        assert oracle.rho_offset(int(w), int(h)) == want
+
+
+# ----------------------------------------------------------------------------
+# Sobel + binarize (Eq. 1, Fig. 2; DESIGN R1-R4)
+# ----------------------------------------------------------------------------
+def test_sobel_hand_computed_centres(oracle):
+    g = load_golden("sobel_pins.json")
+    for case in g["center_cases"]:
+        img = np.array(case["image"], np.uint8)
+        assert oracle.sobel_magnitude(img)[1, 1] == case["center"], case["cite"]
+
+
+def test_sobel_step_and_ramp(oracle):
+    g = load_golden("sobel_pins.json")
+    st = g["step_4x6"]
+    img = np.array(st["image"], np.uint8)
+    mag = oracle.sobel_magnitude(img)
+    assert mag[1:-1, 1:-1].tolist() == st["magnitude_interior"]
+    b = oracle.sobel_binarize(img, st["threshold"])
+    assert int((b == 255).sum()) == st["edges"]
+    rp = g["ramp_4x5"]
+    img = np.array(rp["image"], np.uint8)
+    assert oracle.sobel_magnitude(img)[1:-1, 1:-1].tolist() == rp["magnitude_interior"]
+    for t, e in rp["thresholds"]:
+        assert int((oracle.sobel_binarize(img, t) == 255).sum()) == e
+
+
+def test_sobel_maximum_is_1530_and_threshold_edges(oracle):
+    img = np.array([[0, 255, 255], [0, 0, 255], [0, 0, 0]], np.uint8)
+    assert oracle.sobel_binarize(img, 1530)[1, 1] == 255
+    assert oracle.sobel_binarize(img, 1531)[1, 1] == 0
+
+
+def test_sobel_matches_scipy_correlate(oracle):
+    # Library routine: scipy 2-D correlation ('valid' = interior) with Fig. 2.
+    for seed, (h, w) in enumerate([(3, 3), (7, 11), (40, 33), (64, 64)]):
+        img = synth.random_image(seed, w, h)
+        gx = signal.correlate2d(img.astype(np.int64), SX, mode="valid")
+        gy = signal.correlate2d(img.astype(np.int64), SY, mode="valid")
+        mag = oracle.sobel_magnitude(img)
+        assert np.array_equal(mag[1:-1, 1:-1], np.abs(gx) + np.abs(gy))
+        # convolution (180-degree flipped kernels) gives the same |G| (DESIGN R1)
+        cx = signal.convolve2d(img.astype(np.int64), SX, mode="valid")
+        cy = signal.convolve2d(img.astype(np.int64), SY, mode="valid")
+        assert np.array_equal(mag[1:-1, 1:-1], np.abs(cx) + np.abs(cy))
+
+
+def test_sobel_exhaustive_binary_patches(oracle):
+    # every {0,255}^9 patch: |G| even, <= 1530, max attained; matches the literal sum
+    mags = []
+    for bits in range(512):
+        p = np.array([(bits >> i) & 1 for i in range(9)], np.int64).reshape(3, 3) * 255
+        m = int(oracle.sobel_magnitude(p.astype(np.uint8))[1, 1])
+        assert m == abs(int((SX * p).sum())) + abs(int((SY * p).sum()))
+        mags.append(m)
+    assert max(mags) == 1530 and all(m % 2 == 0 for m in mags)
+
+
+def test_sobel_border_and_tiny_images(oracle):
+    for h, w in [(1, 1), (1, 7), (2, 2), (2, 9), (9, 2), (3, 3), (5, 4)]:
+        img = synth.random_image(h * 31 + w, w, h, "binary")
+        b = oracle.sobel_binarize(img, 0)
+        assert b[0, :].max(initial=0) == 0 and b[-1, :].max(initial=0) == 0
+        assert b[:, 0].max(initial=0) == 0 and b[:, -1].max(initial=0) == 0
+        # T <= 0: every interior pixel is an edge
+        assert int((b == 255).sum()) == max(h - 2, 0) * max(w - 2, 0)
+
+
+def test_sobel_flip_invariance_and_monotone_threshold(oracle):
+    img = synth.random_image(11, 37, 29)
+    base = oracle.sobel_binarize(img, 200)
+    assert np.array_equal(oracle.sobel_binarize(img[:, ::-1], 200), base[:, ::-1])
+    assert np.array_equal(oracle.sobel_binarize(img[::-1, :], 200), base[::-1, :])
+    sq = synth.random_image(12, 31, 31)
+    assert np.array_equal(oracle.sobel_binarize(sq.T, 150), oracle.sobel_binarize(sq, 150).T)
+    counts = [int((oracle.sobel_binarize(img, t) == 255).sum()) for t in range(0, 1600, 97)]
+    assert all(a >= b for a, b in zip(counts, counts[1:]))
+
+
+def test_constant_image_has_no_edges(oracle):
+    for v in (0, 77, 255):
+        img = np.full((13, 17), v, np.uint8)
+        assert (oracle.sobel_binarize(img, 1) == 0).all()
+
+
+# ----------------------------------------------------------------------------
+# Compaction
+# ----------------------------------------------------------------------------
+def test_compact_matches_numpy_nonzero(oracle):
+    for seed, (h, w) in enumerate([(1, 1), (5, 9), (33, 70)]):
+        b = synth.random_image(seed, w, h, "binary")
+        ys, xs = np.nonzero(b == 255)  # library: row-major order
+        want = (ys.astype(np.uint32) << 16) | xs.astype(np.uint32)
+        assert np.array_equal(oracle.compact(b), want)
+
+
+# ----------------------------------------------------------------------------
+# Trig table input pins (the table is an input, DESIGN R11)
+# ----------------------------------------------------------------------------
+def test_q15_table_pins():
+    g = load_golden("hough_pins.json")
+    for case in g["q15"]:
+        n = case["n_theta"]
+        c, s = synth.q15_table(n)
+        assert c[0] == case["C0"] and s[n // 2] == case["S_half"] and c[n // 2] == case["C_half"]
+        assert c[n // 4] == case["C_quarter"] and s[n // 4] == case["S_quarter"]
+        for t in range(1, n):  # Eq. 4-5 hold exactly
+            assert s[t] == s[n - t] and c[t] == -c[n - t]
+        th = np.pi * np.arange(n) / n
+        assert np.abs(c - 32768 * np.cos(th)).max() <= 0.5
+        assert np.abs(s - 32768 * np.sin(th)).max() <= 0.5
+
+
+# ----------------------------------------------------------------------------
+# Hough voting (Eq. 3; DESIGN R8-R12)
+# ----------------------------------------------------------------------------
+def _round_half_up(fr: Fraction) -> int:
+    return math.floor(fr + Fraction(1, 2))
+
+
+@pytest.mark.parametrize("n_theta", [1, 2, 3, 8, 180, 181, 720, 1024])
+def test_single_pixel_exact_rational(oracle, n_theta):
+    # One pixel votes once per theta at round_half_up((x C + y S) / 2^15) + D,
+    # computed with exact rationals (no shifts, no floor_div).
+    c, s = synth.q15_table(n_theta)
+    w, h = 97, 61
+    d = oracle.rho_offset(w, h)
+    rng = np.random.default_rng(n_theta)
+    pts = [(0, 0), (w - 1, h - 1), (w - 1, 0), (0, h - 1)] + \
+        [tuple(map(int, p)) for p in zip(rng.integers(0, w, 6), rng.integers(0, h, 6))]
+    for x, y in pts:
+        acc = oracle.hough_accumulate(np.array([(y << 16) | x], np.uint32), w, h, c, s)
+        assert int(acc.sum()) == n_theta
+        for t in range(n_theta):
+            r = _round_half_up(Fraction(x * int(c[t]) + y * int(s[t]), 32768))
+            assert acc[t, r + d] == 1
+            # Eq. 3 error bound: |r - (x cos + y sin)| <= 1/2 + (x + y) / 2^16
+            true_r = x * math.cos(math.pi * t / n_theta) + y * math.sin(math.pi * t / n_theta)
+            assert abs(r - true_r) <= 0.5 + (x + y) / 65536.0 + 1e-9
+
+
+def test_origin_votes_at_D(oracle):
+    c, s = synth.q15_table(180)
+    acc = oracle.hough_accumulate(np.array([0], np.uint32), 320, 240, c, s)
+    assert (acc[:, 400] == 1).all() and int(acc.sum()) == 180
+
+
+def test_rho_of_spec_examples(oracle):
+    c, s = synth.q15_table(180)
+    d = 400
+    acc = oracle.hough_accumulate(np.array([(7 << 16) | 10], np.uint32), 320, 240, c, s)
+    assert acc[0, d + 10] == 1   # (10, y, theta=0) -> D + 10
+    assert acc[90, d + 7] == 1   # (x, 7, theta=90) -> D + 7
+
+
+def test_vote_conservation(oracle):
+    for n_theta in (1, 7, 180, 720):
+        c, s = synth.q15_table(n_theta)
+        b = synth.random_image(n_theta, 50, 40, "binary")
+        e = oracle.compact(b)
+        acc = oracle.hough_accumulate(e, 50, 40, c, s)
+        assert int(acc.sum()) == len(e) * n_theta
+        assert (acc.sum(axis=1) == len(e)).all()
+
+
+@pytest.mark.parametrize("n_theta", [180, 720, 1024])
+def test_lines_closed_forms(oracle, n_theta):
+    g = load_golden("hough_pins.json")
+    c, s = synth.q15_table(n_theta)
+    w, h = 400, 300
+    d = oracle.rho_offset(w, h)
+    # horizontal line of N pixels at y0: acc[n/2][D + y0] = N = max(acc)
+    y0, n = 123, w
+    e = np.array([(y0 << 16) | x for x in range(n)], np.uint32)
+    acc = oracle.hough_accumulate(e, w, h, c, s)
+    assert acc[n_theta // 2, d + y0] == n and acc.max() == n
+    # vertical line at x0: acc[0][D + x0] = N
+    x0 = 77
+    e = np.array([(y << 16) | x0 for y in range(h)], np.uint32)
+    acc = oracle.hough_accumulate(e, w, h, c, s)
+    assert acc[0, d + x0] == h and acc.max() == h
+    # x + y = 200 at theta = 45 deg; x - y = 100 at theta = 135 deg
+    dg = g["diagonal_x_plus_y"]
+    e = np.array([((dg["c"] - x) << 16) | x for x in range(dg["c"] + 1)], np.uint32)
+    acc = oracle.hough_accumulate(e, w, h, c, s)
+    assert acc[n_theta // 4, d + dg["rho_minus_D"]] == dg["c"] + 1
+    ad = g["antidiagonal_x_minus_y"]
+    e = np.array([(y << 16) | (y + ad["c"]) for y in range(h) if y + ad["c"] < w], np.uint32)
+    acc = oracle.hough_accumulate(e, w, h, c, s)
+    assert acc[3 * n_theta // 4, d + ad["rho_minus_D"]] == len(e)
+
+
+def test_exhaustive_4x4_subsets_additivity(oracle):
+    # Brute force: all 2^16 subsets of a 4x4 patch at an offset; each accumulator
+    # equals the sum of its pixels' single-pixel accumulators (pinned above).
+    c, s = synth.q15_table(8)
+    w, h, ox, oy = 16, 16, 5, 9
+    pix = [((oy + i // 4) << 16) | (ox + i % 4) for i in range(16)]
+    singles = np.stack([oracle.hough_accumulate(np.array([p], np.uint32), w, h, c, s).ravel()
+                        for p in pix]).astype(np.int64)
+    masks = ((np.arange(1 << 16)[:, None] >> np.arange(16)[None, :]) & 1).astype(np.int64)
+    want = masks @ singles
+    for m in range(1 << 16):
+        e = np.array([pix[i] for i in range(16) if (m >> i) & 1], np.uint32)
+        acc = oracle.hough_accumulate(e, w, h, c, s)
+        assert np.array_equal(acc.ravel(), want[m])
+
+
+def test_range_error_on_oversized_table(oracle):
+    c = np.array([65536], np.int32)   # |C| > 2^15 pushes rho out of [0, n_rho)
+    s = np.array([0], np.int32)
+    with pytest.raises(oracle.OracleError):
+        oracle.hough_accumulate(np.array([(0 << 16) | 9], np.uint32), 10, 1, c, s)
+
+
+# ----------------------------------------------------------------------------
+# Peaks (DESIGN R13, R14)
+# ----------------------------------------------------------------------------
+def _brute_peaks(acc, ht, hr, min_votes, k):
+    n_t, n_r = acc.shape
+    cands = []
+    for t in range(n_t):
+        for r in range(n_r):
+            v = int(acc[t, r])
+            if v < max(1, min_votes):
+                continue
+            win = [(int(acc[tt, rr]), -tt, -rr)
+                   for tt in range(max(0, t - ht), min(n_t, t + ht + 1))
+                   for rr in range(max(0, r - hr), min(n_r, r + hr + 1))]
+            if max(win) == (v, -t, -r):
+                cands.append((v, -t, -r))
+    cands.sort(reverse=True)
+    out = [(-tt, -rr, v) for v, tt, rr in cands[:k]]
+    return out + [(-1, -1, 0)] * (k - len(out)), min(k, len(cands))
+
+
+def _as_tuples(peaks):
+    return [(int(p["theta_bin"]), int(p["rho_bin"]), int(p["votes"])) for p in peaks]
+
+
+def test_peaks_brute_force_random(oracle):
+    rng = np.random.default_rng(3)
+    for trial in range(60):
+        n_t, n_r = int(rng.integers(1, 12)), int(rng.integers(1, 30))
+        acc = rng.integers(0, int(rng.integers(1, 6)), size=(n_t, n_r)).astype(np.uint32)
+        ht, hr = int(rng.integers(0, 4)), int(rng.integers(0, 6))
+        mv, k = int(rng.integers(0, 4)), int(rng.integers(1, 9))
+        got, n = oracle.hough_peaks(acc, ht, hr, mv, k)
+        want, wn = _brute_peaks(acc, ht, hr, mv, k)
+        assert n == wn and _as_tuples(got) == want, (trial, acc, ht, hr, mv, k)
+
+
+def test_peaks_window_zero_is_sort(oracle):
+    rng = np.random.default_rng(4)
+    acc = rng.integers(0, 4, size=(6, 9)).astype(np.uint32)
+    got, n = oracle.hough_peaks(acc, 0, 0, 1, 100)
+    t, r = np.nonzero(acc)
+    order = sorted(zip(acc[t, r].tolist(), (-t).tolist(), (-r).tolist()), reverse=True)
+    assert n == len(order)
+    assert _as_tuples(got)[:n] == [(-a, -b, v) for v, a, b in order]
+
+
+def test_peaks_special_cases(oracle):
+    acc = np.zeros((10, 20), np.uint32)
+    got, n = oracle.hough_peaks(acc, 2, 3, 1, 4)
+    assert n == 0 and _as_tuples(got) == [(-1, -1, 0)] * 4          # all-zero
+    acc[4, 7] = 9
+    got, n = oracle.hough_peaks(acc, 2, 3, 1, 4)
+    assert n == 1 and _as_tuples(got)[0] == (4, 7, 9)
+    acc[8, 15] = 9   # equal maxima farther apart than the window -> lower theta first
+    got, n = oracle.hough_peaks(acc, 2, 3, 1, 4)
+    assert n == 2 and _as_tuples(got)[:2] == [(4, 7, 9), (8, 15, 9)]
+    acc[5, 8] = 9    # tie inside the window: the lower (theta, rho) wins
+    got, n = oracle.hough_peaks(acc, 2, 3, 1, 4)
+    assert _as_tuples(got)[:2] == [(4, 7, 9), (8, 15, 9)] and n == 2
+    got, n = oracle.hough_peaks(acc, 2, 3, 10, 4)                   # min_votes
+    assert n == 0
+
+
+def test_peaks_no_theta_wraparound(oracle):
+    acc = np.zeros((10, 5), np.uint32)
+    acc[0, 2] = 5
+    acc[9, 2] = 7
+    got, n = oracle.hough_peaks(acc, 2, 1, 1, 4)
+    assert n == 2 and _as_tuples(got)[:2] == [(9, 2, 7), (0, 2, 5)]
+
+
+# ----------------------------------------------------------------------------
+# End to end: planted lanes (S:527 generalised; BASELINE.json configs[0])
+# ----------------------------------------------------------------------------
+def test_cfg1_planted_lanes_recovered(oracle):
+    cfg = synth.CONFIGS["cfg1"]
+    img = synth.gen_frame("cfg1", 0)
+    c, s = synth.q15_table(cfg.n_theta)
+    r = oracle.detect(img, cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+                      cfg.min_votes, cfg.k)
+    d = oracle.rho_offset(cfg.width, cfg.height)
+    assert r["n_peaks"] == 2
+    found = sorted((int(p["theta_bin"]), int(p["rho_bin"]) - d) for p in r["peaks"])
+    lanes = sorted((l["theta_deg"], l["r"]) for l in
+                   load_golden("hough_pins.json")["cfg1_lanes"]["lanes"])
+    for (t, rho), (th, rr) in zip(found, lanes):
+        assert abs(t - th) <= 1.0 and abs(rho - rr) <= 3.5, (found, lanes)
+    assert int(r["acc"].sum()) == r["n_edges"] * cfg.n_theta
+    assert np.array_equal(r["binary"], oracle.sobel_binarize(img, cfg.threshold))
+
+
+def test_detect_composes_stages(oracle):
+    img = synth.gen_frame("cfg1", 0)
+    c, s = synth.q15_table(180)
+    r = oracle.detect(img, 200, c, s, 2, 8, 1, 5)
+    b = oracle.sobel_binarize(img, 200)
+    e = oracle.compact(b)
+    acc = oracle.hough_accumulate(e, 320, 240, c, s)
+    pk, n = oracle.hough_peaks(acc, 2, 8, 1, 5)
+    assert np.array_equal(r["edges"], e) and np.array_equal(r["acc"], acc)
+    assert _as_tuples(r["peaks"]) == _as_tuples(pk) and r["n_peaks"] == n
