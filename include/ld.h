@@ -1,0 +1,207 @@
+/*
+ * ld.h -- C ABI of libld.so, the B200-native (sm_100a) lane-detection hot path
+ * of Alshemi, Saif & Taher, "Hardware Acceleration of Lane Detection
+ * Algorithm: a GPU versus FPGA Comparison" (arXiv 2212.09460).
+ *
+ * The paper's problem statement (Fig. 1): gray 8-bit image -> Sobel
+ * edge detection (Step 1) -> binarization (Step 2) -> Hough matrix (Step 3) ->
+ * Hough peaks (Step 4, done in MATLAB in the paper).
+ * Citations: "P:n" = line n of the paper text; "DESIGN R<k>" = the k-th
+ * reading of the paper listed in DESIGN.md section 3.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All functions are extern "C", never throw, never allocate device memory,
+ *    never synchronize the device or the stream.  `stream` is a cudaStream_t
+ *    (passed as void*; NULL = legacy default stream).  Work is enqueued on it;
+ *    results are valid once the stream reaches that point.  Inputs must stay
+ *    unmodified until then.
+ *  - Device pointers: every buffer argument is a DEVICE pointer owned by the
+ *    caller, except the trig tables (HOST pointers, copied by value into the
+ *    launch) and the ld_image descriptor (HOST).  The *_host entry point is
+ *    the only one taking host image/peak buffers.
+ *  - Outputs are fully overwritten (accumulators zeroed, unused peak slots set
+ *    to the sentinel {-1, -1, 0}).
+ *  - Validation happens on the host before any launch, so an error status has
+ *    no side effect on any output.  On error, ld_last_error_detail() returns a
+ *    thread-local one-line explanation.  A failed CUDA call returns
+ *    LD_ERR_CUDA and outputs are then undefined.
+ *  - Coordinates: origin top-left, x = column, y = row (DESIGN R7).  An edge is
+ *    packed as (y << 16) | x in global image coordinates.
+ *  - Geometry: D = ceil(sqrt(W^2 + H^2)) (integer), n_rho = 2D + 1 (R10);
+ *    theta_t = pi * t / n_theta, t in [0, n_theta) (R8).
+ *  - All arithmetic is integer; every output is bit-exact against the oracle.
+ */
+#ifndef LD_H
+#define LD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LD_MAX_DIM 16384   /* W, H <= 16384: x, y fit in 16 bits; rho fits in int32 */
+#define LD_MAX_THETA 2048  /* trig tables are passed by value (2 x 8 KB)           */
+#define LD_MAX_K 1024      /* peaks per frame                                       */
+
+typedef enum {
+  LD_OK = 0,
+  LD_ERR_INVALID_ARG = 1, /* null pointer, bad size, misaligned pitch/stride       */
+  LD_ERR_RANGE = 2,       /* trig table would put a vote outside [0, n_rho)       */
+  LD_ERR_WORKSPACE = 3,   /* workspace too small or misaligned                    */
+  LD_ERR_UNSUPPORTED = 4, /* not an sm_100 device, or shared memory too small     */
+  LD_ERR_CUDA = 5         /* a CUDA call or launch failed                         */
+} ld_status;
+
+/* One Hough peak: signed rho = rho_bin - D.  Sentinel: {-1, -1, 0}. */
+typedef struct {
+  int32_t theta_bin;
+  int32_t rho_bin;
+  uint32_t votes;
+} ld_peak;
+
+/* A batch of 8-bit gray frames, row-major [batch][rows][pitch] ("a pixel
+ * is normally represented by 8 unsigned bits").
+ *  width, height : FULL image size; they fix the border, D and coordinates.
+ *  pitch         : bytes between rows, >= width, multiple of 16.
+ *  frame_stride  : bytes between frames, multiple of 16, >= rows * pitch.
+ *  batch         : number of frames, >= 1.
+ *  row_begin/end : rows owned by this call, 0 <= row_begin < row_end <= height;
+ *                  [0, height) for whole frames, a band for row-banded
+ *                  multi-GPU runs.  The gray pointer then addresses global row
+ *                  max(row_begin - 1, 0) of frame 0, and rows up to
+ *                  min(row_end + 1, height) - 1 must be readable (1-row halo). */
+typedef struct {
+  int32_t width;
+  int32_t height;
+  int64_t pitch;
+  int64_t frame_stride;
+  int32_t batch;
+  int32_t row_begin;
+  int32_t row_end;
+} ld_image;
+
+/* D = ceil(sqrt(W^2 + H^2)) by exact integer square root; -1 if W or H < 1. */
+int32_t ld_rho_offset(int32_t width, int32_t height);
+
+/* Steps 1-2 (Eq. 1, Fig. 2; GPU design P:155-169), fused with edge
+ * compaction ("threads read the coordinates of input pixels stored in
+ * the global memory").  For each owned pixel (x, y):
+ *   out = 255 if 1 <= x <= W-2, 1 <= y <= H-2 and |Gx| + |Gy| >= threshold,
+ *   out = 0   otherwise (1-px border forced to 0, DESIGN R2; ">=" R4).
+ *  threshold   : any int32; <= 0 marks every interior pixel, >= 1531 none.
+ *  binary      : nullable. [batch][row_end-row_begin][img->pitch] bytes, output
+ *                row i = global row row_begin + i; bytes x >= width are 0.
+ *  edge_xy     : nullable. [batch][edge_stride] uint32; frame f's edges are
+ *                edge_xy[f*edge_stride + 0 .. edge_count[f]) in UNSPECIFIED
+ *                order (a set; DESIGN R15).
+ *  edge_stride : >= (row_end-row_begin) * max(width-2, 0) when edge_xy != NULL,
+ *                so the list can never overflow.
+ *  edge_count  : required. [batch] uint32, overwritten with the edge count.
+ * Staging: TMA 2-D tiles with a 1-px halo, persistent CTAs, mbarrier ring. */
+int ld_sobel_binarize(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                      uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
+                      uint32_t *edge_count, void *stream);
+
+/* Step 3 (Eq. 3; GPU design P:171-175): theta-partitioned voting.
+ * acc[f][t][r] = #{ edges e of frame f : ((x*C[t] + y*S[t] + 2^14) >> 15) + D == r }
+ * (arithmetic shift = floor; i.e. r - D = round-half-up of x cos + y sin in
+ * Q15, DESIGN R9).
+ *  edge_xy, edge_count, edge_stride : as produced by ld_sobel_binarize
+ *                (DEVICE counts; no host synchronisation is needed).
+ *  width, height : full image size (fixes D and n_rho; coordinates must lie
+ *                inside it -- true for lists produced by ld_sobel_binarize).
+ *  cos_q15, sin_q15 : HOST int32[n_theta], |value| <= 32768, caller supplied
+ *                (R11).  Validated: for every t the rho bins of the four image
+ *                corners must lie in [0, n_rho), which proves every vote is in
+ *                range (rho is linear in x, y and floor is monotone); else
+ *                LD_ERR_RANGE.
+ *  acc         : [batch][n_theta][n_rho] uint32, fully overwritten.
+ * No global atomics: each CTA owns a theta band of the accumulator in shared
+ * memory and writes it out with plain coalesced stores. */
+int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count,
+                        int64_t edge_stride, int32_t batch, int32_t width,
+                        int32_t height, int32_t n_theta, const int32_t *cos_q15,
+                        const int32_t *sin_q15, uint32_t *acc, void *stream);
+
+/* Step 4 ("picking the line with the most pixel value"), made
+ * deterministic (DESIGN R13, R14): key(t, r) = (acc[t][r], -t, -r),
+ * lexicographic.  (t, r) is a peak candidate iff acc[t][r] >= max(1, min_votes)
+ * and its key exceeds every other key in the window |t'-t| <= half_theta,
+ * |r'-r| <= half_rho clipped to the accumulator (no theta wrap-around).
+ * peaks[f][0..k) = the min(k, #candidates) largest keys, descending, then the
+ * sentinel; n_peaks[f] = min(k, #candidates).
+ *  acc       : [batch][n_theta][n_rho] uint32 (device).
+ *  k         : 1..LD_MAX_K.   half_theta, half_rho >= 0.
+ *  workspace : device, >= ld_hough_peaks_workspace_bytes(...), 16-B aligned. */
+size_t ld_hough_peaks_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_rho,
+                                      int32_t k);
+int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                   int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                   ld_peak *peaks, int32_t *n_peaks, void *workspace,
+                   size_t workspace_bytes, void *stream);
+
+/* Steps 1-4 for a batch of whole frames (img->row_begin = 0, row_end = height):
+ * ld_sobel_binarize (no binary map) -> ld_hough_accumulate -> ld_hough_peaks,
+ * stream-ordered, no host synchronisation.
+ *  peaks [batch][k], n_peaks [batch]  : required outputs (device).
+ *  edge_count [batch]                 : nullable output (device).
+ *  acc [batch][n_theta][n_rho]        : nullable; when given the accumulators
+ *                                       are exported there, else they live in
+ *                                       the workspace.
+ *  workspace : device, >= ld_detect_workspace_bytes(img, n_theta, k, acc==NULL). */
+size_t ld_detect_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k,
+                                 int32_t acc_in_workspace);
+int ld_detect_batch(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                    int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
+                    int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                    int32_t k, ld_peak *peaks, int32_t *n_peaks, uint32_t *edge_count,
+                    uint32_t *acc, void *workspace, size_t workspace_bytes,
+                    void *stream);
+
+/* ld_detect_batch from HOST buffers: gray_host [batch][height][pitch] (pinned
+ * host memory for overlap), peaks_host [batch][k], n_peaks_host [batch],
+ * edge_count_host [batch] (nullable).  Frames are processed in chunks of
+ * chunk_frames: the H2D copy of chunk i+1 overlaps the kernels of chunk i; the
+ * D2H copy of peaks/counts is enqueued on `stream`.  Synchronises `stream`
+ * before returning (host outputs are valid on return).
+ *  workspace : device, >= ld_detect_host_workspace_bytes(img, n_theta, k,
+ *              chunk_frames). */
+size_t ld_detect_host_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k,
+                                      int32_t chunk_frames);
+int ld_detect_batch_host(const uint8_t *gray_host, const ld_image *img,
+                         int32_t threshold, int32_t n_theta, const int32_t *cos_q15,
+                         const int32_t *sin_q15, int32_t half_theta, int32_t half_rho,
+                         uint32_t min_votes, int32_t k, ld_peak *peaks_host,
+                         int32_t *n_peaks_host, uint32_t *edge_count_host,
+                         int32_t chunk_frames, void *workspace, size_t workspace_bytes,
+                         void *stream);
+
+/* B5 microbenchmark of the shared-memory atomic pipe (the roofline of the
+ * voting stage).  Launches one CTA per SM x blocks_per_sm, each thread issuing
+ * `iters` red.shared.add.u32 with the given address pattern:
+ *   mode 0: conflict-free (lane l always hits bank l, distinct words)
+ *   mode 1: pseudo-random addresses over a 48 K-word array
+ *   mode 2: one address per warp (fully serialised)
+ * *atomics_out (host) receives the total atomics issued.  scratch: device,
+ * >= 4 * grid * 32 bytes (per-CTA checksums). */
+int ld_bench_smem_atomics(int32_t mode, int32_t iters, int32_t blocks_per_sm,
+                          uint64_t *atomics_out, void *scratch, void *stream);
+
+/* Number of SMs / L2 bytes of the current device (host query, cached). */
+int32_t ld_device_sm_count(void);
+int64_t ld_device_l2_bytes(void);
+
+const char *ld_status_string(int status);
+const char *ld_last_error_detail(void);
+
+/* Kernel launches enqueued by the most recent ld_* call on this host thread
+ * (for the bench's gpu_launches count). */
+int32_t ld_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LD_H */

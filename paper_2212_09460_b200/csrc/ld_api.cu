@@ -1,0 +1,586 @@
+// ld_api.cu -- host side of libld.so: validation, geometry, TMA descriptor
+// encoding, launch configuration, workspace layout and the C ABI of include/ld.h.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "ld_internal.cuh"
+
+namespace ld {
+
+static thread_local char g_err[512] = "";
+static thread_local int g_launches = 0;
+
+void note_launch(int n) { g_launches += n; }
+
+static int fail(int status, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+static int cuda_fail(cudaError_t e, const char *what) {
+  return fail(LD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct DevInfo {
+  bool ok = false;
+  int sm_count = 0;
+  int smem_optin = 0;
+  int64_t l2 = 0;
+  int major = 0, minor = 0;
+};
+
+static std::mutex g_mu;
+static DevInfo g_dev[64];
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int device_info(DevInfo *out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo &d = g_dev[dev & 63];
+  if (!d.ok) {
+    cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    d.l2 = l2;
+    cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    d.ok = true;
+  }
+  *out = d;
+  if (d.major != 10 || d.minor != 0)
+    return fail(LD_ERR_UNSUPPORTED, "device is sm_%d%d; libld.so is built for sm_100a only",
+                d.major, d.minor);
+  return LD_OK;
+}
+
+static int get_encoder() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_encode) return LD_OK;
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return fail(LD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return LD_OK;
+}
+
+static int32_t rho_offset(int32_t w, int32_t h) {
+  if (w < 1 || h < 1) return -1;
+  const int64_t s = static_cast<int64_t>(w) * w + static_cast<int64_t>(h) * h;
+  int64_t r = static_cast<int64_t>(std::sqrt(static_cast<double>(s)));
+  while (r * r < s) ++r;
+  while (r > 0 && (r - 1) * (r - 1) >= s) --r;
+  return static_cast<int32_t>(r);
+}
+
+static bool aligned(const void *p, uintptr_t a) {
+  return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
+}
+
+static int check_image(const uint8_t *gray, const ld_image *img) {
+  if (!img) return fail(LD_ERR_INVALID_ARG, "img is NULL");
+  if (!gray) return fail(LD_ERR_INVALID_ARG, "gray is NULL");
+  if (img->width < 1 || img->height < 1 || img->width > LD_MAX_DIM || img->height > LD_MAX_DIM)
+    return fail(LD_ERR_INVALID_ARG, "width/height %d x %d outside [1, %d]", img->width,
+                img->height, LD_MAX_DIM);
+  if (img->pitch < img->width || img->pitch % 16 != 0)
+    return fail(LD_ERR_INVALID_ARG, "pitch %lld must be >= width and a multiple of 16",
+                static_cast<long long>(img->pitch));
+  if (img->batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
+  if (img->row_begin < 0 || img->row_end > img->height || img->row_begin >= img->row_end)
+    return fail(LD_ERR_INVALID_ARG, "rows [%d, %d) invalid for height %d", img->row_begin,
+                img->row_end, img->height);
+  const int ry0 = img->row_begin > 0 ? img->row_begin - 1 : 0;
+  const int ry1 = img->row_end < img->height ? img->row_end + 1 : img->height;
+  if (img->batch > 1 &&
+      (img->frame_stride % 16 != 0 || img->frame_stride < static_cast<int64_t>(ry1 - ry0) * img->pitch))
+    return fail(LD_ERR_INVALID_ARG, "frame_stride %lld must be a multiple of 16 and >= %lld",
+                static_cast<long long>(img->frame_stride),
+                static_cast<long long>(ry1 - ry0) * img->pitch);
+  if (!aligned(gray, 16)) return fail(LD_ERR_INVALID_ARG, "gray must be 16-byte aligned");
+  return LD_OK;
+}
+
+static int64_t max_edges_per_frame(const ld_image *img) {
+  const int64_t w2 = img->width > 2 ? img->width - 2 : 0;
+  return static_cast<int64_t>(img->row_end - img->row_begin) * w2;
+}
+
+// Range proof (ld.h): |C|,|S| <= 32768 and the corner rho bins are in range.
+static int check_trig(int32_t n_theta, const int32_t *c, const int32_t *s, int32_t w,
+                      int32_t h, int32_t d) {
+  if (n_theta < 1 || n_theta > LD_MAX_THETA)
+    return fail(LD_ERR_INVALID_ARG, "n_theta %d outside [1, %d]", n_theta, LD_MAX_THETA);
+  if (!c || !s) return fail(LD_ERR_INVALID_ARG, "trig table pointer is NULL");
+  const int64_t n_rho = 2 * static_cast<int64_t>(d) + 1;
+  const int64_t xs[2] = {0, w - 1}, ys[2] = {0, h - 1};
+  for (int t = 0; t < n_theta; ++t) {
+    if (c[t] < -32768 || c[t] > 32768 || s[t] < -32768 || s[t] > 32768)
+      return fail(LD_ERR_RANGE, "trig entry %d (%d, %d) exceeds |32768|", t, c[t], s[t]);
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        const int64_t v = xs[a] * c[t] + ys[b] * s[t] + 16384 + (static_cast<int64_t>(d) << 15);
+        const int64_t rho = v >> 15;  // v >= 0 is required too (floor of a negative)
+        if (v < 0 || rho < 0 || rho >= n_rho)
+          return fail(LD_ERR_RANGE, "theta bin %d sends corner (%lld, %lld) to rho bin %lld",
+                      t, static_cast<long long>(xs[a]), static_cast<long long>(ys[b]),
+                      static_cast<long long>(rho));
+      }
+  }
+  return LD_OK;
+}
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                      uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
+                      uint32_t *edge_count, cudaStream_t stream) {
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  if ((rc = get_encoder())) return rc;
+
+  const int W = img->width, H = img->height;
+  const int ry0 = img->row_begin > 0 ? img->row_begin - 1 : 0;
+  const int ry1 = img->row_end < H ? img->row_end + 1 : H;
+  const int rows_read = ry1 - ry0;
+  const int64_t fstride = img->batch > 1 ? img->frame_stride
+                                         : static_cast<int64_t>(rows_read) * img->pitch;
+
+  CUtensorMap tmap;
+  cuuint64_t gdim[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(rows_read),
+                        static_cast<cuuint64_t>(img->batch)};
+  cuuint64_t gstride[2] = {static_cast<cuuint64_t>(img->pitch), static_cast<cuuint64_t>(fstride)};
+  cuuint32_t box[3] = {SB_BOX_W, SB_BOX_H, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = g_encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(gray),
+                         gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(LD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", cr);
+
+  SobelParams p;
+  p.width = W;
+  p.height = H;
+  p.row_begin = img->row_begin;
+  p.row_end = img->row_end;
+  p.ry0 = ry0;
+  p.tiles_x = (W + SB_TILE_W - 1) / SB_TILE_W;
+  p.tiles_y = (img->row_end - img->row_begin + SB_TILE_H - 1) / SB_TILE_H;
+  p.tiles_per_frame = p.tiles_x * p.tiles_y;
+  const int64_t n_tiles = static_cast<int64_t>(p.tiles_per_frame) * img->batch;
+  if (n_tiles > (1ll << 30)) return fail(LD_ERR_INVALID_ARG, "batch too large");
+  p.n_tiles = static_cast<int32_t>(n_tiles);
+  p.batch = img->batch;
+  int t2 = threshold <= 0 ? 0 : static_cast<int>((static_cast<int64_t>(threshold) + 1) / 2);
+  p.t2 = t2 > 766 ? 766 : t2;
+  const char *env = getenv("LD_EDGE_ORDER");
+  p.scatter = (env && strcmp(env, "raster") == 0) ? 0 : 1;
+  p.binary = binary;
+  p.bin_pitch = img->pitch;
+  p.bin_frame_stride = static_cast<int64_t>(img->row_end - img->row_begin) * img->pitch;
+  p.edges = edge_xy;
+  p.edge_stride = edge_stride;
+  p.counts = edge_count;
+
+  cudaError_t e = cudaMemsetAsync(edge_count, 0, sizeof(uint32_t) * img->batch, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(edge_count)");
+  const int64_t max_ctas = static_cast<int64_t>(dev.sm_count) * SB_CTAS_PER_SM;
+  const int n_ctas = static_cast<int>(n_tiles < max_ctas ? n_tiles : max_ctas);
+  e = launch_sobel(tmap, p, n_ctas, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sobel_binarize_compact_kernel launch");
+  return LD_OK;
+}
+
+static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
+                      int32_t batch, int32_t width, int32_t height, int32_t n_theta,
+                      const int32_t *cos_q15, const int32_t *sin_q15, uint32_t *acc,
+                      cudaStream_t stream) {
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  const int32_t d = rho_offset(width, height);
+  if ((rc = check_trig(n_theta, cos_q15, sin_q15, width, height, d))) return rc;
+  const int n_rho = 2 * d + 1;
+  const size_t limit = static_cast<size_t>(dev.smem_optin) - sizeof(int2) * HV_MAX_ROWS - 1024;
+  int n_bands = 0;
+  const int rpb = hough_rows_per_band(n_theta, n_rho, limit, &n_bands);
+  if (rpb < 1) return fail(LD_ERR_UNSUPPORTED, "one accumulator row (%d bins) exceeds shared memory", n_rho);
+  static thread_local TrigTable trig;  // 16 KB: keep it off the stack
+  memcpy(trig.c, cos_q15, sizeof(int32_t) * n_theta);
+  memcpy(trig.s, sin_q15, sizeof(int32_t) * n_theta);
+  HoughParams p;
+  p.edges = edge_xy;
+  p.counts = edge_count;
+  p.edge_stride = edge_stride;
+  p.batch = batch;
+  p.n_theta = n_theta;
+  p.n_rho = n_rho;
+  p.rows_per_band = rpb;
+  p.n_bands = n_bands;
+  p.koff = 16384 + (d << 15);
+  p.acc = acc;
+  const size_t smem = align_up(static_cast<size_t>(rpb) * n_rho * 4, 16);
+  cudaError_t e = launch_hough(p, trig, smem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");
+  return LD_OK;
+}
+
+static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                      int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                      ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t ws_bytes,
+                      cudaStream_t stream) {
+  PeaksParams p;
+  p.acc = acc;
+  p.batch = batch;
+  p.n_theta = n_theta;
+  p.n_rho = n_rho;
+  p.half_theta = half_theta;
+  p.half_rho = half_rho;
+  p.floor_votes = min_votes > 1 ? min_votes : 1u;
+  p.k = k;
+  p.n_bands = (n_theta + PK_ROWS - 1) / PK_ROWS;
+  p.band_keys = static_cast<unsigned long long *>(workspace);
+  p.peaks = peaks;
+  p.n_peaks = n_peaks;
+  (void)ws_bytes;
+  cudaError_t e = launch_peaks(p, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "peaks kernels launch");
+  return LD_OK;
+}
+
+static int check_peaks_args(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                            int32_t half_theta, int32_t half_rho, int32_t k, const ld_peak *peaks,
+                            const int32_t *n_peaks) {
+  if (!acc || !peaks || !n_peaks) return fail(LD_ERR_INVALID_ARG, "NULL acc/peaks/n_peaks");
+  if (batch < 1 || n_theta < 1 || n_theta > LD_MAX_THETA || n_rho < 1)
+    return fail(LD_ERR_INVALID_ARG, "bad accumulator shape [%d][%d][%d]", batch, n_theta, n_rho);
+  if (static_cast<int64_t>(n_theta) * n_rho >= (1ll << 32) - 1)
+    return fail(LD_ERR_INVALID_ARG, "accumulator too large for the 32-bit cell index");
+  if (half_theta < 0 || half_rho < 0) return fail(LD_ERR_INVALID_ARG, "negative window");
+  if (k < 1 || k > LD_MAX_K) return fail(LD_ERR_INVALID_ARG, "k %d outside [1, %d]", k, LD_MAX_K);
+  return LD_OK;
+}
+
+struct DetectLayout {
+  size_t counts_off, edges_off, acc_off, peaks_off, total;
+  int64_t edge_stride;
+};
+
+static DetectLayout detect_layout(const ld_image *img, int32_t n_theta, int32_t k, bool acc_ws) {
+  DetectLayout L;
+  const int64_t me = max_edges_per_frame(img);
+  L.edge_stride = static_cast<int64_t>(align_up(static_cast<size_t>(me > 0 ? me : 1), 4));
+  const int32_t d = rho_offset(img->width, img->height);
+  const size_t acc_bytes = static_cast<size_t>(img->batch) * n_theta * (2 * static_cast<size_t>(d) + 1) * 4;
+  size_t off = 0;
+  L.counts_off = off;
+  off = align_up(off + sizeof(uint32_t) * img->batch, 256);
+  L.edges_off = off;
+  off = align_up(off + sizeof(uint32_t) * static_cast<size_t>(L.edge_stride) * img->batch, 256);
+  L.acc_off = off;
+  if (acc_ws) off = align_up(off + acc_bytes, 256);
+  L.peaks_off = off;
+  off = align_up(off + peaks_workspace_bytes(img->batch, n_theta, k), 256);
+  L.total = off;
+  return L;
+}
+
+}  // namespace ld
+
+using namespace ld;
+
+extern "C" {
+
+int32_t ld_rho_offset(int32_t width, int32_t height) { return rho_offset(width, height); }
+
+const char *ld_status_string(int status) {
+  switch (status) {
+    case LD_OK: return "LD_OK";
+    case LD_ERR_INVALID_ARG: return "LD_ERR_INVALID_ARG";
+    case LD_ERR_RANGE: return "LD_ERR_RANGE";
+    case LD_ERR_WORKSPACE: return "LD_ERR_WORKSPACE";
+    case LD_ERR_UNSUPPORTED: return "LD_ERR_UNSUPPORTED";
+    case LD_ERR_CUDA: return "LD_ERR_CUDA";
+    default: return "LD_ERR_UNKNOWN";
+  }
+}
+
+const char *ld_last_error_detail(void) { return g_err; }
+
+int32_t ld_last_launch_count(void) { return g_launches; }
+
+int32_t ld_device_sm_count(void) {
+  DevInfo d;
+  device_info(&d);
+  return d.sm_count;
+}
+
+int64_t ld_device_l2_bytes(void) {
+  DevInfo d;
+  device_info(&d);
+  return d.l2;
+}
+
+int ld_sobel_binarize(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                      uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
+                      uint32_t *edge_count, void *stream) {
+  g_launches = 0;
+  int rc = check_image(gray, img);
+  if (rc) return rc;
+  if (!edge_count) return fail(LD_ERR_INVALID_ARG, "edge_count is NULL");
+  if (edge_xy && edge_stride < max_edges_per_frame(img))
+    return fail(LD_ERR_INVALID_ARG, "edge_stride %lld < %lld possible edges per frame",
+                static_cast<long long>(edge_stride),
+                static_cast<long long>(max_edges_per_frame(img)));
+  if (binary && !aligned(binary, 16)) return fail(LD_ERR_INVALID_ARG, "binary must be 16-byte aligned");
+  return sobel_impl(gray, img, threshold, binary, edge_xy, edge_stride, edge_count,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
+                        int32_t batch, int32_t width, int32_t height, int32_t n_theta,
+                        const int32_t *cos_q15, const int32_t *sin_q15, uint32_t *acc,
+                        void *stream) {
+  g_launches = 0;
+  if (!edge_xy || !edge_count || !acc) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
+  if (batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
+  if (width < 1 || height < 1 || width > LD_MAX_DIM || height > LD_MAX_DIM)
+    return fail(LD_ERR_INVALID_ARG, "width/height outside [1, %d]", LD_MAX_DIM);
+  if (!aligned(edge_xy, 16) || edge_stride < 0 || edge_stride % 4 != 0)
+    return fail(LD_ERR_INVALID_ARG, "edge_xy must be 16-byte aligned and edge_stride a multiple of 4");
+  return hough_impl(edge_xy, edge_count, edge_stride, batch, width, height, n_theta, cos_q15,
+                    sin_q15, acc, static_cast<cudaStream_t>(stream));
+}
+
+size_t ld_hough_peaks_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_rho, int32_t k) {
+  (void)n_rho;
+  if (batch < 1 || n_theta < 1 || k < 1) return 0;
+  return peaks_workspace_bytes(batch, n_theta, k);
+}
+
+int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                   int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                   ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t workspace_bytes,
+                   void *stream) {
+  g_launches = 0;
+  int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
+  if (rc) return rc;
+  DevInfo dev;
+  if ((rc = device_info(&dev))) return rc;
+  if (!workspace || !aligned(workspace, 16) ||
+      workspace_bytes < peaks_workspace_bytes(batch, n_theta, k))
+    return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 16-byte aligned",
+                peaks_workspace_bytes(batch, n_theta, k));
+  return peaks_impl(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
+                    n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t ld_detect_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k,
+                                 int32_t acc_in_workspace) {
+  if (!img || img->batch < 1 || img->width < 1 || img->height < 1 || n_theta < 1 || k < 1) return 0;
+  ld_image whole = *img;
+  whole.row_begin = 0;
+  whole.row_end = img->height;
+  return detect_layout(&whole, n_theta, k, acc_in_workspace != 0).total;
+}
+
+int ld_detect_batch(const uint8_t *gray, const ld_image *img, int32_t threshold, int32_t n_theta,
+                    const int32_t *cos_q15, const int32_t *sin_q15, int32_t half_theta,
+                    int32_t half_rho, uint32_t min_votes, int32_t k, ld_peak *peaks,
+                    int32_t *n_peaks, uint32_t *edge_count, uint32_t *acc, void *workspace,
+                    size_t workspace_bytes, void *stream) {
+  g_launches = 0;
+  int rc = check_image(gray, img);
+  if (rc) return rc;
+  if (img->row_begin != 0 || img->row_end != img->height)
+    return fail(LD_ERR_INVALID_ARG, "ld_detect_batch takes whole frames (rows [0, height))");
+  const int32_t d = rho_offset(img->width, img->height);
+  const int32_t n_rho = 2 * d + 1;
+  if ((rc = check_trig(n_theta, cos_q15, sin_q15, img->width, img->height, d))) return rc;
+  if ((rc = check_peaks_args(acc ? acc : reinterpret_cast<uint32_t *>(16), img->batch, n_theta,
+                             n_rho, half_theta, half_rho, k, peaks, n_peaks)))
+    return rc;
+  const DetectLayout L = detect_layout(img, n_theta, k, acc == nullptr);
+  if (!workspace || !aligned(workspace, 256) || workspace_bytes < L.total)
+    return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 256-byte aligned", L.total);
+  if (acc && !aligned(acc, 16)) return fail(LD_ERR_INVALID_ARG, "acc must be 16-byte aligned");
+  char *ws = static_cast<char *>(workspace);
+  uint32_t *counts = reinterpret_cast<uint32_t *>(ws + L.counts_off);
+  uint32_t *edges = reinterpret_cast<uint32_t *>(ws + L.edges_off);
+  uint32_t *A = acc ? acc : reinterpret_cast<uint32_t *>(ws + L.acc_off);
+  void *pws = ws + L.peaks_off;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((rc = sobel_impl(gray, img, threshold, nullptr, edges, L.edge_stride, counts, s))) return rc;
+  if ((rc = hough_impl(edges, counts, L.edge_stride, img->batch, img->width, img->height, n_theta,
+                       cos_q15, sin_q15, A, s)))
+    return rc;
+  if ((rc = peaks_impl(A, img->batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
+                       n_peaks, pws, workspace_bytes - L.peaks_off, s)))
+    return rc;
+  if (edge_count) {
+    cudaError_t e = cudaMemcpyAsync(edge_count, counts, sizeof(uint32_t) * img->batch,
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(edge_count)");
+  }
+  return LD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer path: chunked, double-buffered H2D overlapped with the kernels.
+// Device workspace layout: [2][chunk][frame_stride] gray staging, then for each
+// of the 2 slots {peaks[chunk][k], n_peaks[chunk], counts[chunk]}, then one
+// ld_detect_batch workspace sized for `chunk` frames (acc in workspace).
+// ---------------------------------------------------------------------------
+struct HostLayout {
+  size_t gray_off[2], peaks_off[2], npk_off[2], cnt_off[2], det_off, det_bytes, total;
+  int64_t fstride;
+};
+
+static HostLayout host_layout(const ld_image *img, int32_t n_theta, int32_t k, int32_t chunk) {
+  HostLayout L;
+  L.fstride = img->batch > 1 ? img->frame_stride : static_cast<int64_t>(img->height) * img->pitch;
+  size_t off = 0;
+  for (int i = 0; i < 2; ++i) {
+    L.gray_off[i] = off;
+    off = align_up(off + static_cast<size_t>(L.fstride) * chunk, 256);
+  }
+  for (int i = 0; i < 2; ++i) {
+    L.peaks_off[i] = off;
+    off = align_up(off + sizeof(ld_peak) * static_cast<size_t>(k) * chunk, 256);
+    L.npk_off[i] = off;
+    off = align_up(off + sizeof(int32_t) * chunk, 256);
+    L.cnt_off[i] = off;
+    off = align_up(off + sizeof(uint32_t) * chunk, 256);
+  }
+  ld_image ci = *img;
+  ci.batch = chunk;
+  ci.row_begin = 0;
+  ci.row_end = img->height;
+  L.det_off = off;
+  L.det_bytes = detect_layout(&ci, n_theta, k, true).total;
+  L.total = off + L.det_bytes;
+  return L;
+}
+
+size_t ld_detect_host_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k,
+                                      int32_t chunk_frames) {
+  if (!img || img->batch < 1 || chunk_frames < 1 || n_theta < 1 || k < 1) return 0;
+  const int32_t chunk = chunk_frames < img->batch ? chunk_frames : img->batch;
+  return host_layout(img, n_theta, k, chunk).total;
+}
+
+int ld_detect_batch_host(const uint8_t *gray_host, const ld_image *img, int32_t threshold,
+                         int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
+                         int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                         ld_peak *peaks_host, int32_t *n_peaks_host, uint32_t *edge_count_host,
+                         int32_t chunk_frames, void *workspace, size_t workspace_bytes,
+                         void *stream) {
+  if (!gray_host || !img || !peaks_host || !n_peaks_host)
+    return fail(LD_ERR_INVALID_ARG, "NULL host pointer");
+  if (chunk_frames < 1) return fail(LD_ERR_INVALID_ARG, "chunk_frames must be >= 1");
+  if (img->row_begin != 0 || img->row_end != img->height)
+    return fail(LD_ERR_INVALID_ARG, "ld_detect_batch_host takes whole frames");
+  const int32_t chunk = chunk_frames < img->batch ? chunk_frames : img->batch;
+  const HostLayout L = host_layout(img, n_theta, k, chunk);
+  if (!workspace || !aligned(workspace, 256) || workspace_bytes < L.total)
+    return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 256-byte aligned", L.total);
+  int launches = 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t cs = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+  int rc = LD_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) rc = cuda_fail(e, "stream/event creation");
+  char *ws = static_cast<char *>(workspace);
+  const int n_chunks = (img->batch + chunk - 1) / chunk;
+  // the copy stream must not start before earlier work on `stream` that may use the workspace
+  if (rc == LD_OK) {
+    e = cudaEventRecord(done[1], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, done[1], 0);
+    if (e != cudaSuccess) rc = cuda_fail(e, "initial ordering");
+  }
+  for (int ci = 0; ci < n_chunks && rc == LD_OK; ++ci) {
+    const int slot = ci & 1;
+    const int f0 = ci * chunk;
+    const int nf = img->batch - f0 < chunk ? img->batch - f0 : chunk;
+    uint8_t *dgray = reinterpret_cast<uint8_t *>(ws + L.gray_off[slot]);
+    if (ci >= 2) {  // slot reuse: wait for the kernels of chunk ci-2
+      e = cudaStreamWaitEvent(cs, done[slot], 0);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "cudaStreamWaitEvent"); break; }
+    }
+    e = cudaMemcpyAsync(dgray, gray_host + static_cast<int64_t>(f0) * L.fstride,
+                        static_cast<size_t>(L.fstride) * nf, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(copied[slot], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, copied[slot], 0);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "H2D copy"); break; }
+    ld_image ci_img = *img;
+    ci_img.batch = nf;
+    ci_img.frame_stride = L.fstride;
+    ld_peak *dpk = reinterpret_cast<ld_peak *>(ws + L.peaks_off[slot]);
+    int32_t *dnp = reinterpret_cast<int32_t *>(ws + L.npk_off[slot]);
+    uint32_t *dcnt = reinterpret_cast<uint32_t *>(ws + L.cnt_off[slot]);
+    rc = ld_detect_batch(dgray, &ci_img, threshold, n_theta, cos_q15, sin_q15, half_theta,
+                         half_rho, min_votes, k, dpk, dnp, dcnt, nullptr, ws + L.det_off,
+                         L.det_bytes, s);
+    launches += g_launches;
+    if (rc) break;
+    e = cudaEventRecord(done[slot], s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(peaks_host + static_cast<int64_t>(f0) * k, dpk,
+                          sizeof(ld_peak) * static_cast<size_t>(k) * nf, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(n_peaks_host + f0, dnp, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && edge_count_host)
+      e = cudaMemcpyAsync(edge_count_host + f0, dcnt, sizeof(uint32_t) * nf,
+                          cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "D2H copy"); break; }
+  }
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess && rc == LD_OK) rc = cuda_fail(e, "cudaStreamSynchronize");
+  if (cs) cudaStreamSynchronize(cs);
+  for (int i = 0; i < 2; ++i) {
+    if (copied[i]) cudaEventDestroy(copied[i]);
+    if (done[i]) cudaEventDestroy(done[i]);
+  }
+  if (cs) cudaStreamDestroy(cs);
+  g_launches = launches;
+  return rc;
+}
+
+int ld_bench_smem_atomics(int32_t mode, int32_t iters, int32_t blocks_per_sm,
+                          uint64_t *atomics_out, void *scratch, void *stream) {
+  g_launches = 0;
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  if (mode < 0 || mode > 2 || iters < 1 || blocks_per_sm < 1 || !scratch)
+    return fail(LD_ERR_INVALID_ARG, "bad microbenchmark arguments");
+  const int grid = dev.sm_count * blocks_per_sm;
+  cudaError_t e = launch_smem_atomic_bench(mode, iters, grid, static_cast<uint32_t *>(scratch),
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "smem_atomic_bench_kernel launch");
+  if (atomics_out) *atomics_out = static_cast<uint64_t>(grid) * 1024ull * static_cast<uint64_t>(iters);
+  return LD_OK;
+}
+
+}  // extern "C"

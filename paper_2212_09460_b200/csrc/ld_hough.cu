@@ -1,0 +1,178 @@
+// ld_hough.cu -- B3: theta-partitioned shared-memory Hough voting, sm_100a;
+//                B5: shared-memory atomic microbenchmark (the voting roofline).
+//
+// Paper: Eq. 3, voting, 180 one-degree PEs, the GPU
+// design of one thread block per theta with the voting space in block shared
+// memory and atomic adds for colliding votes.  DESIGN.md 6.2.
+//
+// Design: the paper gives each theta its own 48 KB block (K80).  On sm_100a a
+// CTA owns a BAND of theta rows -- as many rows of n_rho uint32 counters as fit
+// in the 227 KB opt-in shared memory -- so each frame's edge list is streamed
+// n_theta / rows times instead of n_theta times.  Every thread holds 4 edges
+// (one 16-byte load) and, for each row of the band, issues one
+// red.shared.add.u32 per edge at ((x*C + y*S + 2^14 + (D << 15)) >> 15).  The
+// range proof done on the host (ld_api.cu) makes a per-vote bounds check
+// unnecessary.  The band is then written to HBM with plain coalesced stores:
+// no global atomics anywhere.
+#include "ld_internal.cuh"
+
+namespace ld {
+
+__global__ void __launch_bounds__(HV_THREADS, 1)
+    hough_vote_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
+  extern __shared__ __align__(16) uint32_t slice[];
+  __shared__ int2 cs[HV_MAX_ROWS];
+
+  const int tid = threadIdx.x;
+  const int band = blockIdx.x;
+  const int f = blockIdx.y;
+  const int t0 = band * p.rows_per_band;
+  const int nr = min(p.rows_per_band, p.n_theta - t0);
+  const int ncell = nr * p.n_rho;
+
+  {
+    uint4 *s4 = reinterpret_cast<uint4 *>(slice);
+    const int n4 = (ncell + 3) >> 2;
+    for (int i = tid; i < n4; i += HV_THREADS) s4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < nr; i += HV_THREADS) cs[i] = make_int2(trig.c[t0 + i], trig.s[t0 + i]);
+  }
+  __syncthreads();
+
+  const uint32_t n_edges = p.counts[f];
+  const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
+  const uint32_t sbase = smem_u32(slice);
+  const uint32_t row_bytes = static_cast<uint32_t>(p.n_rho) * 4u;
+  const int koff = p.koff;
+
+  for (uint32_t e = static_cast<uint32_t>(tid) * 4u; e < n_edges; e += HV_THREADS * 4u) {
+    uint32_t q[4];
+    int nv = 4;
+    if (e + 4u <= n_edges) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(el + e));
+      q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+    } else {
+      nv = static_cast<int>(n_edges - e);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[j] = (j < nv) ? __ldg(el + e + j) : 0u;
+    }
+    int xs[4], ys[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      xs[j] = static_cast<int>(q[j] & 0xFFFFu);
+      ys[j] = static_cast<int>(q[j] >> 16);
+    }
+    if (nv == 4) {
+#pragma unroll 2
+      for (int r = 0; r < nr; ++r) {
+        const int2 c = cs[r];
+        const uint32_t rowb = sbase + static_cast<uint32_t>(r) * row_bytes;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int v = xs[j] * c.x + ys[j] * c.y + koff;
+          red_shared_add(rowb + (static_cast<uint32_t>(v >> 15) << 2), 1u);
+        }
+      }
+    } else {
+      for (int r = 0; r < nr; ++r) {
+        const int2 c = cs[r];
+        const uint32_t rowb = sbase + static_cast<uint32_t>(r) * row_bytes;
+        for (int j = 0; j < nv; ++j) {
+          const int v = xs[j] * c.x + ys[j] * c.y + koff;
+          red_shared_add(rowb + (static_cast<uint32_t>(v >> 15) << 2), 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  uint32_t *dst = p.acc + (static_cast<int64_t>(f) * p.n_theta + t0) * p.n_rho;
+  for (int i = tid; i < ncell; i += HV_THREADS) dst[i] = slice[i];
+}
+
+int hough_rows_per_band(int n_theta, int n_rho, size_t smem_limit, int *n_bands) {
+  const size_t row = static_cast<size_t>(n_rho) * 4u;
+  int rows_max = static_cast<int>(smem_limit / row);
+  if (rows_max > HV_MAX_ROWS) rows_max = HV_MAX_ROWS;
+  if (rows_max < 1) return 0;
+  const int nb = (n_theta + rows_max - 1) / rows_max;
+  *n_bands = nb;
+  return (n_theta + nb - 1) / nb;
+}
+
+static bool g_hough_attr[64];
+
+cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, size_t smem_bytes,
+                         cudaStream_t stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_hough_attr[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(hough_vote_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024 - static_cast<int>(sizeof(int2)) * HV_MAX_ROWS);
+    if (e != cudaSuccess) return e;
+    g_hough_attr[dev & 63] = true;
+  }
+  dim3 grid(p.n_bands, p.batch);
+  hough_vote_kernel<<<grid, HV_THREADS, smem_bytes, stream>>>(p, trig);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// B5: red.shared.add.u32 throughput.  1024 threads per CTA, 48 K-word array.
+// ---------------------------------------------------------------------------
+constexpr int AB_WORDS = 49152;
+
+__global__ void __launch_bounds__(1024, 1)
+    smem_atomic_bench_kernel(int mode, int iters, uint32_t *out) {
+  extern __shared__ __align__(16) uint32_t buf[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < AB_WORDS; i += blockDim.x) buf[i] = 0u;
+  __syncthreads();
+  const uint32_t base = smem_u32(buf);
+  if (mode == 0) {
+    // conflict-free: lane l -> bank l, a different word every iteration
+    uint32_t row = static_cast<uint32_t>(warp) * 37u;
+#pragma unroll 8
+    for (int i = 0; i < iters; ++i) {
+      red_shared_add(base + ((lane + 32u * (row & 1023u)) << 2), 1u);
+      row += 1u;
+    }
+  } else if (mode == 1) {
+    uint32_t x = (blockIdx.x * 1024u + tid) * 2654435761u + 12345u;
+#pragma unroll 8
+    for (int i = 0; i < iters; ++i) {
+      x = x * 1664525u + 1013904223u;
+      red_shared_add(base + ((x >> 17) << 2), 1u);
+    }
+  } else {
+#pragma unroll 8
+    for (int i = 0; i < iters; ++i) red_shared_add(base + (static_cast<uint32_t>(warp) << 7), 1u);
+  }
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t s = 0;
+    for (int i = tid; i < AB_WORDS; i += 32) s += buf[i];
+    out[blockIdx.x * 32 + tid] = s;
+  }
+}
+
+static bool g_bench_attr[64];
+
+cudaError_t launch_smem_atomic_bench(int mode, int iters, int grid, uint32_t *scratch,
+                                     cudaStream_t stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int smem = AB_WORDS * 4;
+  if (!g_bench_attr[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(smem_atomic_bench_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    g_bench_attr[dev & 63] = true;
+  }
+  smem_atomic_bench_kernel<<<grid, 1024, smem, stream>>>(mode, iters, scratch);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ld

@@ -1,0 +1,154 @@
+// ld_internal.cuh -- shared declarations of the libld.so translation units.
+// Product code only: nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ld.h"
+
+namespace ld {
+
+// ---------------------------------------------------------------------------
+// B1: fused Sobel + binarize + compaction (ld_sobel.cu)
+// ---------------------------------------------------------------------------
+constexpr int SB_BOX_W = 256;       // TMA box width in bytes (hardware max 256)
+constexpr int SB_HALO_L = 16;       // box starts 16 columns left of the tile
+constexpr int SB_CHUNKS = 14;       // 16-px output chunks per tile row
+constexpr int SB_TILE_W = SB_CHUNKS * 16;  // 224 output columns per tile
+constexpr int SB_SR = 4;            // output rows per thread strip
+constexpr int SB_STRIPS = 16;       // strips per tile
+constexpr int SB_TILE_H = SB_SR * SB_STRIPS;  // 64 output rows per tile
+constexpr int SB_BOX_H = SB_TILE_H + 2;       // + 1-row halo above and below
+constexpr int SB_THREADS = SB_CHUNKS * SB_STRIPS;  // 224 = 7 warps
+constexpr int SB_STAGES = 4;
+constexpr int SB_STAGE_BYTES = SB_BOX_W * SB_BOX_H;  // 16896 = 132 * 128
+constexpr int SB_CTAS_PER_SM = 3;
+
+struct SobelParams {
+  int32_t width, height;
+  int32_t row_begin, row_end;  // owned rows (global)
+  int32_t ry0;                 // global row of tensor row 0 = max(row_begin-1, 0)
+  int32_t tiles_x, tiles_y, tiles_per_frame, n_tiles;
+  int32_t batch;
+  int32_t t2;                  // ceil(T/2) clamped to [0, 766]
+  int32_t scatter;             // permute edge order inside a tile (perf only)
+  uint8_t *binary;
+  int64_t bin_pitch, bin_frame_stride;
+  uint32_t *edges;
+  int64_t edge_stride;
+  uint32_t *counts;
+};
+
+cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int n_ctas,
+                         cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// B3: theta-band shared-memory Hough voting (ld_hough.cu)
+// ---------------------------------------------------------------------------
+struct TrigTable {
+  int32_t c[LD_MAX_THETA];
+  int32_t s[LD_MAX_THETA];
+};
+
+struct HoughParams {
+  const uint32_t *edges;
+  const uint32_t *counts;
+  int64_t edge_stride;
+  int32_t batch;
+  int32_t n_theta, n_rho;
+  int32_t rows_per_band, n_bands;
+  int32_t koff;  // 2^14 + (D << 15): rho_bin = (x*C + y*S + koff) >> 15
+  uint32_t *acc;
+};
+
+constexpr int HV_THREADS = 1024;
+constexpr int HV_MAX_ROWS = 256;
+
+cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, size_t smem_bytes,
+                         cudaStream_t stream);
+int hough_rows_per_band(int n_theta, int n_rho, size_t smem_limit, int *n_bands);
+
+// ---------------------------------------------------------------------------
+// B4: peaks (ld_peaks.cu)
+// ---------------------------------------------------------------------------
+constexpr int PK_THREADS = 512;
+constexpr int PK_ROWS = 4;  // theta rows per band CTA
+
+struct PeaksParams {
+  const uint32_t *acc;
+  int32_t batch, n_theta, n_rho;
+  int32_t half_theta, half_rho;
+  uint32_t floor_votes;  // max(1, min_votes)
+  int32_t k;
+  int32_t n_bands;
+  unsigned long long *band_keys;  // [batch][n_bands][k]
+  ld_peak *peaks;
+  int32_t *n_peaks;
+};
+
+size_t peaks_workspace_bytes(int batch, int n_theta, int k);
+cudaError_t launch_peaks(const PeaksParams &p, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// B5: shared-memory atomic microbenchmark (ld_hough.cu)
+// ---------------------------------------------------------------------------
+cudaError_t launch_smem_atomic_bench(int mode, int iters, int grid, uint32_t *scratch,
+                                     cudaStream_t stream);
+
+// launch counter of the current host thread (ld_api.cu)
+void note_launch(int n = 1);
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LD_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+}  // namespace ld

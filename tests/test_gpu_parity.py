@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Everything here is integer work, so the bar is exact equality of the binary
+map, the edge count, the edge list as a set (DESIGN R15), the accumulator and
+the peaks (DESIGN R22).  Inputs are the seeded generators of
+paper_2212_09460_b200.synth; expected values come only from oracle/.
+"""
+import numpy as np
+import pytest
+
+from paper_2212_09460_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ld():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2212_09460_b200 import build, ld as _ld
+    build.build()
+    return _ld
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def peak_tuples(p, n=None):
+    p = np.asarray(p).reshape(-1, 3)
+    out = [(int(a), int(b), int(np.uint32(np.int32(c)))) for a, b, c in p]
+    return out
+
+
+def oracle_peak_tuples(pk):
+    return [(int(p["theta_bin"]), int(p["rho_bin"]), int(p["votes"])) for p in pk]
+
+
+def gpu_sobel(ld, frames, threshold, pitch_pad=0):
+    """frames: uint8 [B][H][W] numpy -> binary, sorted edge lists, counts."""
+    b, h, w = frames.shape
+    pitch = ld._round_up(w, 16) + pitch_pad
+    buf = np.zeros((b, h, pitch), np.uint8)
+    buf[:, :, :w] = frames
+    g = cuda(buf)
+    img = ld.make_image(w, h, pitch, h * pitch, b)
+    stride = ld._round_up(max(h * max(w - 2, 0), 1), 4)
+    binary = torch.full((b, h, pitch), 7, dtype=torch.uint8, device="cuda")
+    edges = torch.full((b, stride), -1, dtype=torch.int32, device="cuda")
+    counts = torch.full((b,), -1, dtype=torch.int32, device="cuda")
+    ld.ld_sobel_binarize(g, img, threshold, binary, edges, stride, counts)
+    torch.cuda.synchronize()
+    cnt = counts.cpu().numpy()
+    el = edges.cpu().numpy().view(np.uint32)
+    lists = [np.sort(el[i, :cnt[i]]) for i in range(b)]
+    return binary.cpu().numpy()[:, :, :w], lists, cnt
+
+
+# ----------------------------------------------------------------------------
+# Stage 1-2: Sobel + binarize + compaction
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4"])
+def test_sobel_configs(ld, oracle, name):
+    cfg = synth.CONFIGS[name]
+    img = synth.gen_frame(name, 0)
+    binary, lists, cnt = gpu_sobel(ld, img[None], cfg.threshold)
+    want = oracle.sobel_binarize(img, cfg.threshold)
+    assert np.array_equal(binary[0], want)
+    we = oracle.compact(want)
+    assert cnt[0] == len(we)
+    assert np.array_equal(lists[0], np.sort(we))
+
+
+def test_sobel_cfg5_full_size(ld, oracle):
+    img = synth.gen_frame("cfg5", 0)
+    binary, lists, cnt = gpu_sobel(ld, img[None], 200)
+    want = oracle.sobel_binarize(img, 200)
+    assert np.array_equal(binary[0], want)
+    assert np.array_equal(lists[0], np.sort(oracle.compact(want)))
+
+
+def test_sobel_batch_cfg3_frames(ld, oracle):
+    frames = synth.gen_batch("cfg3", 0, 6)
+    binary, lists, cnt = gpu_sobel(ld, frames, 200)
+    for i in range(6):
+        want = oracle.sobel_binarize(frames[i], 200)
+        assert np.array_equal(binary[i], want), i
+        assert np.array_equal(lists[i], np.sort(oracle.compact(want))), i
+
+
+SIZES = [(1, 1), (1, 5), (2, 2), (3, 3), (4, 3), (17, 2), (2, 40), (5, 7), (15, 16), (16, 16),
+         (17, 17), (31, 33), (223, 65), (224, 64), (225, 66), (241, 129), (256, 300), (300, 1)]
+
+
+@pytest.mark.parametrize("w,h", SIZES)
+@pytest.mark.parametrize("kind", ["uniform", "binary"])
+def test_sobel_fuzz_sizes(ld, oracle, w, h, kind):
+    img = synth.random_image(w * 1000 + h, w, h, kind)
+    for t in (0, 1, 199, 200, 201, 1530, 1531, -5):
+        binary, lists, cnt = gpu_sobel(ld, img[None], t, pitch_pad=16 if w % 2 else 0)
+        want = oracle.sobel_binarize(img, t)
+        assert np.array_equal(binary[0], want), (w, h, t)
+        assert np.array_equal(lists[0], np.sort(oracle.compact(want))), (w, h, t)
+
+
+def test_sobel_bands_match_whole(ld, oracle):
+    # row bands with a 1-row halo (ld_image.row_begin/row_end) == whole frame
+    img = synth.random_image(77, 200, 150, "uniform")
+    want = oracle.sobel_binarize(img, 300)
+    pitch = 208
+    full = np.zeros((150, pitch), np.uint8)
+    full[:, :200] = img
+    got_rows, got_edges = [], []
+    for rb, re in [(0, 1), (1, 37), (37, 64), (64, 65), (65, 149), (149, 150)]:
+        r0, r1 = max(rb - 1, 0), min(re + 1, 150)
+        g = cuda(full[r0:r1].copy())
+        im = ld.make_image(200, 150, pitch, (r1 - r0) * pitch, 1, rb, re)
+        stride = ld._round_up((re - rb) * 198, 4)
+        b = torch.zeros((re - rb, pitch), dtype=torch.uint8, device="cuda")
+        e = torch.zeros((max(stride, 4),), dtype=torch.int32, device="cuda")
+        c = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        ld.ld_sobel_binarize(g, im, 300, b, e, stride, c)
+        torch.cuda.synchronize()
+        got_rows.append(b.cpu().numpy()[:, :200])
+        got_edges.append(e.cpu().numpy().view(np.uint32)[: int(c.item())])
+    assert np.array_equal(np.concatenate(got_rows), want)
+    assert np.array_equal(np.sort(np.concatenate(got_edges)), np.sort(oracle.compact(want)))
+
+
+# ----------------------------------------------------------------------------
+# Stage 3: voting
+# ----------------------------------------------------------------------------
+def gpu_vote_list(ld, edge_lists, w, h, n_theta):
+    c, s = synth.q15_table(n_theta)
+    b = len(edge_lists)
+    stride = ld._round_up(max(max(len(e) for e in edge_lists), 1), 4)
+    el = np.zeros((b, stride), np.uint32)
+    for i, e in enumerate(edge_lists):
+        el[i, :len(e)] = e
+    counts = cuda(np.array([len(e) for e in edge_lists], np.int32))
+    acc = ld.hough_accumulate(cuda(el.view(np.int32)), counts, stride, w, h, c, s)
+    torch.cuda.synchronize()
+    return acc.cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("n_theta", [1, 2, 3, 180, 181, 720, 1024, 2048])
+def test_vote_random_lists(ld, oracle, n_theta):
+    c, s = synth.q15_table(n_theta)
+    rng = np.random.default_rng(n_theta)
+    w, h = 301, 203
+    lists = []
+    for n in (0, 1, 5, 4099):
+        xs, ys = rng.integers(0, w, n), rng.integers(0, h, n)
+        lists.append(((ys.astype(np.uint32) << 16) | xs.astype(np.uint32)))
+    got = gpu_vote_list(ld, lists, w, h, n_theta)
+    for i, e in enumerate(lists):
+        assert np.array_equal(got[i], oracle.hough_accumulate(e, w, h, c, s)), (n_theta, len(e))
+
+
+def test_vote_extreme_corners_and_tiny(ld, oracle):
+    for w, h in [(1, 1), (2, 1), (16384, 1), (1, 16384), (16384, 16384)]:
+        c, s = synth.q15_table(64)
+        corners = sorted({(0, 0), (w - 1, 0), (0, h - 1), (w - 1, h - 1)})
+        e = np.array([(y << 16) | x for x, y in corners], np.uint32)
+        got = gpu_vote_list(ld, [e], w, h, 64)
+        assert np.array_equal(got[0], oracle.hough_accumulate(e, w, h, c, s)), (w, h)
+
+
+def test_vote_collinear_hotspot(ld, oracle):
+    # thousands of votes into the same bin (same-address atomics)
+    c, s = synth.q15_table(180)
+    e = np.array([(100 << 16) | x for x in range(1000)] * 3, np.uint32)
+    got = gpu_vote_list(ld, [e], 1000, 200, 180)
+    want = oracle.hough_accumulate(e, 1000, 200, c, s)
+    assert np.array_equal(got[0], want) and want.max() == 3000
+
+
+def test_vote_range_error(ld):
+    c = np.array([40000], np.int32)
+    s = np.array([0], np.int32)
+    with pytest.raises(ld.LdError) as ei:
+        gpu_vote_list_raw(ld, c, s)
+    assert ei.value.status == ld.LD_ERR_RANGE
+
+
+def gpu_vote_list_raw(ld, c, s):
+    el = torch.zeros((4,), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    acc = torch.zeros((1, len(c), 2 * ld.ld_rho_offset(10, 10) + 1), dtype=torch.int32,
+                      device="cuda")
+    ld.ld_hough_accumulate(el, cnt, 4, 1, 10, 10, len(c), c, s, acc)
+
+
+# ----------------------------------------------------------------------------
+# Stage 4: peaks
+# ----------------------------------------------------------------------------
+def test_peaks_random_small(ld, oracle):
+    rng = np.random.default_rng(9)
+    for trial in range(40):
+        b = int(rng.integers(1, 4))
+        n_t, n_r = int(rng.integers(1, 40)), int(rng.integers(1, 700))
+        acc = rng.integers(0, int(rng.integers(1, 8)), size=(b, n_t, n_r)).astype(np.uint32)
+        ht, hr = int(rng.integers(0, 5)), int(rng.integers(0, 30))
+        mv, k = int(rng.integers(0, 5)), int(rng.choice([1, 2, 4, 7, 64, 1024]))
+        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, mv, k)
+        torch.cuda.synchronize()
+        peaks, npk = peaks.cpu().numpy(), npk.cpu().numpy()
+        for f in range(b):
+            want, wn = oracle.hough_peaks(acc[f], ht, hr, mv, k)
+            assert npk[f] == wn, (trial, f)
+            assert peak_tuples(peaks[f]) == oracle_peak_tuples(want), (trial, f)
+
+
+def test_peaks_window_zero_many_candidates(ld, oracle):
+    # every nonzero cell is a candidate: exercises the candidate buffer merges
+    rng = np.random.default_rng(2)
+    acc = rng.integers(0, 1000, size=(1, 37, 1999)).astype(np.uint32)
+    for k in (1, 5, 1024):
+        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), 0, 0, 1, k)
+        want, wn = oracle.hough_peaks(acc[0], 0, 0, 1, k)
+        assert int(npk[0]) == wn and peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(want)
+
+
+# ----------------------------------------------------------------------------
+# End to end (ld_detect_batch) on every config
+# ----------------------------------------------------------------------------
+def run_detect(ld, name, frames):
+    cfg = synth.CONFIGS[name]
+    c, s = synth.q15_table(cfg.n_theta)
+    b, h, w = frames.shape
+    det = ld.Detector(w, h, b, cfg.n_theta, c, s, cfg.threshold, cfg.k, cfg.half_theta,
+                      cfg.half_rho, cfg.min_votes, export_acc=True)
+    g = torch.zeros((b, h, det.pitch), dtype=torch.uint8, device="cuda")
+    g[:, :, :w] = cuda(frames)
+    peaks, npk, counts, acc = det(g)
+    torch.cuda.synchronize()
+    return det, peaks, npk, counts, acc
+
+
+def check_frame(oracle, name, frame, peaks_f, npk_f, count_f, acc_f):
+    cfg = synth.CONFIGS[name]
+    c, s = synth.q15_table(cfg.n_theta)
+    r = oracle.detect(frame, cfg.threshold, c, s, cfg.half_theta, cfg.half_rho, cfg.min_votes,
+                      cfg.k)
+    assert int(count_f) == r["n_edges"]
+    if acc_f is not None:
+        assert np.array_equal(acc_f, r["acc"])
+    assert int(npk_f) == r["n_peaks"]
+    assert peak_tuples(peaks_f) == oracle_peak_tuples(r["peaks"])
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg5"])
+def test_detect_single_frame_configs(ld, oracle, name):
+    frames = synth.gen_frame(name, 0)[None]
+    det, peaks, npk, counts, acc = run_detect(ld, name, frames)
+    check_frame(oracle, name, frames[0], peaks.cpu().numpy()[0], npk.cpu()[0], counts.cpu()[0],
+                acc.cpu().numpy().view(np.uint32)[0])
+
+
+def test_detect_cfg4_two_frames(ld, oracle):
+    frames = synth.gen_batch("cfg4", 0, 2)
+    det, peaks, npk, counts, acc = run_detect(ld, "cfg4", frames)
+    for i in range(2):
+        check_frame(oracle, "cfg4", frames[i], peaks.cpu().numpy()[i], npk.cpu()[i],
+                    counts.cpu()[i], acc[i].cpu().numpy().view(np.uint32))
+
+
+def test_detect_cfg3_full_batch_sampled(ld, oracle):
+    # full BASELINE size and launch configuration (256 frames); sampled frames
+    # against the oracle, invariants on every frame
+    cfg = synth.CONFIGS["cfg3"]
+    frames = synth.gen_batch("cfg3")
+    det, peaks, npk, counts, acc = run_detect(ld, "cfg3", frames)
+    sums = acc.view(256, -1).sum(dim=1, dtype=torch.int64).cpu().numpy()
+    cnt = counts.cpu().numpy().astype(np.int64)
+    assert np.array_equal(sums, cnt * cfg.n_theta)   # vote conservation, every frame
+    pk = peaks.cpu().numpy()
+    for i in (0, 1, 77, 128, 254, 255):
+        check_frame(oracle, "cfg3", frames[i], pk[i], npk.cpu()[i], cnt[i],
+                    acc[i].cpu().numpy().view(np.uint32))
+
+
+def test_detect_deterministic(ld):
+    frames = synth.gen_batch("cfg3", 0, 16)
+    a = run_detect(ld, "cfg3", frames)
+    b = run_detect(ld, "cfg3", frames)
+    for x, y in zip(a[1:], b[1:]):
+        assert torch.equal(x, y)
+
+
+def test_detect_host_path_matches_device(ld):
+    cfg = synth.CONFIGS["cfg3"]
+    c, s = synth.q15_table(cfg.n_theta)
+    frames = synth.gen_batch("cfg3", 0, 20)
+    _, peaks, npk, counts, _ = run_detect(ld, "cfg3", frames)
+    hd = ld.HostDetector(1280, 720, 20, cfg.n_theta, c, s, cfg.threshold, cfg.k, cfg.half_theta,
+                         cfg.half_rho, cfg.min_votes, chunk_frames=6)
+    host = torch.from_numpy(frames).pin_memory()
+    hp, hn, hc = hd(host)
+    assert torch.equal(hp, peaks.cpu()) and torch.equal(hn, npk.cpu())
+    assert torch.equal(hc, counts.cpu())
+
+
+def test_banded_accumulators_sum_to_whole(ld, oracle):
+    # cfg5 split in row bands: per-band accumulators summed == whole == oracle
+    cfg = synth.CONFIGS["cfg5"]
+    c, s = synth.q15_table(cfg.n_theta)
+    img = synth.gen_frame("cfg5", 0)
+    W = H = 4096
+    want = oracle.hough_accumulate(oracle.compact(oracle.sobel_binarize(img, 200)), W, H, c, s)
+    g_all = cuda(img)
+    for n in (2, 8):
+        total = None
+        for r in range(n):
+            rb, re = r * H // n, (r + 1) * H // n
+            r0, r1 = max(rb - 1, 0), min(re + 1, H)
+            im = ld.make_image(W, H, W, (r1 - r0) * W, 1, rb, re)
+            stride = ld._round_up((re - rb) * (W - 2), 4)
+            e = torch.empty((stride,), dtype=torch.int32, device="cuda")
+            cnt = torch.empty((1,), dtype=torch.int32, device="cuda")
+            ld.ld_sobel_binarize(g_all[r0:r1], im, 200, None, e, stride, cnt)
+            acc = ld.hough_accumulate(e, cnt, stride, W, H, c, s)
+            total = acc if total is None else total + acc
+        torch.cuda.synchronize()
+        assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want), n
