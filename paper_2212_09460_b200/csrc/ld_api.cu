@@ -189,8 +189,6 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
   p.batch = img->batch;
   int t2 = threshold <= 0 ? 0 : static_cast<int>((static_cast<int64_t>(threshold) + 1) / 2);
   p.t2 = t2 > 766 ? 766 : t2;
-  const char *env = getenv("LD_EDGE_ORDER");
-  p.scatter = (env && strcmp(env, "raster") == 0) ? 0 : 1;
   p.binary = binary;
   p.bin_pitch = img->pitch;
   p.bin_frame_stride = static_cast<int64_t>(img->row_end - img->row_begin) * img->pitch;
@@ -254,7 +252,7 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   p.half_rho = half_rho;
   p.floor_votes = min_votes > 1 ? min_votes : 1u;
   p.k = k;
-  p.n_bands = (n_theta + PK_ROWS - 1) / PK_ROWS;
+  p.n_units = 0;
   p.band_keys = static_cast<unsigned long long *>(workspace);
   p.peaks = peaks;
   p.n_peaks = n_peaks;
@@ -296,7 +294,7 @@ static DetectLayout detect_layout(const ld_image *img, int32_t n_theta, int32_t 
   L.acc_off = off;
   if (acc_ws) off = align_up(off + acc_bytes, 256);
   L.peaks_off = off;
-  off = align_up(off + peaks_workspace_bytes(img->batch, n_theta, k), 256);
+  off = align_up(off + peaks_workspace_bytes(img->batch, n_theta, 2 * d + 1, k), 256);
   L.total = off;
   return L;
 }
@@ -370,8 +368,8 @@ int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count, int
 
 size_t ld_hough_peaks_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_rho, int32_t k) {
   (void)n_rho;
-  if (batch < 1 || n_theta < 1 || k < 1) return 0;
-  return peaks_workspace_bytes(batch, n_theta, k);
+  if (batch < 1 || n_theta < 1 || n_rho < 1 || k < 1) return 0;
+  return peaks_workspace_bytes(batch, n_theta, n_rho, k);
 }
 
 int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
@@ -384,9 +382,9 @@ int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t 
   DevInfo dev;
   if ((rc = device_info(&dev))) return rc;
   if (!workspace || !aligned(workspace, 16) ||
-      workspace_bytes < peaks_workspace_bytes(batch, n_theta, k))
+      workspace_bytes < peaks_workspace_bytes(batch, n_theta, n_rho, k))
     return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 16-byte aligned",
-                peaks_workspace_bytes(batch, n_theta, k));
+                peaks_workspace_bytes(batch, n_theta, n_rho, k));
   return peaks_impl(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
                     n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }

@@ -9,8 +9,8 @@
 // CTA owns a BAND of theta rows -- as many rows of n_rho uint32 counters as fit
 // in the 227 KB opt-in shared memory -- so each frame's edge list is streamed
 // n_theta / rows times instead of n_theta times.  Every thread holds 4 edges
-// (one 16-byte load) and, for each row of the band, issues one
-// red.shared.add.u32 per edge at ((x*C + y*S + 2^14 + (D << 15)) >> 15).  The
+// and, for each row of the band, issues one red.shared.add.u32 per edge at
+// ((x*C + y*S + 2^14 + (D << 15)) >> 15) (SASS: ATOMS.POPC.INC).  The
 // range proof done on the host (ld_api.cu) makes a per-vote bounds check
 // unnecessary.  The band is then written to HBM with plain coalesced stores:
 // no global atomics anywhere.
@@ -44,24 +44,24 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   const uint32_t row_bytes = static_cast<uint32_t>(p.n_rho) * 4u;
   const int koff = p.koff;
 
-  for (uint32_t e = static_cast<uint32_t>(tid) * 4u; e < n_edges; e += HV_THREADS * 4u) {
-    uint32_t q[4];
-    int nv = 4;
-    if (e + 4u <= n_edges) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(el + e));
-      q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
-    } else {
-      nv = static_cast<int>(n_edges - e);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) q[j] = (j < nv) ? __ldg(el + e + j) : 0u;
-    }
+  // Each warp takes blocks of 128 consecutive list entries; at step j its 32
+  // lanes hold the 32 consecutive entries blk + 32j + lane, which the
+  // compaction made spatially compact (ld_sobel.cu): per theta they fall into
+  // few consecutive rho bins, i.e. distinct banks, and equal bins merge.
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARPS = HV_THREADS / 32;
+  for (uint32_t blk = static_cast<uint32_t>(warp) * 128u; blk < n_edges; blk += NWARPS * 128u) {
     int xs[4], ys[4];
+    bool ok[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      xs[j] = static_cast<int>(q[j] & 0xFFFFu);
-      ys[j] = static_cast<int>(q[j] >> 16);
+      const uint32_t e = blk + 32u * j + lane;
+      ok[j] = e < n_edges;
+      const uint32_t q = ok[j] ? __ldg(el + e) : 0u;
+      xs[j] = static_cast<int>(q & 0xFFFFu);
+      ys[j] = static_cast<int>(q >> 16);
     }
-    if (nv == 4) {
+    if (blk + 128u <= n_edges) {
 #pragma unroll 2
       for (int r = 0; r < nr; ++r) {
         const int2 c = cs[r];
@@ -76,9 +76,12 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
       for (int r = 0; r < nr; ++r) {
         const int2 c = cs[r];
         const uint32_t rowb = sbase + static_cast<uint32_t>(r) * row_bytes;
-        for (int j = 0; j < nv; ++j) {
-          const int v = xs[j] * c.x + ys[j] * c.y + koff;
-          red_shared_add(rowb + (static_cast<uint32_t>(v >> 15) << 2), 1u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (ok[j]) {
+            const int v = xs[j] * c.x + ys[j] * c.y + koff;
+            red_shared_add(rowb + (static_cast<uint32_t>(v >> 15) << 2), 1u);
+          }
         }
       }
     }

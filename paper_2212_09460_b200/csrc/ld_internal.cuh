@@ -33,7 +33,6 @@ struct SobelParams {
   int32_t tiles_x, tiles_y, tiles_per_frame, n_tiles;
   int32_t batch;
   int32_t t2;                  // ceil(T/2) clamped to [0, 766]
-  int32_t scatter;             // permute edge order inside a tile (perf only)
   uint8_t *binary;
   int64_t bin_pitch, bin_frame_stride;
   uint32_t *edges;
@@ -74,7 +73,10 @@ int hough_rows_per_band(int n_theta, int n_rho, size_t smem_limit, int *n_bands)
 // B4: peaks (ld_peaks.cu)
 // ---------------------------------------------------------------------------
 constexpr int PK_THREADS = 512;
-constexpr int PK_ROWS = 4;  // theta rows per band CTA
+constexpr int PK_ROWS = 4;         // theta rows per band CTA (generic kernel)
+constexpr int PT_TR = 16;          // theta rows per tile (tiled kernel)
+constexpr int PT_MAX_THREADS = 512;
+constexpr int PT_MAX_HT = 12;      // largest half_theta with a tiled instance
 
 struct PeaksParams {
   const uint32_t *acc;
@@ -82,13 +84,14 @@ struct PeaksParams {
   int32_t half_theta, half_rho;
   uint32_t floor_votes;  // max(1, min_votes)
   int32_t k;
-  int32_t n_bands;
-  unsigned long long *band_keys;  // [batch][n_bands][k]
+  int32_t n_units;                // tiles (tiled kernel) or bands (generic) per frame
+  int32_t tch, tc, tiles_t, tiles_r;  // tiled kernel geometry
+  unsigned long long *band_keys;  // [batch][n_units][k]
   ld_peak *peaks;
   int32_t *n_peaks;
 };
 
-size_t peaks_workspace_bytes(int batch, int n_theta, int k);
+size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k);
 cudaError_t launch_peaks(const PeaksParams &p, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------

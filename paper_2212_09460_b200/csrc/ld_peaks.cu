@@ -8,11 +8,15 @@
 // candidate iff acc >= max(1, min_votes) and its key is the maximum of its
 // (2ht+1) x (2hr+1) window clipped to the accumulator.  DESIGN.md 6.3.
 //
-// Kernel 1 (frames x theta bands of PK_ROWS rows): each thread tests cells of
-// the band; a cell whose key is not above the band's running K-th best key is
-// skipped before the window scan.  Candidates are buffered in shared memory and
-// merged into the band's top-K with a bitonic sort when a chunk produced any.
-// Kernel 2 (one CTA per frame): merges the bands' top-K lists.
+// Kernel 1, fast path (peaks_tile_kernel): separable window maximum over
+// 16 x tc tiles, see below.  Kernel 1, generic fallback for very large windows
+// (peaks_band_kernel: frames x theta bands of PK_ROWS rows): each thread tests
+// cells of the band by a window scan with early exit; a cell whose key is not
+// above the band's running K-th best key is skipped first.  Candidates are
+// buffered in shared memory and merged into the band's top-K with a bitonic
+// sort.  Kernel 2 (one CTA per frame): merges the per-unit top-K lists.
+#include <cstdlib>
+
 #include "ld_internal.cuh"
 
 namespace ld {
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
     }
     __syncthreads();
   }
-  u64 *out = p.band_keys + (static_cast<int64_t>(f) * p.n_bands + band) * p.k;
+  u64 *out = p.band_keys + (static_cast<int64_t>(f) * p.n_units + band) * p.k;
   const int ntop = s_ntop;
   for (int i = threadIdx.x; i < p.k; i += PK_THREADS) out[i] = i < ntop ? top[i] : 0ull;
 }
@@ -134,15 +138,29 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksPara
   __shared__ u64 top[LD_MAX_K];
   __shared__ int s_ntop;
   const int f = blockIdx.x;
-  const u64 *in = p.band_keys + static_cast<int64_t>(f) * p.n_bands * p.k;
-  const int n_in = p.n_bands * p.k;
-  if (threadIdx.x == 0) s_ntop = 0;
+  const u64 *in = p.band_keys + static_cast<int64_t>(f) * p.n_units * p.k;
+  const int n_in = p.n_units * p.k;
+  __shared__ int s_nbuf;
+  if (threadIdx.x == 0) {
+    s_ntop = 0;
+    s_nbuf = 0;
+  }
   __syncthreads();
   for (int base = 0; base < n_in; base += PK_CHUNK) {
+    // keys not above the current k-th best cannot enter the top-k: skip them
+    const u64 kth = (s_ntop == p.k) ? top[p.k - 1] : 0ull;
     const int nb = min(PK_CHUNK, n_in - base);
-    for (int i = threadIdx.x; i < nb; i += PK_THREADS) buf[i] = in[base + i];
+    for (int i = threadIdx.x; i < nb; i += PK_THREADS) {
+      const u64 key = in[base + i];
+      if (key > kth) buf[atomicAdd(&s_nbuf, 1)] = key;
+    }
     __syncthreads();
-    merge_topk(buf, nb, top, &s_ntop, p.k);
+    const int n = s_nbuf;
+    if (n > 0) {
+      merge_topk(buf, n, top, &s_ntop, p.k);
+      if (threadIdx.x == 0) s_nbuf = 0;
+      __syncthreads();
+    }
   }
   const int ntop = s_ntop;
   ld_peak *out = p.peaks + static_cast<int64_t>(f) * p.k;
@@ -171,14 +189,183 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksPara
   if (threadIdx.x == 0) p.n_peaks[f] = s_nz;
 }
 
-size_t peaks_workspace_bytes(int batch, int n_theta, int k) {
-  const int nb = (n_theta + PK_ROWS - 1) / PK_ROWS;
-  return static_cast<size_t>(batch) * nb * k * sizeof(u64);
+// ---------------------------------------------------------------------------
+// Tiled kernel (the fast path).  CTA = PT_TR theta rows x tc rho columns of one
+// frame, blockDim = tch = tc + 2*half_rho loaded columns, HT = half_theta as a
+// template parameter so the column (theta-direction) maximum is computed in
+// registers with static indexing:
+//   1. thread j loads column c0 - hr + j for rows t0-HT .. t0+TR+HT (coalesced
+//      across threads), outside the accumulator = 0 (never a candidate, never
+//      beats a candidate, never ties one because candidates have votes >= 1);
+//   2. Cs[i][j] = max over the 2HT+1 rows around row i (theta window);
+//   3. owned cell (i, j) with v >= floor is a window maximum iff
+//      v >= Cs[i][j-hr .. j+hr]; tested nearest-first with early exit;
+//   4. a window maximum is a candidate iff no equal value sits at a lower
+//      (theta, rho) index inside its window (exact tie-break, rare path);
+//   5. candidates (at most one per (HT+1) x (hr+1) block of the tile, so the
+//      buffer is sized exactly) are sorted and the tile's best k written out.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ bool no_lower_equal(const uint32_t *A, int n_rho, int t, int r, uint32_t v,
+                                            int ht, int hr) {
+  const int ra = max(r - hr, 0);
+  for (int tt = max(t - ht, 0); tt <= t; ++tt) {
+    const uint32_t *row = A + static_cast<int64_t>(tt) * n_rho;
+    const int rb = (tt < t) ? min(r + hr, n_rho - 1) : r - 1;
+    for (int rr = ra; rr <= rb; ++rr)
+      if (__ldg(row + rr) == v) return false;
+  }
+  return true;
 }
 
-cudaError_t launch_peaks(const PeaksParams &p, cudaStream_t stream) {
-  dim3 g1(p.n_bands, p.batch);
-  peaks_band_kernel<<<g1, PK_THREADS, 0, stream>>>(p);
+template <int HT>
+__global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksParams p) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  const int tch = p.tch;
+  uint32_t *Cs = reinterpret_cast<uint32_t *>(psm);
+  u64 *buf = reinterpret_cast<u64 *>(psm + ((PT_TR * tch * 4 + 15) & ~15));
+  __shared__ int s_nbuf;
+
+  const int tile = blockIdx.x, f = blockIdx.y;
+  const int tt = tile / p.tiles_r, tr = tile - tt * p.tiles_r;
+  const int t0 = tt * PT_TR;
+  const int hr = p.half_rho;
+  const int j = threadIdx.x;
+  const int c = tr * p.tc - hr + j;  // global rho column of this thread
+  const uint32_t *A = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
+
+  constexpr int NV = PT_TR + 2 * HT;
+  uint32_t v[NV];
+  const bool cin = c >= 0 && c < p.n_rho;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const int t = t0 - HT + q;
+    v[q] = (cin && t >= 0 && t < p.n_theta) ? __ldg(A + static_cast<int64_t>(t) * p.n_rho + c) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < PT_TR; ++i) {
+    uint32_t m = v[i];
+#pragma unroll
+    for (int k = 1; k <= 2 * HT; ++k) m = max(m, v[i + k]);
+    Cs[i * tch + j] = m;
+  }
+  if (j == 0) s_nbuf = 0;
+  __syncthreads();
+
+  if (j >= hr && j < hr + p.tc && c < p.n_rho) {
+#pragma unroll
+    for (int i = 0; i < PT_TR; ++i) {
+      const int t = t0 + i;
+      const uint32_t vv = v[i + HT];
+      if (t < p.n_theta && vv >= p.floor_votes) {
+        const uint32_t *crow = Cs + i * tch + j;
+        bool ok = crow[0] <= vv;
+        for (int d = 1; ok && d <= hr; ++d) ok = (crow[d] <= vv) && (crow[-d] <= vv);
+        if (ok) ok = no_lower_equal(A, p.n_rho, t, c, vv, HT, hr);
+        if (ok) {
+          const int slot = atomicAdd(&s_nbuf, 1);
+          buf[slot] = mk_key(vv, static_cast<uint32_t>(t * p.n_rho + c));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int n = s_nbuf;
+  u64 *out = p.band_keys + (static_cast<int64_t>(f) * p.n_units + tile) * p.k;
+  if (n > p.k) {
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int i = n + threadIdx.x; i < np2; i += blockDim.x) buf[i] = 0ull;
+    __syncthreads();
+    bitonic_desc(buf, np2);
+  }
+  for (int i = threadIdx.x; i < p.k; i += blockDim.x) out[i] = i < n ? buf[i] : 0ull;
+}
+
+typedef void (*TileKernel)(const PeaksParams);
+static TileKernel tile_kernel(int ht) {
+  switch (ht) {
+    case 0: return peaks_tile_kernel<0>;
+    case 1: return peaks_tile_kernel<1>;
+    case 2: return peaks_tile_kernel<2>;
+    case 3: return peaks_tile_kernel<3>;
+    case 4: return peaks_tile_kernel<4>;
+    case 5: return peaks_tile_kernel<5>;
+    case 6: return peaks_tile_kernel<6>;
+    case 7: return peaks_tile_kernel<7>;
+    case 8: return peaks_tile_kernel<8>;
+    case 9: return peaks_tile_kernel<9>;
+    case 10: return peaks_tile_kernel<10>;
+    case 11: return peaks_tile_kernel<11>;
+    case 12: return peaks_tile_kernel<12>;
+    default: return nullptr;
+  }
+}
+
+// Tile geometry for a window; returns false when the generic band kernel must be used.
+bool peaks_tile_plan(int n_theta, int n_rho, int half_theta, int half_rho, int k, PeaksParams *p,
+                     size_t *smem) {
+  if (half_theta > PT_MAX_HT) return false;
+  int best_tch = 0, best_tc = 0;
+  double best = 1e30;
+  for (int tch = 128; tch <= PT_MAX_THREADS; tch *= 2) {
+    const int tc = tch - 2 * half_rho;
+    if (tc < 32) continue;
+    const double cost = static_cast<double>(tch) / tc + (tch < 256 ? 0.25 : 0.0);
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_tch = tch;
+      best_tc = tc;
+    }
+  }
+  if (!best_tch) return false;
+  const int cand = ((PT_TR + half_theta) / (half_theta + 1)) *
+                   ((best_tc + half_rho) / (half_rho + 1));
+  int np2 = 1;
+  while (np2 < cand) np2 <<= 1;
+  if (np2 < 1) np2 = 1;
+  const size_t bytes = static_cast<size_t>((PT_TR * best_tch * 4 + 15) & ~15) + sizeof(u64) * np2;
+  if (bytes > 200 * 1024) return false;
+  p->tch = best_tch;
+  p->tc = best_tc;
+  p->tiles_t = (n_theta + PT_TR - 1) / PT_TR;
+  p->tiles_r = (n_rho + best_tc - 1) / best_tc;
+  p->n_units = p->tiles_t * p->tiles_r;
+  *smem = bytes;
+  (void)k;
+  return true;
+}
+
+size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k) {
+  // worst case over both kernels: tiles with tc >= 32, or bands of PK_ROWS rows
+  const size_t tiles = static_cast<size_t>((n_theta + PT_TR - 1) / PT_TR) * ((n_rho + 31) / 32);
+  const size_t bands = static_cast<size_t>((n_theta + PK_ROWS - 1) / PK_ROWS);
+  return static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
+}
+
+static bool g_tile_attr[64][PT_MAX_HT + 1];
+
+cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
+  PeaksParams p = p_in;
+  size_t smem = 0;
+  const char *env = getenv("LD_PEAKS_KERNEL");
+  const bool force_band = env && env[0] == 'b';
+  if (!force_band && peaks_tile_plan(p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, &p, &smem)) {
+    TileKernel kern = tile_kernel(p.half_theta);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!g_tile_attr[dev & 63][p.half_theta]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           200 * 1024);
+      if (e != cudaSuccess) return e;
+      g_tile_attr[dev & 63][p.half_theta] = true;
+    }
+    dim3 g1(p.n_units, p.batch);
+    kern<<<g1, p.tch, smem, stream>>>(p);
+  } else {
+    p.n_units = (p.n_theta + PK_ROWS - 1) / PK_ROWS;
+    dim3 g1(p.n_units, p.batch);
+    peaks_band_kernel<<<g1, PK_THREADS, 0, stream>>>(p);
+  }
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -19,11 +19,12 @@
 //    processed per 32-bit register as 16-bit lanes (SWAR): each lane of
 //    A + 2048 - T2 lies in [517, 2813], so bit 11 of each half is the
 //    comparison result and no carry ever crosses a half.
-//  * Compaction: per-thread popcount, warp shuffle scan, one counter
-//    reservation (atomicAdd on the frame's edge counter) per tile, then each
-//    thread writes its edges.  Inside a tile the order is permuted
-//    (q -> q*P mod total) so that consecutive list entries come from distant
-//    pixels -- this spreads the voting kernel's shared-memory addresses.
+//  * Compaction: per-thread popcount, a CTA scan in 16x16-cell order, one
+//    counter reservation (atomicAdd on the frame's edge counter) per tile,
+//    whose round trip is hidden by writing each tile's edges one iteration
+//    late.  The cell order makes every 32 consecutive list entries spatially
+//    compact: the voting kernel's warps then hit few, consecutive rho bins
+//    (distinct shared-memory banks; same-bin lanes merge in ATOMS.POPC.INC).
 #include "ld_internal.cuh"
 
 namespace ld {
@@ -84,20 +85,43 @@ __device__ __forceinline__ uint32_t sobel_row(const RowV &u, const RowV &m, cons
   return all;
 }
 
+__device__ __forceinline__ void write_edges(const SobelParams &p, const uint32_t masks[SB_SR],
+                                            int f, int ybase, int xs, uint32_t off) {
+  uint32_t *dst = p.edges + static_cast<int64_t>(f) * p.edge_stride + off;
+#pragma unroll
+  for (int i = 0; i < SB_SR; ++i) {
+    uint32_t m = masks[i];
+    const uint32_t yy = static_cast<uint32_t>(ybase + i) << 16;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      *dst++ = yy | static_cast<uint32_t>(xs + 4 * (b & 7) + (b >> 3));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(SB_THREADS, SB_CTAS_PER_SM)
     sobel_binarize_compact_kernel(const __grid_constant__ CUtensorMap tmap,
                                   const SobelParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
+  constexpr int NW = SB_THREADS / 32;
   __shared__ __align__(8) uint64_t full_bar[SB_STAGES];
-  __shared__ uint32_t s_warp[SB_THREADS / 32];
-  __shared__ uint32_t s_base, s_total;
+  __shared__ uint32_t s_cnt[SB_THREADS];        // per-thread counts, in cell order
+  __shared__ uint32_t s_excl[2][SB_THREADS];    // exclusive scan inside each warp
+  __shared__ uint32_t s_wt[NW];                 // warp totals
+  __shared__ uint32_t s_wbase[2][NW];           // exclusive scan of warp totals
+  __shared__ uint32_t s_base[2];                // frame-list base of the tile
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int chunk = tid % SB_CHUNKS;
   const int strip = tid / SB_CHUNKS;
+  // List order inside a tile: 16x16-pixel cells (4 strips of one chunk), cells
+  // row-major.  32 consecutive list entries then span a compact region, so a
+  // warp of the voting kernel hits <= ~32 consecutive rho bins per theta.
+  const int ord = ((strip >> 2) * SB_CHUNKS + chunk) * 4 + (strip & 3);
   const uint32_t k0 = static_cast<uint32_t>(2048 - p.t2) * 0x00010001u;
 
   auto issue = [&](int tile, int stage) {
@@ -123,10 +147,17 @@ __global__ void __launch_bounds__(SB_THREADS, SB_CTAS_PER_SM)
     }
   }
 
+  // previous tile, written one iteration late so that the counter
+  // reservation (a global atomic round trip) overlaps the next tile's work
+  uint32_t pmask[SB_SR] = {0u, 0u, 0u, 0u};
+  int pf = 0, pybase = 0, pxs = 0;
+  uint32_t base_reg = 0;  // thread 0: reservation result of the previous tile
+
   int it = 0;
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const int stage = it % SB_STAGES;
     const uint32_t parity = (it / SB_STAGES) & 1;
+    const int cb = it & 1, pb = cb ^ 1;
     const int f = tile / p.tiles_per_frame;
     const int rem = tile - f * p.tiles_per_frame;
     const int ty = rem / p.tiles_x;
@@ -183,56 +214,54 @@ __global__ void __launch_bounds__(SB_THREADS, SB_CTAS_PER_SM)
         r1 = r2;
       }
     }
-
-    // ---- compaction: one counter reservation per tile ----
     uint32_t cnt = 0;
 #pragma unroll
     for (int i = 0; i < SB_SR; ++i) cnt += __popc(masks[i]);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();  // (A): every thread is done reading this stage
+    s_cnt[ord] = cnt;
+    if (tid == 0 && it > 0) s_base[pb] = base_reg;
+    __syncthreads();  // (A): stage consumed, counts and previous base visible
     if (tid == 0) {
-      uint32_t acc = 0;
-#pragma unroll
-      for (int w = 0; w < SB_THREADS / 32; ++w) {
-        const uint32_t t = s_warp[w];
-        s_warp[w] = acc;
-        acc += t;
-      }
-      s_total = acc;
-      s_base = acc ? atomicAdd(&p.counts[f], acc) : 0u;
       const int next = tile + SB_STAGES * gridDim.x;
       if (next < p.n_tiles) issue(next, stage);
     }
-    __syncthreads();  // (B)
-    const uint32_t total = s_total;
-    if (p.edges != nullptr && cnt != 0) {
-      uint32_t *dst = p.edges + static_cast<int64_t>(f) * p.edge_stride + s_base;
-      const uint32_t q0 = s_warp[warp] + incl - cnt;  // rank of my first edge in the tile
-      uint32_t P = 1, pos = q0;
-      if (p.scatter) {
-        P = (total % 97u) ? 97u : (total % 89u) ? 89u : (total % 83u) ? 83u : 79u;
-        P %= total;
-        pos = static_cast<uint32_t>((static_cast<uint64_t>(q0) * P) % total);
-      }
+    if (it > 0 && p.edges != nullptr) {
+      const uint32_t off = s_base[pb] + s_wbase[pb][ord >> 5] + s_excl[pb][ord];
+      write_edges(p, pmask, pf, pybase, pxs, off);
+    }
+    {  // scan of this tile's counts in cell order
+      const uint32_t x = s_cnt[tid];
+      uint32_t incl = x;
 #pragma unroll
-      for (int i = 0; i < SB_SR; ++i) {
-        uint32_t m = masks[i];
-        const uint32_t yy = static_cast<uint32_t>(ybase + i) << 16;
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          const uint32_t x = static_cast<uint32_t>(xs + 4 * (b & 7) + (b >> 3));
-          dst[pos] = yy | x;
-          pos += P;
-          if (pos >= total) pos -= total;
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
       }
+      s_excl[cb][tid] = incl - x;
+      if (lane == 31) s_wt[warp] = incl;
+    }
+    __syncthreads();  // (B)
+    if (tid == 0) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        s_wbase[cb][w] = acc;
+        acc += s_wt[w];
+      }
+      base_reg = acc ? atomicAdd(&p.counts[f], acc) : 0u;  // consumed next iteration
+    }
+#pragma unroll
+    for (int i = 0; i < SB_SR; ++i) pmask[i] = masks[i];
+    pf = f;
+    pybase = ybase;
+    pxs = xs;
+  }
+  if (it > 0) {
+    const int pb = (it - 1) & 1;
+    if (tid == 0) s_base[pb] = base_reg;
+    __syncthreads();
+    if (p.edges != nullptr) {
+      const uint32_t off = s_base[pb] + s_wbase[pb][ord >> 5] + s_excl[pb][ord];
+      write_edges(p, pmask, pf, pybase, pxs, off);
     }
   }
 }

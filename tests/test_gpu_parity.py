@@ -324,3 +324,31 @@ def test_banded_accumulators_sum_to_whole(ld, oracle):
             total = acc if total is None else total + acc
         torch.cuda.synchronize()
         assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want), n
+
+
+@pytest.mark.parametrize("kernel", ["tile", "band"])
+def test_peaks_both_kernels_windows(ld, oracle, kernel, monkeypatch):
+    # the tiled kernel (half_theta <= 12, tc >= 32) and the generic band kernel
+    # (forced, or chosen for large windows) agree with the oracle
+    if kernel == "band":
+        monkeypatch.setenv("LD_PEAKS_KERNEL", "band")
+    rng = np.random.default_rng(31)
+    for trial, (ht, hr) in enumerate([(0, 0), (0, 5), (1, 1), (2, 29), (7, 44), (10, 116),
+                                      (12, 3), (13, 2), (3, 240), (20, 300)]):
+        acc = rng.integers(0, 6, size=(2, 61, 1201)).astype(np.uint32)
+        acc[1, 30, 600] = 50      # one dominant peak
+        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, 16)
+        torch.cuda.synchronize()
+        for f in range(2):
+            want, wn = oracle.hough_peaks(acc[f], ht, hr, 1, 16)
+            assert int(npk[f]) == wn, (kernel, ht, hr, f)
+            assert peak_tuples(peaks[f].cpu()) == oracle_peak_tuples(want), (kernel, ht, hr, f)
+
+
+def test_peaks_many_tiles_merge(ld, oracle):
+    # cfg5-like geometry: thousands of tile lists merged per frame
+    rng = np.random.default_rng(5)
+    acc = rng.integers(0, 30, size=(1, 1024, 2001)).astype(np.uint32)
+    peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), 10, 116, 1, 64)
+    want, wn = oracle.hough_peaks(acc[0], 10, 116, 1, 64)
+    assert int(npk[0]) == wn and peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(want)
