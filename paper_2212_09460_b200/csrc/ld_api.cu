@@ -166,7 +166,9 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
   cuuint64_t gdim[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(rows_read),
                         static_cast<cuuint64_t>(img->batch)};
   cuuint64_t gstride[2] = {static_cast<cuuint64_t>(img->pitch), static_cast<cuuint64_t>(fstride)};
-  cuuint32_t box[3] = {SB_BOX_W, SB_BOX_H, 1};
+  const SobelCfg cfg = sobel_cfg();
+  const int tile_h = cfg.sr * SB_STRIPS;
+  cuuint32_t box[3] = {SB_BOX_W, static_cast<cuuint32_t>(tile_h + 2), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult cr = g_encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(gray),
                          gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -181,7 +183,7 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
   p.row_end = img->row_end;
   p.ry0 = ry0;
   p.tiles_x = (W + SB_TILE_W - 1) / SB_TILE_W;
-  p.tiles_y = (img->row_end - img->row_begin + SB_TILE_H - 1) / SB_TILE_H;
+  p.tiles_y = (img->row_end - img->row_begin + tile_h - 1) / tile_h;
   p.tiles_per_frame = p.tiles_x * p.tiles_y;
   const int64_t n_tiles = static_cast<int64_t>(p.tiles_per_frame) * img->batch;
   if (n_tiles > (1ll << 30)) return fail(LD_ERR_INVALID_ARG, "batch too large");
@@ -198,9 +200,7 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
 
   cudaError_t e = cudaMemsetAsync(edge_count, 0, sizeof(uint32_t) * img->batch, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(edge_count)");
-  const int64_t max_ctas = static_cast<int64_t>(dev.sm_count) * SB_CTAS_PER_SM;
-  const int n_ctas = static_cast<int>(n_tiles < max_ctas ? n_tiles : max_ctas);
-  e = launch_sobel(tmap, p, n_ctas, stream);
+  e = launch_sobel(tmap, p, dev.sm_count, stream);
   if (e != cudaSuccess) return cuda_fail(e, "sobel_binarize_compact_kernel launch");
   return LD_OK;
 }
@@ -215,7 +215,7 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   const int32_t d = rho_offset(width, height);
   if ((rc = check_trig(n_theta, cos_q15, sin_q15, width, height, d))) return rc;
   const int n_rho = 2 * d + 1;
-  const size_t limit = static_cast<size_t>(dev.smem_optin) - sizeof(int2) * HV_MAX_ROWS - 1024;
+  const size_t limit = static_cast<size_t>(dev.smem_optin) - sizeof(uint4) * HV_MAX_ROWS - 1024;
   int n_bands = 0;
   const int rpb = hough_rows_per_band(n_theta, n_rho, limit, &n_bands);
   if (rpb < 1) return fail(LD_ERR_UNSUPPORTED, "one accumulator row (%d bins) exceeds shared memory", n_rho);

@@ -21,7 +21,7 @@ namespace ld {
 __global__ void __launch_bounds__(HV_THREADS, 1)
     hough_vote_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
   extern __shared__ __align__(16) uint32_t slice[];
-  __shared__ int2 cs[HV_MAX_ROWS];
+  __shared__ uint4 rowk[HV_MAX_ROWS];  // per row: C, S, K = koff + (row address << 13)
 
   const int tid = threadIdx.x;
   const int band = blockIdx.x;
@@ -29,60 +29,59 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   const int t0 = band * p.rows_per_band;
   const int nr = min(p.rows_per_band, p.n_theta - t0);
   const int ncell = nr * p.n_rho;
+  const uint32_t sbase = smem_u32(slice);
+  const uint32_t row_bytes = static_cast<uint32_t>(p.n_rho) * 4u;
 
   {
     uint4 *s4 = reinterpret_cast<uint4 *>(slice);
     const int n4 = (ncell + 3) >> 2;
     for (int i = tid; i < n4; i += HV_THREADS) s4[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (int i = tid; i < nr; i += HV_THREADS) cs[i] = make_int2(trig.c[t0 + i], trig.s[t0 + i]);
+    // The byte address of the counter of (row r, bin rho) is
+    //   sbase + r*row_bytes + 4*rho = ((v + ((sbase + r*row_bytes) << 13)) >> 13) & ~3
+    // with v = x*C + y*S + koff in [0, 2^31) (host range proof) and the row
+    // address < 2^18, so the folded sum stays below 2^32: exact in uint32.
+    for (int i = tid; i < nr; i += HV_THREADS)
+      rowk[i] = make_uint4(static_cast<uint32_t>(trig.c[t0 + i]), static_cast<uint32_t>(trig.s[t0 + i]),
+                           static_cast<uint32_t>(p.koff) + ((sbase + i * row_bytes) << 13), 0u);
   }
   __syncthreads();
 
   const uint32_t n_edges = p.counts[f];
   const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
-  const uint32_t sbase = smem_u32(slice);
-  const uint32_t row_bytes = static_cast<uint32_t>(p.n_rho) * 4u;
-  const int koff = p.koff;
 
-  // Each warp takes blocks of 128 consecutive list entries; at step j its 32
+  // Each warp takes blocks of 256 consecutive list entries; at step j its 32
   // lanes hold the 32 consecutive entries blk + 32j + lane, which the
   // compaction made spatially compact (ld_sobel.cu): per theta they fall into
   // few consecutive rho bins, i.e. distinct banks, and equal bins merge.
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = HV_THREADS / 32;
-  for (uint32_t blk = static_cast<uint32_t>(warp) * 128u; blk < n_edges; blk += NWARPS * 128u) {
-    int xs[4], ys[4];
-    bool ok[4];
+  constexpr int EPL = 8;  // edges per lane per block
+  for (uint32_t blk = static_cast<uint32_t>(warp) * (32u * EPL); blk < n_edges;
+       blk += NWARPS * 32u * EPL) {
+    uint32_t xs[EPL], ys[EPL];
+    bool ok[EPL];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < EPL; ++j) {
       const uint32_t e = blk + 32u * j + lane;
       ok[j] = e < n_edges;
       const uint32_t q = ok[j] ? __ldg(el + e) : 0u;
-      xs[j] = static_cast<int>(q & 0xFFFFu);
-      ys[j] = static_cast<int>(q >> 16);
+      xs[j] = q & 0xFFFFu;
+      ys[j] = q >> 16;
     }
-    if (blk + 128u <= n_edges) {
+    if (blk + 32u * EPL <= n_edges) {
 #pragma unroll 2
       for (int r = 0; r < nr; ++r) {
-        const int2 c = cs[r];
-        const uint32_t rowb = sbase + static_cast<uint32_t>(r) * row_bytes;
+        const uint4 k = rowk[r];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int v = xs[j] * c.x + ys[j] * c.y + koff;
-          red_shared_add(rowb + (static_cast<uint32_t>(v >> 15) << 2), 1u);
-        }
+        for (int j = 0; j < EPL; ++j)
+          red_shared_add(((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u, 1u);
       }
     } else {
       for (int r = 0; r < nr; ++r) {
-        const int2 c = cs[r];
-        const uint32_t rowb = sbase + static_cast<uint32_t>(r) * row_bytes;
+        const uint4 k = rowk[r];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (ok[j]) {
-            const int v = xs[j] * c.x + ys[j] * c.y + koff;
-            red_shared_add(rowb + (static_cast<uint32_t>(v >> 15) << 2), 1u);
-          }
-        }
+        for (int j = 0; j < EPL; ++j)
+          if (ok[j]) red_shared_add(((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u, 1u);
       }
     }
   }
@@ -111,7 +110,7 @@ cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, size_t sme
   if (!g_hough_attr[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(hough_vote_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024 - static_cast<int>(sizeof(int2)) * HV_MAX_ROWS);
+                                         227 * 1024 - static_cast<int>(sizeof(uint4)) * HV_MAX_ROWS);
     if (e != cudaSuccess) return e;
     g_hough_attr[dev & 63] = true;
   }

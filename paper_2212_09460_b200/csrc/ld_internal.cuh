@@ -17,14 +17,15 @@ constexpr int SB_BOX_W = 256;       // TMA box width in bytes (hardware max 256)
 constexpr int SB_HALO_L = 16;       // box starts 16 columns left of the tile
 constexpr int SB_CHUNKS = 14;       // 16-px output chunks per tile row
 constexpr int SB_TILE_W = SB_CHUNKS * 16;  // 224 output columns per tile
-constexpr int SB_SR = 4;            // output rows per thread strip
-constexpr int SB_STRIPS = 16;       // strips per tile
-constexpr int SB_TILE_H = SB_SR * SB_STRIPS;  // 64 output rows per tile
-constexpr int SB_BOX_H = SB_TILE_H + 2;       // + 1-row halo above and below
+constexpr int SB_STRIPS = 16;       // thread strips per tile (vertical)
 constexpr int SB_THREADS = SB_CHUNKS * SB_STRIPS;  // 224 = 7 warps
-constexpr int SB_STAGES = 4;
-constexpr int SB_STAGE_BYTES = SB_BOX_W * SB_BOX_H;  // 16896 = 132 * 128
-constexpr int SB_CTAS_PER_SM = 3;
+
+// compile-time variants: SR output rows per strip (tile height 16*SR), TMA ring
+// depth, CTAs per SM; selected on the host (LD_SOBEL_CFG=4 picks the SR=4 one)
+struct SobelCfg {
+  int sr, stages, ctas_per_sm;
+};
+SobelCfg sobel_cfg();
 
 struct SobelParams {
   int32_t width, height;
@@ -40,7 +41,7 @@ struct SobelParams {
   uint32_t *counts;
 };
 
-cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int n_ctas,
+cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_count,
                          cudaStream_t stream);
 
 // ---------------------------------------------------------------------------

@@ -201,28 +201,20 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksPara
 //   3. owned cell (i, j) with v >= floor is a window maximum iff
 //      v >= Cs[i][j-hr .. j+hr]; tested nearest-first with early exit;
 //   4. a window maximum is a candidate iff no equal value sits at a lower
-//      (theta, rho) index inside its window (exact tie-break, rare path);
+//      (theta, rho) index inside its window (exact tie-break); only columns
+//      whose theta-window maximum equals v can hold such a value, and only
+//      those are scanned (the value tile Vs is kept in shared memory);
 //   5. candidates (at most one per (HT+1) x (hr+1) block of the tile, so the
 //      buffer is sized exactly) are sorted and the tile's best k written out.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ bool no_lower_equal(const uint32_t *A, int n_rho, int t, int r, uint32_t v,
-                                            int ht, int hr) {
-  const int ra = max(r - hr, 0);
-  for (int tt = max(t - ht, 0); tt <= t; ++tt) {
-    const uint32_t *row = A + static_cast<int64_t>(tt) * n_rho;
-    const int rb = (tt < t) ? min(r + hr, n_rho - 1) : r - 1;
-    for (int rr = ra; rr <= rb; ++rr)
-      if (__ldg(row + rr) == v) return false;
-  }
-  return true;
-}
-
 template <int HT>
 __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksParams p) {
   extern __shared__ __align__(16) unsigned char psm[];
+  constexpr int NV = PT_TR + 2 * HT;
   const int tch = p.tch;
-  uint32_t *Cs = reinterpret_cast<uint32_t *>(psm);
-  u64 *buf = reinterpret_cast<u64 *>(psm + ((PT_TR * tch * 4 + 15) & ~15));
+  uint32_t *Vs = reinterpret_cast<uint32_t *>(psm);  // [NV][tch] values
+  uint32_t *Cs = Vs + NV * tch;                       // [PT_TR][tch] theta-window max
+  u64 *buf = reinterpret_cast<u64 *>(psm + (((NV + PT_TR) * tch * 4 + 15) & ~15));
   __shared__ int s_nbuf;
 
   const int tile = blockIdx.x, f = blockIdx.y;
@@ -233,7 +225,6 @@ __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksP
   const int c = tr * p.tc - hr + j;  // global rho column of this thread
   const uint32_t *A = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
 
-  constexpr int NV = PT_TR + 2 * HT;
   uint32_t v[NV];
   const bool cin = c >= 0 && c < p.n_rho;
 #pragma unroll
@@ -241,6 +232,8 @@ __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksP
     const int t = t0 - HT + q;
     v[q] = (cin && t >= 0 && t < p.n_theta) ? __ldg(A + static_cast<int64_t>(t) * p.n_rho + c) : 0u;
   }
+#pragma unroll
+  for (int q = 0; q < NV; ++q) Vs[q * tch + j] = v[q];
 #pragma unroll
   for (int i = 0; i < PT_TR; ++i) {
     uint32_t m = v[i];
@@ -258,9 +251,21 @@ __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksP
       const uint32_t vv = v[i + HT];
       if (t < p.n_theta && vv >= p.floor_votes) {
         const uint32_t *crow = Cs + i * tch + j;
+        // own column: a larger value anywhere, or an equal value in an earlier row
         bool ok = crow[0] <= vv;
-        for (int d = 1; ok && d <= hr; ++d) ok = (crow[d] <= vv) && (crow[-d] <= vv);
-        if (ok) ok = no_lower_equal(A, p.n_rho, t, c, vv, HT, hr);
+#pragma unroll
+        for (int k = 0; k < HT; ++k) ok = ok && (v[i + k] != vv);
+        for (int d = 1; ok && d <= hr; ++d) {
+          const uint32_t cl = crow[-d], cr = crow[d];
+          ok = (cl <= vv) && (cr <= vv);
+          if (ok && cl == vv) {  // rare: equal value in a column to the left
+            // lower index there = rows t-HT .. t (same or earlier theta)
+            for (int q = i; q <= i + HT && ok; ++q) ok = Vs[q * tch + j - d] != vv;
+          }
+          if (ok && cr == vv) {  // rare: equal value to the right: rows t-HT .. t-1
+            for (int q = i; q < i + HT && ok; ++q) ok = Vs[q * tch + j + d] != vv;
+          }
+        }
         if (ok) {
           const int slot = atomicAdd(&s_nbuf, 1);
           buf[slot] = mk_key(vv, static_cast<uint32_t>(t * p.n_rho + c));
@@ -323,7 +328,8 @@ bool peaks_tile_plan(int n_theta, int n_rho, int half_theta, int half_rho, int k
   int np2 = 1;
   while (np2 < cand) np2 <<= 1;
   if (np2 < 1) np2 = 1;
-  const size_t bytes = static_cast<size_t>((PT_TR * best_tch * 4 + 15) & ~15) + sizeof(u64) * np2;
+  const size_t bytes =
+      static_cast<size_t>(((2 * PT_TR + 2 * half_theta) * best_tch * 4 + 15) & ~15) + sizeof(u64) * np2;
   if (bytes > 200 * 1024) return false;
   p->tch = best_tch;
   p->tc = best_tc;
