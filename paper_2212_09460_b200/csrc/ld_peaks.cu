@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksPara
 //      beats a candidate, never ties one because candidates have votes >= 1);
 //   2. Cs[i][j] = max over the 2HT+1 rows around row i (theta window);
 //   3. owned cell (i, j) with v >= floor is a window maximum iff
-//      v >= Cs[i][j-hr .. j+hr]; tested nearest-first with early exit;
+//      v >= Cs[i][j-hr .. j+hr].  A branch-free prefilter (v == Cs[i][j] and
+//      v >= Cs[i][j +- 1..2]) keeps ~1/25 of the cells of a noisy
+//      accumulator; the survivors are compacted with warp ballots and only
+//      they run the full test (nearest-first, early exit);
 //   4. a window maximum is a candidate iff no equal value sits at a lower
 //      (theta, rho) index inside its window (exact tie-break); only columns
 //      whose theta-window maximum equals v can hold such a value, and only
@@ -211,27 +214,36 @@ template <int HT>
 __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksParams p) {
   extern __shared__ __align__(16) unsigned char psm[];
   constexpr int NV = PT_TR + 2 * HT;
+  constexpr int PF = 2;  // prefilter radius in rho
   const int tch = p.tch;
-  uint32_t *Vs = reinterpret_cast<uint32_t *>(psm);  // [NV][tch] values
-  uint32_t *Cs = Vs + NV * tch;                       // [PT_TR][tch] theta-window max
-  u64 *buf = reinterpret_cast<u64 *>(psm + (((NV + PT_TR) * tch * 4 + 15) & ~15));
-  __shared__ int s_nbuf;
+  uint32_t *Vs = reinterpret_cast<uint32_t *>(psm);   // [NV][tch] values
+  uint32_t *Cs = Vs + NV * tch;                        // [PT_TR][tch] theta-window max
+  uint16_t *surv = reinterpret_cast<uint16_t *>(Cs + PT_TR * tch);  // [PT_TR*tch]
+  u64 *buf = reinterpret_cast<u64 *>(
+      psm + (((NV + PT_TR) * tch * 4 + PT_TR * tch * 2 + 15) & ~15));
+  __shared__ int s_nbuf, s_nsurv;
 
   const int tile = blockIdx.x, f = blockIdx.y;
   const int tt = tile / p.tiles_r, tr = tile - tt * p.tiles_r;
   const int t0 = tt * PT_TR;
   const int hr = p.half_rho;
   const int j = threadIdx.x;
+  const int lane = j & 31;
   const int c = tr * p.tc - hr + j;  // global rho column of this thread
-  const uint32_t *A = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
+  const int n_rho = p.n_rho;
 
+  // ---- phase A: column values (registers + smem) and theta-window maxima
   uint32_t v[NV];
-  const bool cin = c >= 0 && c < p.n_rho;
+  {
+    const bool cin = c >= 0 && c < n_rho;
+    const uint32_t *col = p.acc + (static_cast<int64_t>(f) * p.n_theta + (t0 - HT)) * n_rho + c;
 #pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    const int t = t0 - HT + q;
-    v[q] = (cin && t >= 0 && t < p.n_theta) ? __ldg(A + static_cast<int64_t>(t) * p.n_rho + c) : 0u;
+    for (int q = 0; q < NV; ++q) {
+      const int t = t0 - HT + q;
+      v[q] = (cin && t >= 0 && t < p.n_theta) ? __ldg(col + static_cast<int64_t>(q) * n_rho) : 0u;
+    }
   }
+  uint32_t cm[PT_TR];
 #pragma unroll
   for (int q = 0; q < NV; ++q) Vs[q * tch + j] = v[q];
 #pragma unroll
@@ -239,38 +251,63 @@ __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksP
     uint32_t m = v[i];
 #pragma unroll
     for (int k = 1; k <= 2 * HT; ++k) m = max(m, v[i + k]);
+    cm[i] = m;
     Cs[i * tch + j] = m;
   }
-  if (j == 0) s_nbuf = 0;
+  if (j == 0) {
+    s_nbuf = 0;
+    s_nsurv = 0;
+  }
   __syncthreads();
 
-  if (j >= hr && j < hr + p.tc && c < p.n_rho) {
+  // ---- phase B: branch-free prefilter, survivors compacted with warp ballots.
+  // A candidate is the maximum of its window, so in particular of its own
+  // theta-window column (v == cm) and of the columns within PF.
+  const bool owned = j >= hr && j < hr + p.tc && c < n_rho;
+  const int pf = hr < PF ? hr : PF;
 #pragma unroll
-    for (int i = 0; i < PT_TR; ++i) {
-      const int t = t0 + i;
-      const uint32_t vv = v[i + HT];
-      if (t < p.n_theta && vv >= p.floor_votes) {
-        const uint32_t *crow = Cs + i * tch + j;
-        // own column: a larger value anywhere, or an equal value in an earlier row
-        bool ok = crow[0] <= vv;
+  for (int i = 0; i < PT_TR; ++i) {
+    const uint32_t vv = v[i + HT];
+    bool pass = owned && (t0 + i < p.n_theta) && vv >= p.floor_votes && vv == cm[i];
+    const uint32_t *crow = Cs + i * tch + j;
 #pragma unroll
-        for (int k = 0; k < HT; ++k) ok = ok && (v[i + k] != vv);
-        for (int d = 1; ok && d <= hr; ++d) {
-          const uint32_t cl = crow[-d], cr = crow[d];
-          ok = (cl <= vv) && (cr <= vv);
-          if (ok && cl == vv) {  // rare: equal value in a column to the left
-            // lower index there = rows t-HT .. t (same or earlier theta)
-            for (int q = i; q <= i + HT && ok; ++q) ok = Vs[q * tch + j - d] != vv;
-          }
-          if (ok && cr == vv) {  // rare: equal value to the right: rows t-HT .. t-1
-            for (int q = i; q < i + HT && ok; ++q) ok = Vs[q * tch + j + d] != vv;
-          }
-        }
-        if (ok) {
-          const int slot = atomicAdd(&s_nbuf, 1);
-          buf[slot] = mk_key(vv, static_cast<uint32_t>(t * p.n_rho + c));
-        }
+    for (int d = 1; d <= PF; ++d)
+      if (d <= pf) pass = pass && crow[owned ? -d : 0] <= vv && crow[owned ? d : 0] <= vv;
+    const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+    if (bal) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&s_nsurv, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (pass) surv[base + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>(i * tch + j);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase C: exact window test for the survivors
+  const int nsurv = s_nsurv;
+  for (int s = threadIdx.x; s < nsurv; s += blockDim.x) {
+    const int idx = surv[s];
+    const int i = idx / tch, jj = idx - i * tch;
+    const uint32_t vv = Vs[(i + HT) * tch + jj];
+    const uint32_t *crow = Cs + i * tch + jj;
+    bool ok = true;
+    // own column: an equal value in an earlier row of the window
+#pragma unroll
+    for (int k = 0; k < HT; ++k) ok = ok && Vs[(i + k) * tch + jj] != vv;
+    for (int d = 1; ok && d <= hr; ++d) {
+      const uint32_t cl = crow[-d], cr = crow[d];
+      ok = (cl <= vv) && (cr <= vv);
+      if (ok && cl == vv) {  // equal value to the left: lower index in rows t-HT .. t
+        for (int q = i; q <= i + HT && ok; ++q) ok = Vs[q * tch + jj - d] != vv;
       }
+      if (ok && cr == vv) {  // equal value to the right: lower index in rows t-HT .. t-1
+        for (int q = i; q < i + HT && ok; ++q) ok = Vs[q * tch + jj + d] != vv;
+      }
+    }
+    if (ok) {
+      const int t = t0 + i;
+      const int cc = tr * p.tc - hr + jj;
+      buf[atomicAdd(&s_nbuf, 1)] = mk_key(vv, static_cast<uint32_t>(t * n_rho + cc));
     }
   }
   __syncthreads();
@@ -329,7 +366,9 @@ bool peaks_tile_plan(int n_theta, int n_rho, int half_theta, int half_rho, int k
   while (np2 < cand) np2 <<= 1;
   if (np2 < 1) np2 = 1;
   const size_t bytes =
-      static_cast<size_t>(((2 * PT_TR + 2 * half_theta) * best_tch * 4 + 15) & ~15) + sizeof(u64) * np2;
+      static_cast<size_t>(((2 * PT_TR + 2 * half_theta) * best_tch * 4 + PT_TR * best_tch * 2 + 15) &
+                          ~15) +
+      sizeof(u64) * np2;
   if (bytes > 200 * 1024) return false;
   p->tch = best_tch;
   p->tc = best_tc;
