@@ -352,3 +352,46 @@ def test_peaks_many_tiles_merge(ld, oracle):
     peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), 10, 116, 1, 64)
     want, wn = oracle.hough_peaks(acc[0], 10, 116, 1, 64)
     assert int(npk[0]) == wn and peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(want)
+
+
+def test_banded_detector_ranks_emulated(ld, oracle):
+    # dist.BandedDetector for every rank of world N in one process (no process
+    # group: its allreduce is then the identity), partial accumulators summed
+    # here == whole-image oracle; world 1 gives the oracle's peaks directly
+    from paper_2212_09460_b200 import dist as pdist
+    cfg = synth.CONFIGS["cfg5"]
+    c, s = synth.q15_table(cfg.n_theta)
+    img = synth.gen_frame("cfg5", 0)
+    W = H = 4096
+    r = oracle.detect(img, cfg.threshold, c, s, cfg.half_theta, cfg.half_rho, cfg.min_votes,
+                      cfg.k)
+    for world in (1, 3, 8):
+        total = None
+        for rank in range(world):
+            det = pdist.BandedDetector(W, H, cfg.n_theta, c, s, cfg.threshold, cfg.k,
+                                       cfg.half_theta, cfg.half_rho, cfg.min_votes, rank, world)
+            det.load(img)
+            peaks, npk, acc, cnt = det()
+            part = acc.clone()
+            total = part if total is None else total + part
+        torch.cuda.synchronize()
+        assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], r["acc"]), world
+        if world == 1:
+            assert int(cnt[0]) == r["n_edges"]
+            assert int(npk[0]) == r["n_peaks"]
+            assert peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(r["peaks"])
+
+
+def test_banded_detector_more_ranks_than_rows(ld, oracle):
+    from paper_2212_09460_b200 import dist as pdist
+    img = synth.random_image(3, 50, 5, "uniform")
+    c, s = synth.q15_table(180)
+    want = oracle.hough_accumulate(oracle.compact(oracle.sobel_binarize(img, 200)), 50, 5, c, s)
+    total = None
+    for rank in range(8):
+        det = pdist.BandedDetector(50, 5, 180, c, s, 200, 4, 2, 8, 1, rank, 8)
+        det.load(img)
+        _, _, acc, _ = det()
+        total = acc.clone() if total is None else total + acc
+    torch.cuda.synchronize()
+    assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want)
