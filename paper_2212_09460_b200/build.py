@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC] + FLAGS + ["-o", tmp] + sources()
+    extra = ["-DLD_DEBUG=1"] if os.environ.get("LD_DEBUG") == "1" else []
+    cmd = [NVCC] + FLAGS + extra + ["-o", tmp] + sources()
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

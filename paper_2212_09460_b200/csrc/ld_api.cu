@@ -253,7 +253,10 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   p.floor_votes = min_votes > 1 ? min_votes : 1u;
   p.k = k;
   p.n_units = 0;
-  p.band_keys = static_cast<unsigned long long *>(workspace);
+  // workspace: [batch] uint32 per-frame thresholds (256-B padded), then the keys
+  p.gtau = static_cast<uint32_t *>(workspace);
+  p.band_keys = reinterpret_cast<unsigned long long *>(
+      static_cast<char *>(workspace) + align_up(sizeof(uint32_t) * static_cast<size_t>(batch), 256));
   p.peaks = peaks;
   p.n_peaks = n_peaks;
   (void)ws_bytes;

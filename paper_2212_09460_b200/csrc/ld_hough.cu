@@ -133,13 +133,17 @@ __global__ void __launch_bounds__(1024, 1)
   __syncthreads();
   const uint32_t base = smem_u32(buf);
   if (mode == 0) {
-    // conflict-free: lane l -> bank l, a different word every iteration
-    uint32_t row = static_cast<uint32_t>(warp) * 37u;
-#pragma unroll 8
-    for (int i = 0; i < iters; ++i) {
-      red_shared_add(base + ((lane + 32u * (row & 1023u)) << 2), 1u);
-      row += 1u;
+    // conflict-free, issue-free: lane l -> bank l, 32 distinct rows per
+    // unrolled group addressed by immediate offsets, so the instruction
+    // stream is (almost) pure ATOMS and the pipe itself is the limit
+    const uint32_t a = base + ((static_cast<uint32_t>(warp) * 32u + lane) << 2);
+    int i = 0;
+    for (; i + 32 <= iters; i += 32) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        red_shared_add(a + j * 4096u, 1u);
     }
+    for (; i < iters; ++i) red_shared_add(a, 1u);
   } else if (mode == 1) {
     uint32_t x = (blockIdx.x * 1024u + tid) * 2654435761u + 12345u;
 #pragma unroll 8

@@ -18,7 +18,8 @@ constexpr int SB_HALO_L = 16;       // box starts 16 columns left of the tile
 constexpr int SB_CHUNKS = 14;       // 16-px output chunks per tile row
 constexpr int SB_TILE_W = SB_CHUNKS * 16;  // 224 output columns per tile
 constexpr int SB_STRIPS = 16;       // thread strips per tile (vertical)
-constexpr int SB_THREADS = SB_CHUNKS * SB_STRIPS;  // 224 = 7 warps
+constexpr int SB_THREADS = SB_CHUNKS * SB_STRIPS;  // 224 = 7 consumer warps
+constexpr int SB_STAGE_CAP = 1024;  // per-warp edge staging buffer (uint32 entries)
 
 // compile-time variants: SR output rows per strip (tile height 16*SR), TMA ring
 // depth, CTAs per SM; selected on the host (LD_SOBEL_CFG=4 picks the SR=4 one)
@@ -87,7 +88,9 @@ struct PeaksParams {
   int32_t k;
   int32_t n_units;                // tiles (tiled kernel) or bands (generic) per frame
   int32_t tch, tc, tiles_t, tiles_r;  // tiled kernel geometry
+  int32_t st_nt, st_sw, st_strips, st_tb, st_chunks, st_buf;  // streaming kernel geometry
   unsigned long long *band_keys;  // [batch][n_units][k]
+  uint32_t *gtau;                 // [batch] per-frame running k-th candidate value (stream kernel)
   ld_peak *peaks;
   int32_t *n_peaks;
 };
@@ -126,11 +129,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  // try_wait with a suspend-time hint: the waiting thread sleeps in hardware
+  // until the phase completes (or the hint expires) instead of spinning on
+  // the issue slots other warps need
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "LD_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 0x989680;\n\t"
       "@!p bra LD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");

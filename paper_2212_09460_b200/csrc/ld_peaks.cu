@@ -23,6 +23,20 @@ namespace ld {
 
 typedef unsigned long long u64;
 
+// Debug builds (LD_DEBUG=1 python -m paper_2212_09460_b200.build): indexed
+// shared-memory writes of the streaming kernel are range-checked; a failed
+// check records its source line (first one wins) and the write is skipped.
+#ifdef LD_DEBUG
+__device__ int g_ld_debug_line;
+__device__ __forceinline__ bool ld_chk(bool ok, int line) {
+  if (!ok) atomicCAS(&g_ld_debug_line, 0, line);
+  return ok;
+}
+#define LD_CHK(c) ld_chk((c), __LINE__)
+#else
+#define LD_CHK(c) true
+#endif
+
 constexpr int PK_CHUNK = 2 * PK_THREADS;        // cells tested per round
 constexpr int PK_BUF = PK_CHUNK + LD_MAX_K;     // candidate buffer (power of 2)
 static_assert((PK_BUF & (PK_BUF - 1)) == 0, "PK_BUF must be a power of two");
@@ -323,6 +337,360 @@ __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksP
   for (int i = threadIdx.x; i < p.k; i += blockDim.x) out[i] = i < n ? buf[i] : 0ull;
 }
 
+
+// ---------------------------------------------------------------------------
+// Streaming kernel (the fast path, half_theta <= 12).  CTA = one rho strip of
+// st_sw owned columns x one chunk of st_tb theta rows of one frame; each of
+// the st_nt threads owns CPT columns (c0 - hr + tid + q*st_nt, coalesced),
+// streamed down the chunk's rows G at a time with the 2HT rows above kept in
+// registers, so every accumulator value is read from HBM once (plus the
+// 2HT-row chunk halo) and the theta-window column maximum costs 2HT register
+// max operations per cell.  Per candidate row: column maxima -> shared
+// memory; a cell can only be a window maximum if it equals its own column
+// maximum, and only matters if its votes reach the CTA's running k-th best
+// candidate (tau): such cells -- few -- scan the +-hr column maxima, then
+// resolve exact ties (equal values at a lower (theta, rho) index) from the
+// accumulator itself.  Candidates are merged into the CTA's top-k in shared
+// memory; peaks_merge_kernel merges the CTAs of a frame.
+// ---------------------------------------------------------------------------
+constexpr int PS_G = 4;  // rows per register group
+
+constexpr int PS_NT_MAX = 512;   // threads per CTA, one CTA per SM
+constexpr int PS_NT_MAX2 = 384;  // threads per CTA when two CTAs share an SM
+// register window (2 groups + 2HT rows) x CPT small enough for two CTAs per SM
+constexpr int ps_minb(int ht, int cpt) { return (2 * PS_G + 2 * ht) * cpt <= 48 ? 2 : 1; }
+
+template <int CPT>
+__device__ __forceinline__ void stream_store(uint32_t *dst, const uint32_t (&v)[CPT]) {
+  if constexpr (CPT == 4) {
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (CPT == 2) {
+    *reinterpret_cast<uint2 *>(dst) = make_uint2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) dst[q] = v[q];
+  }
+}
+
+// CTA = st_nt threads x CPT consecutive columns each; rows are read with
+// plain coalesced loads through a per-thread row pointer (immediate column
+// offsets), one group of PS_G rows ahead of the group being tested (register
+// double buffering), so HBM latency overlaps the arithmetic.  Columns outside
+// the accumulator are read through a clamped pointer and masked to 0.
+template <int HT, int CPT, int MINB>
+__global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
+    peaks_stream_kernel(const PeaksParams p) {
+  constexpr int NV = PS_G + 2 * HT;
+  static_assert(PS_G * CPT <= 32, "survivor mask");
+  extern __shared__ __align__(16) unsigned char psm[];
+  const int nt = p.st_nt;
+  const int width = nt * CPT;                          // loaded columns
+  uint32_t *CM = reinterpret_cast<uint32_t *>(psm);     // [PS_G][width] column maxima
+  uint32_t *RAW = CM + PS_G * width;                    // [PS_G + HT][width] rows g0-HT ..
+  u64 *top = reinterpret_cast<u64 *>(RAW + (PS_G + HT) * width);  // [k] (8-aligned: width even)
+  u64 *buf = top + p.k;                                 // [pow2(candidate bound + k)]
+  uint32_t *SL = reinterpret_cast<uint32_t *>(buf + p.st_buf);  // [PS_G * sw] survivors
+  __shared__ int s_nbuf, s_ntop, s_nsurv;
+  __shared__ uint32_t s_tau;
+
+  const int unit = blockIdx.x, f = blockIdx.y;
+  const int strip = unit / p.st_chunks, chunk = unit - strip * p.st_chunks;
+  const int hr = p.half_rho, n_rho = p.n_rho, n_theta = p.n_theta;
+  const int cbase = strip * p.st_sw - hr;  // global column of loaded column 0
+  const int tb0 = chunk * p.st_tb;
+  const int tb1 = min(tb0 + p.st_tb, n_theta);
+  const int tid = threadIdx.x;
+
+  const int j0 = tid * CPT;  // loaded columns j0 .. j0+CPT-1
+  const int col0 = cbase + j0;
+  const int colc = min(max(col0, 0), n_rho - CPT);  // clamped: every load in bounds
+  uint32_t cmask[CPT];
+  bool own[CPT];
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int col = col0 + q;
+    const bool in = col >= 0 && col < n_rho;
+    cmask[q] = in ? 0xFFFFFFFFu : 0u;
+    own[q] = in && j0 + q >= hr && j0 + q < hr + p.st_sw;
+  }
+  const bool shifted = colc != col0;  // edge thread: clamped columns differ
+  const bool hr_wide = hr >= 2 * CPT - 1;  // all in-thread and adjacent-thread columns in the window
+  if (tid == 0) {
+    s_nbuf = 0;
+    s_ntop = 0;
+    s_nsurv = 0;
+    s_tau = p.floor_votes;
+  }
+  const uint32_t *rowp = p.acc + (static_cast<int64_t>(f) * n_theta + (tb0 - HT)) * n_rho + colc;
+  int rnext = tb0 - HT;  // row rowp points at
+  auto load_row = [&](uint32_t (&dst)[CPT]) {
+    uint32_t t[CPT];
+    if (rnext >= 0 && rnext < n_theta) {
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) t[q] = __ldg(rowp + q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) t[q] = 0u;
+    }
+    if (shifted) {  // edge thread: place clamped columns at their loaded index
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        uint32_t v = 0u;
+#pragma unroll
+        for (int u = 0; u < CPT; ++u)
+          if (colc + u == col0 + q) v = t[u];
+        dst[q] = v & cmask[q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) dst[q] = t[q];
+    }
+    rowp += n_rho;
+    ++rnext;
+  };
+
+  // V[k][q] = row (g0 - HT + k); N[k][q] = next group's new rows
+  uint32_t V[NV][CPT], N[PS_G][CPT];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) load_row(V[k]);
+  __syncthreads();
+
+  for (int g0 = tb0; g0 < tb1; g0 += PS_G) {
+    if (g0 + PS_G < tb1) {
+#pragma unroll
+      for (int k = 0; k < PS_G; ++k) load_row(N[k]);  // in flight during this group
+    }
+    uint32_t tq[CPT];  // per column: tau if owned, else "never"
+    {
+      const uint32_t tau = s_tau;
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) tq[q] = own[q] ? tau : 0xFFFFFFFFu;
+    }
+    const int nrows = min(PS_G, tb1 - g0);
+    uint32_t surv = 0;
+#pragma unroll
+    for (int i = 0; i < PS_G; ++i) {
+      uint32_t m[CPT];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        uint32_t mm = V[i][q];
+#pragma unroll
+        for (int k = 1; k <= 2 * HT; ++k) mm = max(mm, V[i + k][q]);
+        m[q] = mm;
+      }
+      // prefilter: a window maximum is >= the column maxima of every column
+      // within +-hr -- here the thread's own CPT columns and the nearest
+      // column of each neighbouring thread (when hr reaches them)
+      uint32_t hm = 0;
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) hm = max(hm, m[q]);
+      const uint32_t ml = __shfl_up_sync(0xffffffffu, m[CPT - 1], 1);
+      const uint32_t mr = __shfl_down_sync(0xffffffffu, m[0], 1);
+      if (hr_wide) hm = max(hm, max(ml, mr));  // lanes 0/31 get their own values back
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const uint32_t need = hr_wide ? hm : m[q];
+        surv |= static_cast<uint32_t>(V[i + HT][q] >= max(need, tq[q])) << (i * CPT + q);
+      }
+      stream_store(CM + i * width + j0, m);
+    }
+#pragma unroll
+    for (int k = 0; k < PS_G + HT; ++k) stream_store(RAW + k * width + j0, V[k]);
+    if (nrows < PS_G) surv &= (1u << (nrows * CPT)) - 1u;
+    while (surv) {  // survivor list of the group: (row << 16) | loaded column
+      const int b = __ffs(surv) - 1;
+      surv &= surv - 1;
+      const int i = b / CPT, q = b - i * CPT;
+      const int slot = atomicAdd(&s_nsurv, 1);
+      if (LD_CHK(slot < PS_G * p.st_sw))
+        SL[slot] = (static_cast<uint32_t>(i) << 16) | static_cast<uint32_t>(j0 + q);
+    }
+    __syncthreads();  // (1) CM, RAW and the survivor list of the group complete
+    {
+      // one warp per survivor: the lanes scan the +-hr column maxima and the
+      // tie rows in parallel (ballots), instead of one divergent lane each
+      const int lane = tid & 31, nw = nt >> 5;
+      const int nsurv = s_nsurv;
+      for (int sidx = tid >> 5; sidx < nsurv; sidx += nw) {
+        const uint32_t e = SL[sidx];
+        const int i = static_cast<int>(e >> 16), j = static_cast<int>(e & 0xFFFFu);
+        const uint32_t *cmr = CM + i * width + j;
+        const uint32_t v = *cmr;  // == the cell's own value
+        bool bad = lane < HT && RAW[(i + lane) * width + j] == v;  // own column, earlier rows
+        bool tie = false;
+        for (int d = 1 + lane; d <= hr; d += 32) {
+          const uint32_t l = cmr[-d], r = cmr[d];
+          bad = bad || l > v || r > v;
+          tie = tie || l == v || r == v;
+        }
+        if (!__any_sync(0xffffffffu, bad) && __any_sync(0xffffffffu, tie)) {
+          // equal column maxima: an equal value at a lower (theta, rho) index
+          // -- to the left rows up to the cell's own, to the right rows above
+          for (int d = 1 + lane; d <= hr && !bad; d += 32) {
+            if (cmr[-d] == v)
+              for (int k = i; k <= i + HT && !bad; ++k) bad = RAW[k * width + j - d] == v;
+            if (!bad && cmr[d] == v)
+              for (int k = i; k < i + HT && !bad; ++k) bad = RAW[k * width + j + d] == v;
+          }
+        }
+        if (!__any_sync(0xffffffffu, bad) && lane == 0) {
+          const int slot = atomicAdd(&s_nbuf, 1);
+          if (LD_CHK(slot < p.st_buf))
+            buf[slot] = mk_key(v, static_cast<uint32_t>((g0 + i) * n_rho + cbase + j));
+        }
+      }
+    }
+    __syncthreads();  // (2) candidates buffered; CM / RAW / SL free
+    const int nbuf = s_nbuf;
+    if (nbuf > 0) merge_topk(buf, nbuf, top, &s_ntop, p.k);
+    if (tid == 0) {
+      // the frame's k-th best candidate is at least any unit's k-th best:
+      // share it through the per-frame threshold
+      s_nsurv = 0;
+      s_nbuf = 0;
+      uint32_t t = s_tau;
+      if (nbuf > 0 && s_ntop == p.k) {
+        t = max(t, static_cast<uint32_t>(top[p.k - 1] >> 32));
+        atomicMax(p.gtau + f, t);
+      }
+      t = max(t, *reinterpret_cast<volatile uint32_t *>(p.gtau + f));
+      s_tau = t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2 * HT; ++k)
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) V[k][q] = V[k + PS_G][q];
+#pragma unroll
+    for (int k = 0; k < PS_G; ++k)
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) V[2 * HT + k][q] = N[k][q];
+  }
+  u64 *out = p.band_keys + (static_cast<int64_t>(f) * p.n_units + unit) * p.k;
+  const int ntop = s_ntop;
+  for (int i = tid; i < p.k; i += nt) out[i] = i < ntop ? top[i] : 0ull;
+}
+
+typedef void (*StreamKernel)(const PeaksParams);
+// two CTAs per SM where the register window is small (<= 85 registers)
+#define LD_SK(HT, CPT) peaks_stream_kernel<HT, CPT, ps_minb(HT, CPT)>
+static StreamKernel stream_kernel(int ht, int cpt) {
+  if (cpt == 4) {
+    switch (ht) {
+      case 0: return LD_SK(0, 4);
+      case 1: return LD_SK(1, 4);
+      case 2: return LD_SK(2, 4);
+      case 3: return LD_SK(3, 4);
+      case 4: return LD_SK(4, 4);
+      case 5: return LD_SK(5, 4);
+      case 6: return LD_SK(6, 4);
+      default: return nullptr;
+    }
+  }
+  switch (ht) {
+    case 0: return LD_SK(0, 2);
+    case 1: return LD_SK(1, 2);
+    case 2: return LD_SK(2, 2);
+    case 3: return LD_SK(3, 2);
+    case 4: return LD_SK(4, 2);
+    case 5: return LD_SK(5, 2);
+    case 6: return LD_SK(6, 2);
+    case 7: return LD_SK(7, 2);
+    case 8: return LD_SK(8, 2);
+    case 9: return LD_SK(9, 2);
+    case 10: return LD_SK(10, 2);
+    case 11: return LD_SK(11, 2);
+    case 12: return LD_SK(12, 2);
+    default: return nullptr;
+  }
+}
+#undef LD_SK
+
+static int pow2_ceil(int v) {
+  int n = 1;
+  while (n < v) n <<= 1;
+  return n;
+}
+
+// Candidates of one group: two window maxima are never inside each other's
+// window, so a PS_G x sw block holds at most one per (ht+1) x (hr+1) cell.
+static int stream_buf_entries(int sw, int ht, int hr, int k) {
+  const int bound = ((PS_G + ht) / (ht + 1)) * ((sw + hr) / (hr + 1));
+  return pow2_ceil(bound + k);
+}
+static size_t stream_smem_bytes(int width, int sw, int ht, int hr, int k) {
+  return sizeof(uint32_t) * static_cast<size_t>(2 * PS_G + ht) * width +
+         sizeof(u64) * (static_cast<size_t>(k) + stream_buf_entries(sw, ht, hr, k)) +
+         sizeof(uint32_t) * static_cast<size_t>(PS_G) * sw;
+}
+
+// Streaming geometry: strips x chunks minimising loaded columns, with enough
+// CTAs to fill the GPU.  Returns false when the generic band kernel must run.
+static bool peaks_stream_plan(int batch, int n_theta, int n_rho, int half_theta, int half_rho,
+                              int k, int sm_count, PeaksParams *p, int *cpt_out, size_t *smem) {
+  if (half_theta > PT_MAX_HT) return false;
+  const char *env_cpt = getenv("LD_PEAKS_CPT");
+  int cpt = (half_theta <= 6 && !(env_cpt && env_cpt[0] == '2')) ? 4 : 2;
+  if (n_rho < cpt) cpt = 2;      // the clamped row pointer needs n_rho >= CPT
+  if (n_rho < cpt) return false;  // (n_rho = 2D + 1 >= 3 for every image)
+  int best_s = 0, best_nt = 0;
+  long best_cost = -1;
+  for (int s = 1; s <= 4096; ++s) {
+    const int sw = (n_rho + s - 1) / s;
+    if (sw < 32 && s > 1) break;
+    const int need = sw + 2 * half_rho;
+    const int nt = (((need + cpt - 1) / cpt) + 31) / 32 * 32;
+    if (nt > (ps_minb(half_theta, cpt) == 2 ? PS_NT_MAX2 : PS_NT_MAX)) continue;
+    const size_t sm_bytes = stream_smem_bytes(nt * cpt, sw, half_theta, half_rho, k);
+    if (sm_bytes > 220 * 1024) continue;
+    const long cost = static_cast<long>(s) * nt * cpt;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_s = s;
+      best_nt = nt;
+    }
+    if (best_cost >= 0 && static_cast<long>(s) * 32 * cpt > 2 * best_cost) break;
+  }
+  if (!best_s) return false;
+  const int sw = (n_rho + best_s - 1) / best_s;
+  // theta chunks: enough CTAs to fill the GPU, with the best wave quantisation
+  // (CTAs per SM from the kernel variant; each chunk re-reads a
+  // 2*half_theta-row halo)
+  const int slots = sm_count * ps_minb(half_theta, cpt);
+  int chunks = 1;
+  double best_eff = -1.0;
+  for (int c = 1; c <= 64; ++c) {
+    int tbc = (n_theta + c - 1) / c;
+    tbc = ((tbc + PS_G - 1) / PS_G) * PS_G;
+    if (tbc < 16 && c > 1) break;
+    const int cc = (n_theta + tbc - 1) / tbc;
+    const long units = static_cast<long>(batch) * best_s * cc;
+    const long waves = (units + slots - 1) / slots;
+    const double eff = static_cast<double>(units) / (waves * slots) *
+                       static_cast<double>(tbc) / (tbc + 2 * half_theta);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      chunks = cc;
+    }
+  }
+  int tb = (n_theta + chunks - 1) / chunks;
+  tb = ((tb + PS_G - 1) / PS_G) * PS_G;
+  if (tb < 16) tb = 16;
+  chunks = (n_theta + tb - 1) / tb;
+  const size_t bytes = stream_smem_bytes(best_nt * cpt, sw, half_theta, half_rho, k);
+  if (bytes > 220 * 1024) return false;
+  p->st_buf = stream_buf_entries(sw, half_theta, half_rho, k);
+  p->st_nt = best_nt;
+  p->st_sw = sw;
+  p->st_strips = best_s;
+  p->st_tb = tb;
+  p->st_chunks = chunks;
+  p->n_units = best_s * chunks;
+  *cpt_out = cpt;
+  *smem = bytes;
+  return true;
+}
+
 typedef void (*TileKernel)(const PeaksParams);
 static TileKernel tile_kernel(int ht) {
   switch (ht) {
@@ -380,24 +748,57 @@ bool peaks_tile_plan(int n_theta, int n_rho, int half_theta, int half_rho, int k
   return true;
 }
 
+#ifdef LD_DEBUG
+extern "C" int ld_debug_error_line(void) {
+  int v = 0;
+  cudaMemcpyFromSymbol(&v, g_ld_debug_line, sizeof(int));
+  return v;
+}
+#endif
+
 size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k) {
-  // worst case over both kernels: tiles with tc >= 32, or bands of PK_ROWS rows
+  // per-frame thresholds (256-B padded), then the per-unit top-k keys: worst
+  // case over the kernels (tiles/units of >= 16 rows x >= 32 columns, or
+  // bands of PK_ROWS rows)
   const size_t tiles = static_cast<size_t>((n_theta + PT_TR - 1) / PT_TR) * ((n_rho + 31) / 32);
   const size_t bands = static_cast<size_t>((n_theta + PK_ROWS - 1) / PK_ROWS);
-  return static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
+  const size_t head = (sizeof(uint32_t) * static_cast<size_t>(batch) + 255) / 256 * 256;
+  return head + static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
 }
 
 static bool g_tile_attr[64][PT_MAX_HT + 1];
+
+static bool g_stream_attr[64][2][PT_MAX_HT + 1];
 
 cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   PeaksParams p = p_in;
   size_t smem = 0;
   const char *env = getenv("LD_PEAKS_KERNEL");
   const bool force_band = env && env[0] == 'b';
-  if (!force_band && peaks_tile_plan(p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, &p, &smem)) {
+  const bool force_tile = env && env[0] == 't';
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int cpt = 0;
+  if (!force_band && !force_tile &&
+      peaks_stream_plan(p.batch, p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
+                        &smem)) {
+    cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+    if (em != cudaSuccess) return em;
+    StreamKernel kern = stream_kernel(p.half_theta, cpt);
+    bool &attr = g_stream_attr[dev & 63][cpt == 4][p.half_theta];
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           220 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 g1(p.n_units, p.batch);
+    kern<<<g1, p.st_nt, smem, stream>>>(p);
+  } else if (!force_band &&
+             peaks_tile_plan(p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, &p, &smem)) {
     TileKernel kern = tile_kernel(p.half_theta);
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (!g_tile_attr[dev & 63][p.half_theta]) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            200 * 1024);

@@ -70,15 +70,17 @@ __device__ __forceinline__ void load_row(const uint8_t *p, RowP &r) {
   for (int k = 1; k < 4; ++k) r.POL[k] = prmt(r.PO[k - 1], r.PO[k], 0x5432u);
 }
 
-// One output row of 16 pixels.  k0 = 2^15 - T2 in both halves, k2 = 2 * k0:
-// X = A + k0 has bit 15 set iff A >= T2, k2 - X = -A + k0 iff -A >= T2 (each
-// half stays in [0, 2^16): no carry crosses halves).  colm has bit 8j+7 of
-// word k set for interior pixels 4k+j.  Returns the edge mask with bit (8j+k)
-// set for pixel 4k+j; hb[k] receives the per-byte flags (bit 7 of each byte).
+// One output row of 16 pixels, as a 16-bit mask with bit b <-> pixel xs + b.
+// k0 = 2^15 - T2 in both halves, k2 = 2 * k0: X = A + k0 has bit 15 set iff
+// A >= T2, k2 - X = -A + k0 iff -A >= T2 (each half stays in [0, 2^16): no
+// carry crosses halves).  fe (pixels 4k, 4k+2) and fo (4k+1, 4k+3) then hold
+// the flags in bits 15 and 31; hi32(fe * 2^(17+4k)) moves them to bits 4k and
+// 16+4k, hi32(fo * 2^(18+4k)) to 4k+1 and 17+4k (IMAD.HI on the FMA pipe,
+// accumulated: the bits never overlap), and acc | acc >> 14 folds the high
+// half onto pixels 4k+2, 4k+3.  colmask clears non-interior columns.
 __device__ __forceinline__ uint32_t sobel_row(const RowP &u, const RowP &m, const RowP &d,
-                                              uint32_t k0, uint32_t k2, const uint32_t colm[4],
-                                              uint32_t hb[4]) {
-  uint32_t all = 0;
+                                              uint32_t k0, uint32_t k2, uint32_t colmask) {
+  uint32_t acc = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     // even pixels 4k, 4k+2
@@ -91,211 +93,263 @@ __device__ __forceinline__ uint32_t sobel_row(const RowP &u, const RowP &m, cons
     const uint32_t ya = u.PO[k] - d.PE[k] + mko;
     const uint32_t yb = d.PO[k] - u.PE[k] + mko;
     const uint32_t fo = (ya | (k2 - ya) | yb | (k2 - yb)) & 0x80008000u;
-    hb[k] = ((fe >> 8) | fo) & colm[k];  // byte j of word k <-> pixel 4k+j
-    all |= hb[k] >> (7 - k);
+    // x (2^s + 1): same high word as x 2^s for these bit patterns (no carry
+    // out of the low word), but not a power of two, so it stays an IMAD.HI
+    acc += __umulhi(fe, (1u << (17 + 4 * k)) + 1u);
+    acc += __umulhi(fo, (1u << (18 + 4 * k)) + 1u);
   }
-  return all;
+  return (acc | (acc >> 14)) & colmask;
 }
 
+// per consumer thread: rank of the lane in (chunk, strip) order within its
+// warp, and the lane of rank (tid % 32); built at compile time
+struct SbOrder {
+  uint8_t rank[SB_THREADS], inv[SB_THREADS];
+};
+constexpr SbOrder make_sb_order() {
+  SbOrder o{};
+  for (int w = 0; w < SB_THREADS / 32; ++w) {
+    for (int l = 0; l < 32; ++l) {
+      const int t = w * 32 + l;
+      const int key = (t % SB_CHUNKS) * SB_STRIPS + t / SB_CHUNKS;
+      int r = 0;
+      for (int m = 0; m < 32; ++m) {
+        const int u = w * 32 + m;
+        r += ((u % SB_CHUNKS) * SB_STRIPS + u / SB_CHUNKS) < key;
+      }
+      o.rank[t] = static_cast<uint8_t>(r);
+      o.inv[w * 32 + r] = static_cast<uint8_t>(l);
+    }
+  }
+  return o;
+}
+__constant__ SbOrder c_sb_order = make_sb_order();
+
+// byte expansion of a 4-bit mask: bit j -> byte j = 0xFF (binary-map output)
+__constant__ uint32_t kNibbleBytes[16] = {
+    0x00000000u, 0x000000FFu, 0x0000FF00u, 0x0000FFFFu, 0x00FF0000u, 0x00FF00FFu,
+    0x00FFFF00u, 0x00FFFFFFu, 0xFF000000u, 0xFF0000FFu, 0xFF00FF00u, 0xFF00FFFFu,
+    0xFFFF0000u, 0xFFFF00FFu, 0xFFFFFF00u, 0xFFFFFFFFu};
+
+// Edges of one thread's SR x 16-pixel block; bit b of masks[i] is pixel
+// (xs + b, ybase + i).  One entry per set bit: BFIND -> clear -> add -> store.
+// emit_edges_smem writes entry j at byte address `addr + 4j` of shared memory
+// (the staging buffer); emit_edges_global to out[j] (overflow path).
 template <int SR>
-__device__ __forceinline__ void write_edges(const SobelParams &p, const uint32_t masks[SR],
-                                            int f, int ybase, int xs, uint32_t off) {
-  uint32_t *dst = p.edges + static_cast<int64_t>(f) * p.edge_stride + off;
+__device__ __forceinline__ void emit_edges_smem(uint32_t addr, const uint32_t masks[SR],
+                                                int ybase, int xs) {
 #pragma unroll
   for (int i = 0; i < SR; ++i) {
     uint32_t m = masks[i];
-    const uint32_t yy = static_cast<uint32_t>(ybase + i) << 16;
+    const uint32_t v0 = (static_cast<uint32_t>(ybase + i) << 16) | static_cast<uint32_t>(xs);
     while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      *dst++ = yy | static_cast<uint32_t>(xs + 4 * (b & 7) + (b >> 3));
+      uint32_t b;
+      asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));
+      m ^= 1u << b;
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v0 + b) : "memory");
+      addr += 4;
     }
   }
 }
 
-template <int SR, int STAGES, int MINB>
-__global__ void __launch_bounds__(SB_THREADS, MINB)
+template <int SR>
+__device__ __forceinline__ void emit_edges_global(uint32_t *out, const uint32_t masks[SR],
+                                                  int ybase, int xs) {
+#pragma unroll
+  for (int i = 0; i < SR; ++i) {
+    uint32_t m = masks[i];
+    const uint32_t v0 = (static_cast<uint32_t>(ybase + i) << 16) | static_cast<uint32_t>(xs);
+    while (m) {
+      const uint32_t b = 31u - __clz(m);
+      m ^= 1u << b;
+      *out++ = v0 + b;
+    }
+  }
+}
+
+// Warp-specialised persistent kernel.  Warps 0..6 (224 threads = 14 column
+// chunks x 16 row strips) consume tiles; warp 7 is the TMA producer.  A stage
+// is handed over with two mbarriers (full: TMA bytes landed; empty: all 7
+// consumer warps finished reading it), so the loop has no CTA-wide barrier;
+// the producer also publishes each stage's (frame, tile row, tile column).
+// Each consumer warp reserves its own slice of the frame's list (one
+// atomicAdd per warp per tile) and emits the tile's edges one tile later,
+// when the reservation has returned: first into a per-warp shared-memory
+// staging buffer at their slice positions, then with coalesced stores.
+// Positions are assigned in (chunk, strip) order so that 32 consecutive list
+// entries cover a compact 16 x ~24-pixel region (few, consecutive rho bins per
+// theta in the voting kernel).
+template <int SR, int STAGES, int MINB, bool WB>
+__global__ void __launch_bounds__(SB_THREADS + 32, MINB)
     sobel_binarize_compact_kernel(const __grid_constant__ CUtensorMap tmap,
                                   const SobelParams p) {
   constexpr int TILE_H = SR * SB_STRIPS;
   constexpr int BOX_H = TILE_H + 2;
   constexpr int STAGE_BYTES = SB_BOX_W * BOX_H;
+  constexpr int NCW = SB_THREADS / 32;  // consumer warps
   static_assert(STAGE_BYTES % 128 == 0, "stage alignment");
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
-  constexpr int NW = SB_THREADS / 32;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint32_t *stage_edges = reinterpret_cast<uint32_t *>(smem + STAGES * STAGE_BYTES);
   __shared__ __align__(8) uint64_t full_bar[STAGES];
-  __shared__ uint32_t s_cnt[SB_THREADS];        // per-thread counts, in cell order
-  __shared__ uint32_t s_excl[2][SB_THREADS];    // exclusive scan inside each warp
-  __shared__ uint32_t s_wt[NW];                 // warp totals
-  __shared__ uint32_t s_wbase[2][NW];           // exclusive scan of warp totals
-  __shared__ uint32_t s_base[2];                // frame-list base of the tile
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ int4 tile_info[STAGES];  // frame, first output row, first column, -
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int chunk = tid % SB_CHUNKS;
-  const int strip = tid / SB_CHUNKS;
-  // List order inside a tile: 16x16-pixel cells (2 strips of one chunk), cells
-  // row-major.  32 consecutive list entries then span a compact region, so a
-  // warp of the voting kernel hits <= ~32 consecutive rho bins per theta.
-  const int ord = ((strip >> 1) * SB_CHUNKS + chunk) * 2 + (strip & 1);
-  const uint32_t k0 = static_cast<uint32_t>(32768 - p.t2) * 0x00010001u;
-  const uint32_t k2 = k0 + k0;
-
-  auto issue = [&](int tile, int stage) {
-    const int f = tile / p.tiles_per_frame;
-    const int rem = tile - f * p.tiles_per_frame;
-    const int ty = rem / p.tiles_x;
-    const int tx = rem - ty * p.tiles_x;
-    const int y = p.row_begin + ty * TILE_H - 1 - p.ry0;  // tensor row of smem row 0
-    const int x = tx * SB_TILE_W - SB_HALO_L;
-    mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
-    tma_load_3d(smem + stage * STAGE_BYTES, &tmap, &full_bar[stage], x, y, f);
-  };
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full_bar[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NCW);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      const int tile = blockIdx.x + s * gridDim.x;
-      if (tile < p.n_tiles) issue(tile, s);
+
+  if (warp == NCW) {  // ---------------- producer warp
+    if (lane == 0) {
+      int it = 0;
+      int f = blockIdx.x / p.tiles_per_frame;
+      int rem = blockIdx.x - f * p.tiles_per_frame;
+      const int sf = gridDim.x / p.tiles_per_frame;
+      const int sr = gridDim.x - sf * p.tiles_per_frame;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+        const int stage = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty_bar[stage], ((it / STAGES) - 1) & 1);
+        const int ty = rem / p.tiles_x;
+        const int tx = rem - ty * p.tiles_x;
+        const int y0 = p.row_begin + ty * TILE_H;
+        tile_info[stage] = make_int4(f, y0, tx * SB_TILE_W, 0);
+        mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);  // release: tile_info visible
+        tma_load_3d(smem + stage * STAGE_BYTES, &tmap, &full_bar[stage],
+                    tx * SB_TILE_W - SB_HALO_L, y0 - 1 - p.ry0, f);
+        f += sf;
+        rem += sr;
+        if (rem >= p.tiles_per_frame) {
+          rem -= p.tiles_per_frame;
+          ++f;
+        }
+      }
     }
+    return;
   }
 
-  // previous tile, written one iteration late so that the counter
-  // reservation (a global atomic round trip) overlaps the next tile's work
+  // ---------------- consumer warps
+  const int chunk = tid % SB_CHUNKS;
+  const int strip = tid / SB_CHUNKS;
+  const uint32_t k0 = static_cast<uint32_t>(32768 - p.t2) * 0x00010001u;
+  const uint32_t k2 = k0 + k0;
+  const int ylo_g = p.row_begin > 1 ? p.row_begin : 1;
+  const int yhi_g = p.height - 2 < p.row_end - 1 ? p.height - 2 : p.row_end - 1;
+  uint32_t *wstage = stage_edges + warp * SB_STAGE_CAP;
+
+  // rank of this lane in (chunk, strip) order within the warp, and the lane
+  // holding rank `lane` (a fixed permutation, tabulated on the host)
+  const int rank = c_sb_order.rank[tid], inv = c_sb_order.inv[tid];
+
+  // previous tile (emitted one iteration late)
   uint32_t pmask[SR];
 #pragma unroll
   for (int i = 0; i < SR; ++i) pmask[i] = 0u;
   int pf = 0, pybase = 0, pxs = 0;
-  uint32_t base_reg = 0;  // thread 0: reservation result of the previous tile
+  uint32_t pexcl = 0, pcnt = 0, ptotal = 0, pres = 0;  // lane 0 holds the reservation
+
+  auto flush = [&]() {
+    // previous tile: its reservation has had a whole tile to return
+    const uint32_t base = __shfl_sync(0xffffffffu, pres, 0);
+    uint32_t *glist = p.edges + static_cast<int64_t>(pf) * p.edge_stride + base;
+    const bool fits = pexcl + pcnt <= SB_STAGE_CAP;
+    if (fits) emit_edges_smem<SR>(smem_u32(wstage + pexcl), pmask, pybase, pxs);
+    else emit_edges_global<SR>(glist + pexcl, pmask, pybase, pxs);
+    // staged prefix: everything before the first lane that overflowed
+    const uint32_t split = __reduce_min_sync(0xffffffffu, fits ? ptotal : pexcl);
+    __syncwarp();
+    for (uint32_t q = lane; q < split; q += 32) glist[q] = wstage[q];
+    __syncwarp();
+  };
 
   int it = 0;
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const int stage = it % STAGES;
-    const uint32_t parity = (it / STAGES) & 1;
-    const int cb = it & 1, pb = cb ^ 1;
-    const int f = tile / p.tiles_per_frame;
-    const int rem = tile - f * p.tiles_per_frame;
-    const int ty = rem / p.tiles_x;
-    const int tx = rem - ty * p.tiles_x;
-    const int y0 = p.row_begin + ty * TILE_H;  // first output row of the tile
-    const int xs = tx * SB_TILE_W + chunk * 16;   // first column of this thread's chunk
+    mbar_wait(&full_bar[stage], (it / STAGES) & 1);
+    const int4 ti = tile_info[stage];
+    const int f = ti.x;
+    const int xs = ti.z + chunk * 16;     // first column of this thread's chunk
+    const int ybase = ti.y + strip * SR;  // output row of masks[0]
 
-    // interior columns: bit 8j+7 of word k for pixel 4k+j with 1 <= x <= W-2
-    uint32_t colm[4];
+    uint32_t colmask = 0xFFFFu;  // interior columns 1 <= x <= W-2
     {
-      const int lo = 1 - xs, hi = p.width - 2 - xs;  // valid j in [lo, hi]
-      if (lo <= 0 && hi >= 15) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) colm[k] = 0x80808080u;
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint32_t b = 0;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int jj = 4 * k + j;
-            if (jj >= lo && jj <= hi) b |= 0x80u << (8 * j);
-          }
-          colm[k] = b;
-        }
+      const int lo = 1 - xs, hi = p.width - 2 - xs;
+      if (lo > 0 || hi < 15) {
+        colmask = (hi < 0 || lo > 15) ? 0u
+                                      : ((0xFFFFu >> (15 - min(hi, 15))) & (0xFFFFu << max(lo, 0)));
       }
     }
 
-    mbar_wait(&full_bar[stage], parity);
-    const uint8_t *buf = smem + stage * STAGE_BYTES + SB_HALO_L + chunk * 16;
-
+    const uint8_t *buf = smem + stage * STAGE_BYTES + SB_HALO_L + chunk * 16 + strip * SR * SB_BOX_W;
     uint32_t masks[SR];
-    const int ybase = y0 + strip * SR;  // output row of masks[0]
-    {
-      // rows whose output is computed: interior (1 <= y <= H-2) and owned
-      const int ylo = ybase < 1 ? 1 : ybase;
-      int yhi = p.height - 2 < p.row_end - 1 ? p.height - 2 : p.row_end - 1;
+#pragma unroll
+    for (int i = 0; i < SR; ++i) masks[i] = 0u;
+    if (ybase < p.row_end && xs < p.width) {  // skip strips/chunks outside the image
       RowP r0, r1, r2;
-      load_row(buf + (strip * SR + 0) * SB_BOX_W, r0);
-      load_row(buf + (strip * SR + 1) * SB_BOX_W, r1);
+      load_row(buf, r0);
+      load_row(buf + SB_BOX_W, r1);
 #pragma unroll
       for (int i = 0; i < SR; ++i) {
-        load_row(buf + (strip * SR + i + 2) * SB_BOX_W, r2);
+        load_row(buf + (i + 2) * SB_BOX_W, r2);
         const int y = ybase + i;
-        uint32_t hb[4] = {0u, 0u, 0u, 0u};
-        uint32_t all = 0;
-        if (y >= ylo && y <= yhi) all = sobel_row(r0, r1, r2, k0, k2, colm, hb);
-        masks[i] = all;
-        if (p.binary != nullptr && y < p.row_end && xs < p.width) {
+        const uint32_t m = sobel_row(r0, r1, r2, k0, k2, colmask);
+        masks[i] = (y >= ylo_g && y <= yhi_g) ? m : 0u;
+        if (WB && y < p.row_end && xs < p.width) {
           uint8_t *dst = p.binary + static_cast<int64_t>(f) * p.bin_frame_stride +
                          static_cast<int64_t>(y - p.row_begin) * p.bin_pitch + xs;
-          // sign-replicating byte permute: 0xFF where bit 7 of the byte is set
+          const uint32_t mm = masks[i];
           *reinterpret_cast<uint4 *>(dst) =
-              make_uint4(prmt(hb[0], 0u, 0xBA98u), prmt(hb[1], 0u, 0xBA98u),
-                         prmt(hb[2], 0u, 0xBA98u), prmt(hb[3], 0u, 0xBA98u));
+              make_uint4(kNibbleBytes[mm & 15u], kNibbleBytes[(mm >> 4) & 15u],
+                         kNibbleBytes[(mm >> 8) & 15u], kNibbleBytes[(mm >> 12) & 15u]);
         }
         r0 = r1;
         r1 = r2;
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);  // stage consumed by this warp
+
+    // warp-level reservation of this tile's slice, scanned in rank order
     uint32_t cnt = 0;
 #pragma unroll
     for (int i = 0; i < SR; ++i) cnt += __popc(masks[i]);
-    s_cnt[ord] = cnt;
-    if (tid == 0 && it > 0) s_base[pb] = base_reg;
-    __syncthreads();  // (A): stage consumed, counts and previous base visible
-    if (tid == 0) {
-      const int next = tile + STAGES * gridDim.x;
-      if (next < p.n_tiles) issue(next, stage);
-    }
-    if (it > 0 && p.edges != nullptr) {
-      const uint32_t off = s_base[pb] + s_wbase[pb][ord >> 5] + s_excl[pb][ord];
-      write_edges<SR>(p, pmask, pf, pybase, pxs, off);
-    }
-    {  // scan of this tile's counts in cell order
-      const uint32_t x = s_cnt[tid];
-      uint32_t incl = x;
+    const uint32_t cr = __shfl_sync(0xffffffffu, cnt, inv);  // count of rank `lane`
+    uint32_t incl = cr;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      s_excl[cb][tid] = incl - x;
-      if (lane == 31) s_wt[warp] = incl;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    __syncthreads();  // (B)
-    if (tid == 0) {
-      uint32_t acc = 0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        s_wbase[cb][w] = acc;
-        acc += s_wt[w];
-      }
-      base_reg = acc ? atomicAdd(&p.counts[f], acc) : 0u;  // consumed next iteration
-    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = __shfl_sync(0xffffffffu, incl - cr, rank);
+
+    if (it > 0 && p.edges != nullptr) flush();
+    if (lane == 0) pres = total ? atomicAdd(&p.counts[f], total) : 0u;
 #pragma unroll
     for (int i = 0; i < SR; ++i) pmask[i] = masks[i];
+    pexcl = excl;
+    pcnt = cnt;
+    ptotal = total;
     pf = f;
     pybase = ybase;
     pxs = xs;
   }
-  if (it > 0) {
-    const int pb = (it - 1) & 1;
-    if (tid == 0) s_base[pb] = base_reg;
-    __syncthreads();
-    if (p.edges != nullptr) {
-      const uint32_t off = s_base[pb] + s_wbase[pb][ord >> 5] + s_excl[pb][ord];
-      write_edges<SR>(p, pmask, pf, pybase, pxs, off);
-    }
-  }
+  if (it > 0 && p.edges != nullptr) flush();
 }
 
-template <int SR, int STAGES, int MINB>
+template <int SR, int STAGES, int MINB, bool WB>
 static cudaError_t launch_cfg(const CUtensorMap &tmap, const SobelParams &p, int n_ctas,
                               cudaStream_t stream) {
-  auto kern = sobel_binarize_compact_kernel<SR, STAGES, MINB>;
-  const size_t smem = static_cast<size_t>(STAGES) * SB_BOX_W * (SR * SB_STRIPS + 2) + 128;
+  auto kern = sobel_binarize_compact_kernel<SR, STAGES, MINB, WB>;
+  const size_t smem = static_cast<size_t>(STAGES) * SB_BOX_W * (SR * SB_STRIPS + 2) +
+                      static_cast<size_t>(SB_THREADS / 32) * SB_STAGE_CAP * 4 + 128;
   static bool attr_done[64];  // idempotent per-device attribute; benign race
   int dev = 0;
   cudaGetDevice(&dev);
@@ -305,15 +359,16 @@ static cudaError_t launch_cfg(const CUtensorMap &tmap, const SobelParams &p, int
     if (e != cudaSuccess) return e;
     attr_done[dev & 63] = true;
   }
-  kern<<<n_ctas, SB_THREADS, smem, stream>>>(tmap, p);
+  kern<<<n_ctas, SB_THREADS + 32, smem, stream>>>(tmap, p);
   note_launch();
   return cudaGetLastError();
 }
 
 SobelCfg sobel_cfg() {
   const char *env = getenv("LD_SOBEL_CFG");
-  if (env && env[0] == '4') return SobelCfg{4, 4, 3};
-  return SobelCfg{8, 3, 2};
+  if (env && env[0] == '4') return SobelCfg{4, 3, 3};
+  if (env && env[0] == '6') return SobelCfg{6, 3, 2};
+  return SobelCfg{8, 2, 2};
 }
 
 cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_count,
@@ -321,8 +376,15 @@ cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_c
   const SobelCfg c = sobel_cfg();
   const int64_t max_ctas = static_cast<int64_t>(sm_count) * c.ctas_per_sm;
   const int n_ctas = static_cast<int>(p.n_tiles < max_ctas ? p.n_tiles : max_ctas);
-  if (c.sr == 4) return launch_cfg<4, 4, 3>(tmap, p, n_ctas, stream);
-  return launch_cfg<8, 3, 2>(tmap, p, n_ctas, stream);
+  const bool wb = p.binary != nullptr;
+  if (c.sr == 4)
+    return wb ? launch_cfg<4, 3, 3, true>(tmap, p, n_ctas, stream)
+              : launch_cfg<4, 3, 3, false>(tmap, p, n_ctas, stream);
+  if (c.sr == 6)
+    return wb ? launch_cfg<6, 3, 2, true>(tmap, p, n_ctas, stream)
+              : launch_cfg<6, 3, 2, false>(tmap, p, n_ctas, stream);
+  return wb ? launch_cfg<8, 2, 2, true>(tmap, p, n_ctas, stream)
+            : launch_cfg<8, 2, 2, false>(tmap, p, n_ctas, stream);
 }
 
 }  // namespace ld

@@ -326,12 +326,13 @@ def test_banded_accumulators_sum_to_whole(ld, oracle):
         assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want), n
 
 
-@pytest.mark.parametrize("kernel", ["tile", "band"])
-def test_peaks_both_kernels_windows(ld, oracle, kernel, monkeypatch):
-    # the tiled kernel (half_theta <= 12, tc >= 32) and the generic band kernel
-    # (forced, or chosen for large windows) agree with the oracle
-    if kernel == "band":
-        monkeypatch.setenv("LD_PEAKS_KERNEL", "band")
+@pytest.mark.parametrize("kernel", ["stream", "tile", "band"])
+def test_peaks_all_kernels_windows(ld, oracle, kernel, monkeypatch):
+    # the streaming kernel (default, half_theta <= 12), the tiled kernel and the
+    # generic band kernel (forced, or chosen for large windows) agree with the
+    # oracle
+    if kernel != "stream":
+        monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
     rng = np.random.default_rng(31)
     for trial, (ht, hr) in enumerate([(0, 0), (0, 5), (1, 1), (2, 29), (7, 44), (10, 116),
                                       (12, 3), (13, 2), (3, 240), (20, 300)]):
@@ -395,3 +396,38 @@ def test_banded_detector_more_ranks_than_rows(ld, oracle):
         total = acc.clone() if total is None else total + acc
     torch.cuda.synchronize()
     assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want)
+
+
+@pytest.mark.parametrize("kernel", ["stream", "band"])
+def test_peaks_ties_and_plateaus(ld, oracle, kernel, monkeypatch):
+    # equal maxima inside one window (plateaus, equal values left/right/above/
+    # below) exercise the exact (theta, rho) tie-break; small value range makes
+    # ties everywhere
+    if kernel != "stream":
+        monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
+    rng = np.random.default_rng(77)
+    for trial, (ht, hr, k) in enumerate([(2, 29, 4), (1, 3, 64), (0, 0, 1024), (7, 44, 8),
+                                         (10, 116, 64), (12, 5, 16), (3, 0, 32)]):
+        acc = rng.integers(0, 3, size=(3, 97, 1500)).astype(np.uint32)
+        acc[0, 40:43, 700:705] = 9                    # plateau
+        acc[1, 10, 100] = acc[1, 10, 103] = acc[1, 12, 101] = 7
+        acc[2, :, 1499] = 5                           # column of equal values at the edge
+        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, k)
+        torch.cuda.synchronize()
+        for f in range(3):
+            want, wn = oracle.hough_peaks(acc[f], ht, hr, 1, k)
+            assert int(npk[f]) == wn, (kernel, trial, f)
+            assert peak_tuples(peaks[f].cpu()) == oracle_peak_tuples(want), (kernel, trial, f)
+
+
+def test_peaks_stream_theta_chunks_single_frame(ld, oracle):
+    # one frame -> the streaming kernel splits theta into chunks with a
+    # half_theta-row halo; peaks near chunk seams must match
+    rng = np.random.default_rng(8)
+    acc = rng.integers(0, 40, size=(1, 1024, 3001)).astype(np.uint32)
+    for t in (0, 15, 16, 17, 31, 32, 33, 63, 64, 500, 1023):
+        acc[0, t, (t * 37) % 3001] = 1000 + t
+    for ht, hr, k in [(10, 116, 64), (2, 29, 4), (0, 0, 16), (12, 300, 32)]:
+        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, k)
+        want, wn = oracle.hough_peaks(acc[0], ht, hr, 1, k)
+        assert int(npk[0]) == wn and peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(want)
