@@ -25,6 +25,7 @@ constexpr int SB_STAGE_CAP = 1024;  // per-warp edge staging buffer (uint32 entr
 // depth, CTAs per SM; selected on the host (LD_SOBEL_CFG=4 picks the SR=4 one)
 struct SobelCfg {
   int sr, stages, ctas_per_sm;
+  int cap = SB_STAGE_CAP;  // per-warp edge staging entries (0: direct global stores)
 };
 SobelCfg sobel_cfg();
 

@@ -460,12 +460,14 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
 #pragma unroll
       for (int k = 0; k < PS_G; ++k) load_row(N[k]);  // in flight during this group
     }
+    // thread 0 prefetches the per-frame threshold now; it is used after the
+    // group, so the global round trip overlaps the group's work
+    uint32_t gt = 0;
+    if (tid == 0) gt = *reinterpret_cast<volatile uint32_t *>(p.gtau + f);
     uint32_t tq[CPT];  // per column: tau if owned, else "never"
-    {
-      const uint32_t tau = s_tau;
+    const uint32_t tau = s_tau;
 #pragma unroll
-      for (int q = 0; q < CPT; ++q) tq[q] = own[q] ? tau : 0xFFFFFFFFu;
-    }
+    for (int q = 0; q < CPT; ++q) tq[q] = own[q] ? tau : 0xFFFFFFFFu;
     const int nrows = min(PS_G, tb1 - g0);
     uint32_t surv = 0;
 #pragma unroll
@@ -487,10 +489,12 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
       const uint32_t ml = __shfl_up_sync(0xffffffffu, m[CPT - 1], 1);
       const uint32_t mr = __shfl_down_sync(0xffffffffu, m[0], 1);
       if (hr_wide) hm = max(hm, max(ml, mr));  // lanes 0/31 get their own values back
+      if (hm >= tau) {  // else no cell of this thread's row can reach tau
 #pragma unroll
-      for (int q = 0; q < CPT; ++q) {
-        const uint32_t need = hr_wide ? hm : m[q];
-        surv |= static_cast<uint32_t>(V[i + HT][q] >= max(need, tq[q])) << (i * CPT + q);
+        for (int q = 0; q < CPT; ++q) {
+          const uint32_t need = hr_wide ? hm : m[q];
+          surv |= static_cast<uint32_t>(V[i + HT][q] >= max(need, tq[q])) << (i * CPT + q);
+        }
       }
       stream_store(CM + i * width + j0, m);
     }
@@ -551,10 +555,9 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
       uint32_t t = s_tau;
       if (nbuf > 0 && s_ntop == p.k) {
         t = max(t, static_cast<uint32_t>(top[p.k - 1] >> 32));
-        atomicMax(p.gtau + f, t);
+        atomicMax(p.gtau + f, t);  // no return value used: a fire-and-forget RED
       }
-      t = max(t, *reinterpret_cast<volatile uint32_t *>(p.gtau + f));
-      s_tau = t;
+      s_tau = max(t, gt);
     }
     __syncthreads();
 #pragma unroll

@@ -138,16 +138,22 @@ __constant__ uint32_t kNibbleBytes[16] = {
 template <int SR>
 __device__ __forceinline__ void emit_edges_smem(uint32_t addr, const uint32_t masks[SR],
                                                 int ybase, int xs) {
+  // two entries per iteration (highest and lowest set bit, independent
+  // FLO chains), so the warp runs half as many divergent iterations
 #pragma unroll
   for (int i = 0; i < SR; ++i) {
     uint32_t m = masks[i];
     const uint32_t v0 = (static_cast<uint32_t>(ybase + i) << 16) | static_cast<uint32_t>(xs);
     while (m) {
-      uint32_t b;
-      asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));
-      m ^= 1u << b;
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v0 + b) : "memory");
-      addr += 4;
+      uint32_t bh, bl;
+      asm("bfind.u32 %0, %1;" : "=r"(bh) : "r"(m));
+      asm("{\n\t.reg .b32 t;\n\tbrev.b32 t, %1;\n\tbfind.shiftamt.u32 %0, t;\n\t}"
+          : "=r"(bl) : "r"(m));
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v0 + bh) : "memory");
+      const bool two = bh != bl;
+      if (two) asm volatile("st.shared.u32 [%0+4], %1;" ::"r"(addr), "r"(v0 + bl) : "memory");
+      m &= ~((1u << bh) | (1u << bl));
+      addr += two ? 8u : 4u;
     }
   }
 }
@@ -179,7 +185,7 @@ __device__ __forceinline__ void emit_edges_global(uint32_t *out, const uint32_t 
 // Positions are assigned in (chunk, strip) order so that 32 consecutive list
 // entries cover a compact 16 x ~24-pixel region (few, consecutive rho bins per
 // theta in the voting kernel).
-template <int SR, int STAGES, int MINB, bool WB>
+template <int SR, int STAGES, int MINB, bool WB, int CAP>
 __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
     sobel_binarize_compact_kernel(const __grid_constant__ CUtensorMap tmap,
                                   const SobelParams p) {
@@ -242,7 +248,7 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
   const uint32_t k2 = k0 + k0;
   const int ylo_g = p.row_begin > 1 ? p.row_begin : 1;
   const int yhi_g = p.height - 2 < p.row_end - 1 ? p.height - 2 : p.row_end - 1;
-  uint32_t *wstage = stage_edges + warp * SB_STAGE_CAP;
+  uint32_t *wstage = stage_edges + warp * CAP;
 
   // rank of this lane in (chunk, strip) order within the warp, and the lane
   // holding rank `lane` (a fixed permutation, tabulated on the host)
@@ -259,14 +265,18 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
     // previous tile: its reservation has had a whole tile to return
     const uint32_t base = __shfl_sync(0xffffffffu, pres, 0);
     uint32_t *glist = p.edges + static_cast<int64_t>(pf) * p.edge_stride + base;
-    const bool fits = pexcl + pcnt <= SB_STAGE_CAP;
-    if (fits) emit_edges_smem<SR>(smem_u32(wstage + pexcl), pmask, pybase, pxs);
-    else emit_edges_global<SR>(glist + pexcl, pmask, pybase, pxs);
-    // staged prefix: everything before the first lane that overflowed
-    const uint32_t split = __reduce_min_sync(0xffffffffu, fits ? ptotal : pexcl);
-    __syncwarp();
-    for (uint32_t q = lane; q < split; q += 32) glist[q] = wstage[q];
-    __syncwarp();
+    if constexpr (CAP == 0) {
+      emit_edges_global<SR>(glist + pexcl, pmask, pybase, pxs);
+    } else {
+      const bool fits = pexcl + pcnt <= static_cast<uint32_t>(CAP);
+      if (fits) emit_edges_smem<SR>(smem_u32(wstage + pexcl), pmask, pybase, pxs);
+      else emit_edges_global<SR>(glist + pexcl, pmask, pybase, pxs);
+      // staged prefix: everything before the first lane that overflowed
+      const uint32_t split = __reduce_min_sync(0xffffffffu, fits ? ptotal : pexcl);
+      __syncwarp();
+      for (uint32_t q = lane; q < split; q += 32) glist[q] = wstage[q];
+      __syncwarp();
+    }
   };
 
   int it = 0;
@@ -344,12 +354,12 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
   if (it > 0 && p.edges != nullptr) flush();
 }
 
-template <int SR, int STAGES, int MINB, bool WB>
+template <int SR, int STAGES, int MINB, bool WB, int CAP = SB_STAGE_CAP>
 static cudaError_t launch_cfg(const CUtensorMap &tmap, const SobelParams &p, int n_ctas,
                               cudaStream_t stream) {
-  auto kern = sobel_binarize_compact_kernel<SR, STAGES, MINB, WB>;
+  auto kern = sobel_binarize_compact_kernel<SR, STAGES, MINB, WB, CAP>;
   const size_t smem = static_cast<size_t>(STAGES) * SB_BOX_W * (SR * SB_STRIPS + 2) +
-                      static_cast<size_t>(SB_THREADS / 32) * SB_STAGE_CAP * 4 + 128;
+                      static_cast<size_t>(SB_THREADS / 32) * CAP * 4 + 128;
   static bool attr_done[64];  // idempotent per-device attribute; benign race
   int dev = 0;
   cudaGetDevice(&dev);
@@ -368,6 +378,9 @@ SobelCfg sobel_cfg() {
   const char *env = getenv("LD_SOBEL_CFG");
   if (env && env[0] == '4') return SobelCfg{4, 3, 3};
   if (env && env[0] == '6') return SobelCfg{6, 3, 2};
+  if (env && env[0] == 'd') return SobelCfg{8, 3, 2, 0};    // no staging, 3 stages
+  if (env && env[0] == 's') return SobelCfg{8, 3, 2, 256};  // small staging, 3 stages
+  if (env && env[0] == 't') return SobelCfg{8, 3, 2, 448};  // 3 stages, 2 CTAs/SM
   return SobelCfg{8, 2, 2};
 }
 
@@ -380,6 +393,15 @@ cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_c
   if (c.sr == 4)
     return wb ? launch_cfg<4, 3, 3, true>(tmap, p, n_ctas, stream)
               : launch_cfg<4, 3, 3, false>(tmap, p, n_ctas, stream);
+  if (c.sr == 8 && c.cap == 0)
+    return wb ? launch_cfg<8, 3, 2, true, 0>(tmap, p, n_ctas, stream)
+              : launch_cfg<8, 3, 2, false, 0>(tmap, p, n_ctas, stream);
+  if (c.sr == 8 && c.cap == 448)
+    return wb ? launch_cfg<8, 3, 2, true, 448>(tmap, p, n_ctas, stream)
+              : launch_cfg<8, 3, 2, false, 448>(tmap, p, n_ctas, stream);
+  if (c.sr == 8 && c.cap == 256)
+    return wb ? launch_cfg<8, 3, 2, true, 256>(tmap, p, n_ctas, stream)
+              : launch_cfg<8, 3, 2, false, 256>(tmap, p, n_ctas, stream);
   if (c.sr == 6)
     return wb ? launch_cfg<6, 3, 2, true>(tmap, p, n_ctas, stream)
               : launch_cfg<6, 3, 2, false>(tmap, p, n_ctas, stream);
