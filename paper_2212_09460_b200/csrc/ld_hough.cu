@@ -16,7 +16,36 @@
 // no global atomics anywhere.
 #include "ld_internal.cuh"
 
+#ifndef LD_HV_UNROLL
+#define LD_HV_UNROLL 4  // band rows per unrolled step
+#endif
+
 namespace ld {
+
+// One block of 32 x EPL consecutive list entries of a warp (entry
+// blk + 32j + lane in lane `lane`), voted into every row of the band.
+template <int EPL, bool FULL>
+__device__ __forceinline__ void vote_block(const uint32_t *el, uint32_t blk, uint32_t end,
+                                           int lane, int nr, const uint4 *rowk) {
+  uint32_t xs[EPL], ys[EPL];
+  bool ok[EPL];
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    const uint32_t e = blk + 32u * j + lane;
+    ok[j] = FULL || e < end;
+    const uint32_t q = ok[j] ? __ldg(el + e) : 0u;
+    xs[j] = q & 0xFFFFu;
+    ys[j] = q >> 16;
+  }
+  constexpr int HV_UNROLL = LD_HV_UNROLL;
+#pragma unroll HV_UNROLL
+  for (int r = 0; r < nr; ++r) {
+    const uint4 k = rowk[r];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j)
+      if (FULL || ok[j]) red_shared_add(((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u, 1u);
+  }
+}
 
 __global__ void __launch_bounds__(HV_THREADS, 1)
     hough_vote_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
@@ -49,42 +78,19 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   const uint32_t n_edges = p.counts[f];
   const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
 
-  // Each warp takes blocks of 256 consecutive list entries; at step j its 32
-  // lanes hold the 32 consecutive entries blk + 32j + lane, which the
-  // compaction made spatially compact (ld_sobel.cu): per theta they fall into
-  // few consecutive rho bins, i.e. distinct banks, and equal bins merge.
+  // Each warp takes blocks of 256 consecutive list entries (8 per lane),
+  // interleaved across the CTA's warps; at step j its 32 lanes hold the 32
+  // consecutive entries blk + 32j + lane, which the compaction made spatially
+  // compact (ld_sobel.cu): per theta they fall into few consecutive rho bins,
+  // i.e. distinct banks, and equal bins merge in ATOMS.POPC.INC.  (Measured on
+  // B200: 16 entries per lane, or contiguous per-warp ranges, are slower.)
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = HV_THREADS / 32;
-  constexpr int EPL = 8;  // edges per lane per block
-  for (uint32_t blk = static_cast<uint32_t>(warp) * (32u * EPL); blk < n_edges;
-       blk += NWARPS * 32u * EPL) {
-    uint32_t xs[EPL], ys[EPL];
-    bool ok[EPL];
-#pragma unroll
-    for (int j = 0; j < EPL; ++j) {
-      const uint32_t e = blk + 32u * j + lane;
-      ok[j] = e < n_edges;
-      const uint32_t q = ok[j] ? __ldg(el + e) : 0u;
-      xs[j] = q & 0xFFFFu;
-      ys[j] = q >> 16;
-    }
-    if (blk + 32u * EPL <= n_edges) {
-#pragma unroll 2
-      for (int r = 0; r < nr; ++r) {
-        const uint4 k = rowk[r];
-#pragma unroll
-        for (int j = 0; j < EPL; ++j)
-          red_shared_add(((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u, 1u);
-      }
-    } else {
-      for (int r = 0; r < nr; ++r) {
-        const uint4 k = rowk[r];
-#pragma unroll
-        for (int j = 0; j < EPL; ++j)
-          if (ok[j]) red_shared_add(((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u, 1u);
-      }
-    }
-  }
+  constexpr int EPL = 8;
+  uint32_t blk = static_cast<uint32_t>(warp) * (32u * EPL);
+  for (; blk + 32u * EPL <= n_edges; blk += NWARPS * 32u * EPL)
+    vote_block<EPL, true>(el, blk, n_edges, lane, nr, rowk);
+  if (blk < n_edges) vote_block<EPL, false>(el, blk, n_edges, lane, nr, rowk);
   __syncthreads();
 
   uint32_t *dst = p.acc + (static_cast<int64_t>(f) * p.n_theta + t0) * p.n_rho;

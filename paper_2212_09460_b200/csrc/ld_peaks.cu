@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksP
 // accumulator itself.  Candidates are merged into the CTA's top-k in shared
 // memory; peaks_merge_kernel merges the CTAs of a frame.
 // ---------------------------------------------------------------------------
-constexpr int PS_G = 4;  // rows per register group
+constexpr int PS_G = 4;    // rows per register group
+constexpr int PS_NPF = 2;  // groups of L2 prefetch beyond the register prefetch
 
 constexpr int PS_NT_MAX = 512;   // threads per CTA, one CTA per SM
 constexpr int PS_NT_MAX2 = 384;  // threads per CTA when two CTAs share an SM
@@ -455,7 +456,31 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
   for (int k = 0; k < NV; ++k) load_row(V[k]);
   __syncthreads();
 
+  // L2 prefetch of the strip's row segments PS_NPF groups ahead (one bulk
+  // prefetch per row, issued by one thread): the register loads of the next
+  // group then hit L2 instead of paying the HBM round trip
+  const uint32_t *frame0 = p.acc + static_cast<int64_t>(f) * n_theta * n_rho;
+  const uintptr_t acc_end = reinterpret_cast<uintptr_t>(p.acc + static_cast<int64_t>(p.batch) * n_theta * n_rho);
+  const int pc0 = max(cbase, 0), pc1 = min(cbase + width, n_rho);
+  // rows are spread over the warps (lane 0 of warp w issues row r0 + w, ...)
+  // so that no single warp carries the prefetch work into the group barrier
+  const bool pf_lane = (tid & 31) == 0;
+  const int pf_w = tid >> 5, pf_nw = nt >> 5;
+  auto l2_prefetch_rows = [&](int r0, int r1) {
+    if (!pf_lane) return;
+    for (int r = max(r0, 0) + pf_w; r < min(r1, n_theta); r += pf_nw) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(frame0 + static_cast<int64_t>(r) * n_rho + pc0) & ~static_cast<uintptr_t>(15);
+      uintptr_t e = (reinterpret_cast<uintptr_t>(frame0 + static_cast<int64_t>(r) * n_rho + pc1) + 15) & ~static_cast<uintptr_t>(15);
+      if (e > (acc_end & ~static_cast<uintptr_t>(15))) e = acc_end & ~static_cast<uintptr_t>(15);
+      if (e > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<uint32_t>(e - a))
+                     : "memory");
+    }
+  };
+  l2_prefetch_rows(tb0 + HT + PS_G, tb0 + HT + (1 + PS_NPF) * PS_G);
+
   for (int g0 = tb0; g0 < tb1; g0 += PS_G) {
+    l2_prefetch_rows(g0 + HT + (1 + PS_NPF) * PS_G, g0 + HT + (2 + PS_NPF) * PS_G);
     if (g0 + PS_G < tb1) {
 #pragma unroll
       for (int k = 0; k < PS_G; ++k) load_row(N[k]);  // in flight during this group

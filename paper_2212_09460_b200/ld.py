@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libld.so")
+LIB_PATH = os.environ.get("LD_LIB", os.path.join(HERE, "libld.so"))  # LD_LIB: dev override
 
 LD_OK, LD_ERR_INVALID_ARG, LD_ERR_RANGE, LD_ERR_WORKSPACE, LD_ERR_UNSUPPORTED, LD_ERR_CUDA = range(6)
 LD_MAX_DIM, LD_MAX_THETA, LD_MAX_K = 16384, 2048, 1024
