@@ -719,6 +719,249 @@ static bool peaks_stream_plan(int batch, int n_theta, int n_rho, int half_theta,
   return true;
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-strip kernel (narrow windows: half_theta <= 3, 4 <= half_rho <= 64,
+// k <= 64).  Every WARP is an independent unit: one strip of 256 loaded
+// columns (owned: 256 - 2 half_rho) x one chunk of theta rows of one frame,
+// 8 consecutive columns per lane.  Nothing is shared between warps, so there
+// is no CTA barrier at all: the latency of one warp's loads is hidden by the
+// other warps instead of stalling a whole CTA at every row group.  The halo
+// columns are read twice (by neighbouring warps), mostly from L2.  Same tests
+// as the streaming kernel: column maxima in registers, in-lane / neighbour-
+// lane prefilter, per-warp and per-frame running k-th best threshold tau,
+// warp-cooperative exact test of the few survivors.
+// ---------------------------------------------------------------------------
+constexpr int PW_CPT = 8, PW_G = 2, PW_W = 8, PW_COLS = 32 * PW_CPT, PW_KMAX = 64, PW_CBUF = 128;
+constexpr int PW_NPF = 12;  // rows of L2 prefetch beyond the register prefetch
+
+template <int HT>
+struct PwSmem {
+  uint32_t CM[PW_G][PW_COLS];        // column maxima of the group's rows
+  uint32_t RAW[PW_G + HT][PW_COLS];  // rows g0-HT .. g0+PW_G-1 (tie checks)
+  u64 top[PW_KMAX];                  // the warp's top-k, descending
+  u64 cbuf[PW_CBUF];                 // candidates of the group
+};
+
+template <int HT>
+__global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksParams p) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * PW_W + warp, f = blockIdx.y;
+  if (unit >= p.n_units) return;  // whole warp; no CTA-wide synchronisation below
+  PwSmem<HT> &S = reinterpret_cast<PwSmem<HT> *>(psm)[warp];
+  constexpr int NV = PW_G + 2 * HT;
+  const int strip = unit / p.st_chunks, chunk = unit - strip * p.st_chunks;
+  const int hr = p.half_rho, n_rho = p.n_rho, n_theta = p.n_theta;
+  const int cbase = strip * p.st_sw - hr;  // global column of loaded column 0
+  const int tb0 = chunk * p.st_tb;
+  const int tb1 = min(tb0 + p.st_tb, n_theta);
+  // lane l owns loaded columns l + 32 q (q < PW_CPT): every load instruction
+  // of the warp reads 32 consecutive words (fully coalesced)
+  const bool all_in = cbase >= 0 && cbase + PW_COLS <= n_rho;  // warp-uniform
+  uint32_t cinm = 0, ownm = 0;
+#pragma unroll
+  for (int q = 0; q < PW_CPT; ++q) {
+    const int j = lane + 32 * q, col = cbase + j;
+    const bool in = col >= 0 && col < n_rho;
+    cinm |= static_cast<uint32_t>(in) << q;
+    ownm |= static_cast<uint32_t>(in && j >= hr && j < hr + p.st_sw) << q;
+  }
+  const uint32_t *rowp = p.acc + (static_cast<int64_t>(f) * n_theta + (tb0 - HT)) * n_rho + cbase + lane;
+  int rnext = tb0 - HT;
+  auto load_row = [&](uint32_t (&dst)[PW_CPT]) {
+    if (rnext >= 0 && rnext < n_theta) {
+      if (all_in) {
+#pragma unroll
+        for (int q = 0; q < PW_CPT; ++q) dst[q] = __ldg(rowp + 32 * q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < PW_CPT; ++q) dst[q] = ((cinm >> q) & 1u) ? __ldg(rowp + 32 * q) : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < PW_CPT; ++q) dst[q] = 0u;
+    }
+    rowp += n_rho;
+    ++rnext;
+  };
+
+  int ntop = 0;                 // warp-uniform
+  uint32_t tau = p.floor_votes;  // warp-uniform
+  uint32_t V[NV][PW_CPT], N[PW_G][PW_CPT];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) load_row(V[k]);
+
+  for (int g0 = tb0; g0 < tb1; g0 += PW_G) {
+    if (g0 + PW_G < tb1) {
+#pragma unroll
+      for (int k = 0; k < PW_G; ++k) load_row(N[k]);
+    }
+    uint32_t gt = 0;
+    if (lane == 0) gt = *reinterpret_cast<volatile uint32_t *>(p.gtau + f);
+    const int nrows = min(PW_G, tb1 - g0);
+    uint32_t surv = 0;
+#pragma unroll
+    for (int i = 0; i < PW_G; ++i) {
+#pragma unroll
+      for (int q = 0; q < PW_CPT; ++q) {
+        uint32_t mm = V[i][q];
+#pragma unroll
+        for (int k = 1; k <= 2 * HT; ++k) mm = max(mm, V[i + k][q]);
+        S.CM[i][lane + 32 * q] = mm;
+        // v <= mm always: v >= max(mm, tau) <=> v == its column maximum and >= tau
+        surv |= static_cast<uint32_t>(V[i + HT][q] >= max(mm, tau)) << (i * PW_CPT + q);
+      }
+    }
+    surv &= (ownm | (ownm << PW_CPT));
+    if (nrows < PW_G) surv &= (1u << (nrows * PW_CPT)) - 1u;
+#pragma unroll
+    for (int k = 0; k < PW_G + HT; ++k)
+#pragma unroll
+      for (int q = 0; q < PW_CPT; ++q) S.RAW[k][lane + 32 * q] = V[k][q];
+    __syncwarp();
+    // cheap per-lane prefilter on the nearest column maxima, then a
+    // warp-cooperative exact test of every remaining survivor
+    {
+      uint32_t t = surv;
+      while (t) {
+        const int b = __ffs(t) - 1;
+        t &= t - 1u;
+        const int i = b / PW_CPT, q = b - i * PW_CPT;
+        const int j = lane + 32 * q;
+        const uint32_t v = S.CM[i][j];
+        const int dmax = min(hr, 2);
+        bool ok = true;
+        for (int d = 1; d <= dmax; ++d) ok = ok && S.CM[i][j - d] <= v && S.CM[i][j + d] <= v;
+        if (!ok) surv &= ~(1u << b);
+      }
+    }
+    int ncand = 0;
+    for (;;) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, surv != 0u);
+      if (!bal) break;
+      const int src = __ffs(bal) - 1;
+      const int b = __shfl_sync(0xffffffffu, __ffs(surv) - 1, src);
+      if (lane == src) surv &= surv - 1u;
+      const int i = b / PW_CPT, q = b - i * PW_CPT;
+      const int j = src + 32 * q;
+      const uint32_t *cmr = S.CM[i] + j;
+      const uint32_t v = *cmr;
+      bool bad = lane < HT && S.RAW[i + lane][j] == v;
+      bool tie = false;
+      for (int d = 1 + lane; d <= hr; d += 32) {
+        const uint32_t l = cmr[-d], r = cmr[d];
+        bad = bad || l > v || r > v;
+        tie = tie || l == v || r == v;
+      }
+      if (!__any_sync(0xffffffffu, bad) && __any_sync(0xffffffffu, tie)) {
+        for (int d = 1 + lane; d <= hr && !bad; d += 32) {
+          if (cmr[-d] == v)
+            for (int k = i; k <= i + HT && !bad; ++k) bad = S.RAW[k][j - d] == v;
+          if (!bad && cmr[d] == v)
+            for (int k = i; k < i + HT && !bad; ++k) bad = S.RAW[k][j + d] == v;
+        }
+      }
+      if (!__any_sync(0xffffffffu, bad)) {
+        if (lane == 0 && LD_CHK(ncand < PW_CBUF))
+          S.cbuf[ncand] = mk_key(v, static_cast<uint32_t>((g0 + i) * n_rho + cbase + j));
+        ++ncand;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {  // insertion into the warp's top-k (candidates are rare)
+      for (int c = 0; c < ncand; ++c) {
+        const u64 key = S.cbuf[c];
+        if (ntop == p.k && key <= S.top[ntop - 1]) continue;
+        int pos = ntop < p.k ? ntop : p.k - 1;
+        while (pos > 0 && S.top[pos - 1] < key) {
+          S.top[pos] = S.top[pos - 1];
+          --pos;
+        }
+        S.top[pos] = key;
+        if (ntop < p.k) ++ntop;
+      }
+      if (ncand > 0 && ntop == p.k) {
+        const uint32_t kth = static_cast<uint32_t>(S.top[p.k - 1] >> 32);
+        if (kth > gt) atomicMax(p.gtau + f, kth);
+        gt = max(gt, kth);
+      }
+    }
+    ntop = __shfl_sync(0xffffffffu, ntop, 0);
+    tau = max(tau, __shfl_sync(0xffffffffu, gt, 0));
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 2 * HT; ++k)
+#pragma unroll
+      for (int q = 0; q < PW_CPT; ++q) V[k][q] = V[k + PW_G][q];
+#pragma unroll
+    for (int k = 0; k < PW_G; ++k)
+#pragma unroll
+      for (int q = 0; q < PW_CPT; ++q) V[2 * HT + k][q] = N[k][q];
+  }
+  u64 *out = p.band_keys + (static_cast<int64_t>(f) * p.n_units + unit) * p.k;
+  for (int i = lane; i < p.k; i += 32) out[i] = i < ntop ? S.top[i] : 0ull;
+}
+
+typedef void (*WarpKernel)(const PeaksParams);
+static WarpKernel warp_kernel(int ht) {
+  switch (ht) {
+    case 0: return peaks_warp_kernel<0>;
+    case 1: return peaks_warp_kernel<1>;
+    case 2: return peaks_warp_kernel<2>;
+    case 3: return peaks_warp_kernel<3>;
+    default: return nullptr;
+  }
+}
+static size_t warp_smem_bytes(int ht) {
+  switch (ht) {
+    case 0: return PW_W * sizeof(PwSmem<0>);
+    case 1: return PW_W * sizeof(PwSmem<1>);
+    case 2: return PW_W * sizeof(PwSmem<2>);
+    default: return PW_W * sizeof(PwSmem<3>);
+  }
+}
+
+// Warp-strip geometry; false when the window or k do not fit the kernel.
+static bool peaks_warp_plan(int batch, int n_theta, int n_rho, int half_theta, int half_rho, int k,
+                            int sm_count, PeaksParams *p, size_t *smem) {
+  const char *env = getenv("LD_PEAKS_KERNEL");
+  if (env && env[0] == 's') return false;  // force the CTA streaming kernel
+  if (half_theta > 3 || half_rho < 4 || half_rho > 64 || k > PW_KMAX || n_rho < PW_CPT)
+    return false;
+  const int sw = PW_COLS - 2 * half_rho;
+  const int strips = (n_rho + sw - 1) / sw;
+  const long slots = 2L * PW_W * sm_count;  // warps resident at once
+  int chunks = 1;
+  double best = -1.0;
+  for (int c = 1; c <= 64; ++c) {
+    int tb = (n_theta + c - 1) / c;
+    tb = (tb + PW_G - 1) / PW_G * PW_G;
+    if (tb < 8 && c > 1) break;
+    const int cc = (n_theta + tb - 1) / tb;
+    const long units = static_cast<long>(batch) * strips * cc;
+    const long waves = (units + slots - 1) / slots;
+    const double eff = static_cast<double>(units) / (waves * slots) * tb / (tb + 2.0 * half_theta);
+    if (eff > best + 1e-3) {
+      best = eff;
+      chunks = cc;
+    }
+  }
+  int tb = (n_theta + chunks - 1) / chunks;
+  tb = (tb + PW_G - 1) / PW_G * PW_G;
+  chunks = (n_theta + tb - 1) / tb;
+  // the workspace holds ceil(n_theta/16) * ceil(n_rho/32) unit lists per frame
+  const long cap = static_cast<long>((n_theta + PT_TR - 1) / PT_TR) * ((n_rho + 31) / 32);
+  if (static_cast<long>(strips) * chunks > cap) return false;
+  p->st_sw = sw;
+  p->st_strips = strips;
+  p->st_tb = tb;
+  p->st_chunks = chunks;
+  p->n_units = strips * chunks;
+  *smem = warp_smem_bytes(half_theta);
+  return true;
+}
+
 typedef void (*TileKernel)(const PeaksParams);
 static TileKernel tile_kernel(int ht) {
   switch (ht) {
@@ -797,6 +1040,7 @@ size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k) {
 static bool g_tile_attr[64][PT_MAX_HT + 1];
 
 static bool g_stream_attr[64][2][PT_MAX_HT + 1];
+static bool g_warp_attr[64][4];
 
 cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   PeaksParams p = p_in;
@@ -810,6 +1054,19 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int cpt = 0;
   if (!force_band && !force_tile &&
+      peaks_warp_plan(p.batch, p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem)) {
+    cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+    if (em != cudaSuccess) return em;
+    WarpKernel kern = warp_kernel(p.half_theta);
+    if (!g_warp_attr[dev & 63][p.half_theta]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      g_warp_attr[dev & 63][p.half_theta] = true;
+    }
+    dim3 g1((p.n_units + PW_W - 1) / PW_W, p.batch);
+    kern<<<g1, 32 * PW_W, smem, stream>>>(p);
+  } else if (!force_band && !force_tile &&
       peaks_stream_plan(p.batch, p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
                         &smem)) {
     cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);

@@ -326,12 +326,12 @@ def test_banded_accumulators_sum_to_whole(ld, oracle):
         assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want), n
 
 
-@pytest.mark.parametrize("kernel", ["stream", "tile", "band"])
+@pytest.mark.parametrize("kernel", ["auto", "stream", "tile", "band"])
 def test_peaks_all_kernels_windows(ld, oracle, kernel, monkeypatch):
-    # the streaming kernel (default, half_theta <= 12), the tiled kernel and the
-    # generic band kernel (forced, or chosen for large windows) agree with the
-    # oracle
-    if kernel != "stream":
+    # the default choice (warp-strip kernel for narrow windows, else the CTA
+    # streaming kernel), the forced CTA streaming kernel, the tiled kernel and
+    # the generic band kernel all agree with the oracle
+    if kernel != "auto":
         monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
     rng = np.random.default_rng(31)
     for trial, (ht, hr) in enumerate([(0, 0), (0, 5), (1, 1), (2, 29), (7, 44), (10, 116),
@@ -398,16 +398,17 @@ def test_banded_detector_more_ranks_than_rows(ld, oracle):
     assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want)
 
 
-@pytest.mark.parametrize("kernel", ["stream", "band"])
+@pytest.mark.parametrize("kernel", ["auto", "stream", "band"])
 def test_peaks_ties_and_plateaus(ld, oracle, kernel, monkeypatch):
     # equal maxima inside one window (plateaus, equal values left/right/above/
     # below) exercise the exact (theta, rho) tie-break; small value range makes
     # ties everywhere
-    if kernel != "stream":
+    if kernel != "auto":
         monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
     rng = np.random.default_rng(77)
     for trial, (ht, hr, k) in enumerate([(2, 29, 4), (1, 3, 64), (0, 0, 1024), (7, 44, 8),
-                                         (10, 116, 64), (12, 5, 16), (3, 0, 32)]):
+                                         (10, 116, 64), (12, 5, 16), (3, 0, 32), (3, 4, 64),
+                                         (0, 64, 2), (2, 15, 64), (1, 14, 7)]):
         acc = rng.integers(0, 3, size=(3, 97, 1500)).astype(np.uint32)
         acc[0, 40:43, 700:705] = 9                    # plateau
         acc[1, 10, 100] = acc[1, 10, 103] = acc[1, 12, 101] = 7
