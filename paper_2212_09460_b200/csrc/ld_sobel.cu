@@ -382,6 +382,7 @@ SobelCfg sobel_cfg() {
   if (env && env[0] == 's') return SobelCfg{8, 3, 2, 256};  // small staging, 3 stages
   if (env && env[0] == 't') return SobelCfg{8, 3, 2, 448};  // 3 stages, 2 CTAs/SM
   if (env && env[0] == 'o') return SobelCfg{8, 2, 3, 256};  // 3 CTAs/SM (register-capped)
+  if (env && env[0] == 'q') return SobelCfg{4, 4, 2, 1024};  // short tiles, 4 stages
   return SobelCfg{8, 2, 2};
 }
 
@@ -397,6 +398,9 @@ cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_c
   if (c.sr == 8 && c.cap == 0)
     return wb ? launch_cfg<8, 3, 2, true, 0>(tmap, p, n_ctas, stream)
               : launch_cfg<8, 3, 2, false, 0>(tmap, p, n_ctas, stream);
+  if (c.sr == 4 && c.stages == 4)
+    return wb ? launch_cfg<4, 4, 2, true, 1024>(tmap, p, n_ctas, stream)
+              : launch_cfg<4, 4, 2, false, 1024>(tmap, p, n_ctas, stream);
   if (c.sr == 8 && c.ctas_per_sm == 3)
     return wb ? launch_cfg<8, 2, 3, true, 256>(tmap, p, n_ctas, stream)
               : launch_cfg<8, 2, 3, false, 256>(tmap, p, n_ctas, stream);
