@@ -233,7 +233,8 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   p.n_bands = n_bands;
   p.koff = 16384 + (d << 15);
   p.acc = acc;
-  const size_t smem = align_up(static_cast<size_t>(rpb) * n_rho * 4, 16);
+  // + 16: the kernel shifts the slice to the destination's address modulo 16
+  const size_t smem = align_up(static_cast<size_t>(rpb) * n_rho * 4, 16) + 16;
   cudaError_t e = launch_hough(p, trig, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");
   return LD_OK;

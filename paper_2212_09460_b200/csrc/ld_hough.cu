@@ -49,7 +49,7 @@ __device__ __forceinline__ void vote_block(const uint32_t *el, uint32_t blk, uin
 
 __global__ void __launch_bounds__(HV_THREADS, 1)
     hough_vote_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
-  extern __shared__ __align__(16) uint32_t slice[];
+  extern __shared__ __align__(16) uint32_t slice_raw[];
   __shared__ uint4 rowk[HV_MAX_ROWS];  // per row: C, S, K = koff + (row address << 13)
 
   const int tid = threadIdx.x;
@@ -58,12 +58,17 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   const int t0 = band * p.rows_per_band;
   const int nr = min(p.rows_per_band, p.n_theta - t0);
   const int ncell = nr * p.n_rho;
+  uint32_t *dst = p.acc + (static_cast<int64_t>(f) * p.n_theta + t0) * p.n_rho;
+  // The slice starts at the same address modulo 16 as its destination, so the
+  // write-out can be one bulk (TMA) copy of its 16-byte-aligned middle part.
+  const int mw = static_cast<int>((reinterpret_cast<uintptr_t>(dst) & 15u) >> 2);
+  uint32_t *slice = slice_raw + mw;
   const uint32_t sbase = smem_u32(slice);
   const uint32_t row_bytes = static_cast<uint32_t>(p.n_rho) * 4u;
 
   {
-    uint4 *s4 = reinterpret_cast<uint4 *>(slice);
-    const int n4 = (ncell + 3) >> 2;
+    uint4 *s4 = reinterpret_cast<uint4 *>(slice_raw);
+    const int n4 = (mw + ncell + 3) >> 2;
     for (int i = tid; i < n4; i += HV_THREADS) s4[i] = make_uint4(0u, 0u, 0u, 0u);
     // The byte address of the counter of (row r, bin rho) is
     //   sbase + r*row_bytes + 4*rho = ((v + ((sbase + r*row_bytes) << 13)) >> 13) & ~3
@@ -78,23 +83,39 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   const uint32_t n_edges = p.counts[f];
   const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
 
-  // Each warp takes blocks of 256 consecutive list entries (8 per lane),
-  // interleaved across the CTA's warps; at step j its 32 lanes hold the 32
-  // consecutive entries blk + 32j + lane, which the compaction made spatially
-  // compact (ld_sobel.cu): per theta they fall into few consecutive rho bins,
-  // i.e. distinct banks, and equal bins merge in ATOMS.POPC.INC.  (Measured on
-  // B200: 16 entries per lane, or contiguous per-warp ranges, are slower.)
+  // Warps take blocks of consecutive list entries, interleaved across the
+  // CTA's warps: 16 entries per lane while whole rounds of such blocks remain
+  // (fewer edge loads per vote), then 8 per lane, then a predicated tail, so
+  // the warps finish within one short block of each other.  At step j a
+  // warp's 32 lanes hold the 32 consecutive entries blk + 32j + lane, which
+  // the compaction made spatially compact (ld_sobel.cu): per theta they fall
+  // into few consecutive rho bins, i.e. distinct banks, and equal bins merge
+  // in ATOMS.POPC.INC.
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = HV_THREADS / 32;
-  constexpr int EPL = 8;
-  uint32_t blk = static_cast<uint32_t>(warp) * (32u * EPL);
-  for (; blk + 32u * EPL <= n_edges; blk += NWARPS * 32u * EPL)
-    vote_block<EPL, true>(el, blk, n_edges, lane, nr, rowk);
-  if (blk < n_edges) vote_block<EPL, false>(el, blk, n_edges, lane, nr, rowk);
+  uint32_t base = 0;
+  for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
+    vote_block<16, true>(el, base + warp * 32u * 16u, n_edges, lane, nr, rowk);
+  uint32_t blk = base + static_cast<uint32_t>(warp) * (32u * 8u);
+  for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
+    vote_block<8, true>(el, blk, n_edges, lane, nr, rowk);
+  if (blk < n_edges) vote_block<8, false>(el, blk, n_edges, lane, nr, rowk);
   __syncthreads();
 
-  uint32_t *dst = p.acc + (static_cast<int64_t>(f) * p.n_theta + t0) * p.n_rho;
-  for (int i = tid; i < ncell; i += HV_THREADS) dst[i] = slice[i];
+  // write-out: unaligned head and tail words by threads, the aligned middle
+  // by one bulk shared->global copy (async proxy: fence the ATOMS writes first)
+  const int head = min((4 - mw) & 3, ncell);
+  const int mid = ((ncell - head) >> 2) << 2;  // words, multiple of 4
+  if (tid < head) dst[tid] = slice[tid];
+  for (int i = head + mid + tid; i < ncell; i += HV_THREADS) dst[i] = slice[i];
+  if (tid == 0 && mid > 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
+                 "r"(smem_u32(slice + head)), "r"(static_cast<uint32_t>(mid) * 4u)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
 }
 
 int hough_rows_per_band(int n_theta, int n_rho, size_t smem_limit, int *n_bands) {
