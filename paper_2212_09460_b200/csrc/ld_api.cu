@@ -215,10 +215,10 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   const int32_t d = rho_offset(width, height);
   if ((rc = check_trig(n_theta, cos_q15, sin_q15, width, height, d))) return rc;
   const int n_rho = 2 * d + 1;
-  const size_t limit = static_cast<size_t>(dev.smem_optin) - sizeof(uint4) * HV_MAX_ROWS - 1024;
-  int n_bands = 0;
-  const int rpb = hough_rows_per_band(n_theta, n_rho, limit, &n_bands);
-  if (rpb < 1) return fail(LD_ERR_UNSUPPORTED, "one accumulator row (%d bins) exceeds shared memory", n_rho);
+  int ctas = 1, rpb = 0, n_bands = 0;
+  size_t smem = 0;
+  if (!hough_plan(n_theta, n_rho, static_cast<size_t>(dev.smem_optin), &ctas, &rpb, &n_bands, &smem))
+    return fail(LD_ERR_UNSUPPORTED, "one accumulator row (%d bins) exceeds shared memory", n_rho);
   static thread_local TrigTable trig;  // 16 KB: keep it off the stack
   memcpy(trig.c, cos_q15, sizeof(int32_t) * n_theta);
   memcpy(trig.s, sin_q15, sizeof(int32_t) * n_theta);
@@ -233,9 +233,7 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   p.n_bands = n_bands;
   p.koff = 16384 + (d << 15);
   p.acc = acc;
-  // + 16: the kernel shifts the slice to the destination's address modulo 16
-  const size_t smem = align_up(static_cast<size_t>(rpb) * n_rho * 4, 16) + 16;
-  cudaError_t e = launch_hough(p, trig, smem, stream);
+  cudaError_t e = launch_hough(p, trig, ctas, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");
   return LD_OK;
 }

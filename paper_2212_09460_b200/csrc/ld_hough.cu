@@ -47,8 +47,10 @@ __device__ __forceinline__ void vote_block(const uint32_t *el, uint32_t blk, uin
   }
 }
 
-__global__ void __launch_bounds__(HV_THREADS, 1)
+template <int CTAS>
+__global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
     hough_vote_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
+  constexpr int NT = HV_THREADS / CTAS;
   extern __shared__ __align__(16) uint32_t slice_raw[];
   __shared__ uint4 rowk[HV_MAX_ROWS];  // per row: C, S, K = koff + (row address << 13)
 
@@ -69,12 +71,12 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   {
     uint4 *s4 = reinterpret_cast<uint4 *>(slice_raw);
     const int n4 = (mw + ncell + 3) >> 2;
-    for (int i = tid; i < n4; i += HV_THREADS) s4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < n4; i += NT) s4[i] = make_uint4(0u, 0u, 0u, 0u);
     // The byte address of the counter of (row r, bin rho) is
     //   sbase + r*row_bytes + 4*rho = ((v + ((sbase + r*row_bytes) << 13)) >> 13) & ~3
     // with v = x*C + y*S + koff in [0, 2^31) (host range proof) and the row
     // address < 2^18, so the folded sum stays below 2^32: exact in uint32.
-    for (int i = tid; i < nr; i += HV_THREADS)
+    for (int i = tid; i < nr; i += NT)
       rowk[i] = make_uint4(static_cast<uint32_t>(trig.c[t0 + i]), static_cast<uint32_t>(trig.s[t0 + i]),
                            static_cast<uint32_t>(p.koff) + ((sbase + i * row_bytes) << 13), 0u);
   }
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   // into few consecutive rho bins, i.e. distinct banks, and equal bins merge
   // in ATOMS.POPC.INC.
   const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NWARPS = HV_THREADS / 32;
+  constexpr int NWARPS = NT / 32;
   uint32_t base = 0;
   for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
     vote_block<16, true>(el, base + warp * 32u * 16u, n_edges, lane, nr, rowk);
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   const int head = min((4 - mw) & 3, ncell);
   const int mid = ((ncell - head) >> 2) << 2;  // words, multiple of 4
   if (tid < head) dst[tid] = slice[tid];
-  for (int i = head + mid + tid; i < ncell; i += HV_THREADS) dst[i] = slice[i];
+  for (int i = head + mid + tid; i < ncell; i += NT) dst[i] = slice[i];
   if (tid == 0 && mid > 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
@@ -118,9 +120,9 @@ __global__ void __launch_bounds__(HV_THREADS, 1)
   }
 }
 
-int hough_rows_per_band(int n_theta, int n_rho, size_t smem_limit, int *n_bands) {
+static int rows_per_band(int n_theta, int n_rho, size_t limit, int *n_bands) {
   const size_t row = static_cast<size_t>(n_rho) * 4u;
-  int rows_max = static_cast<int>(smem_limit / row);
+  int rows_max = static_cast<int>(limit / row);
   if (rows_max > HV_MAX_ROWS) rows_max = HV_MAX_ROWS;
   if (rows_max < 1) return 0;
   const int nb = (n_theta + rows_max - 1) / rows_max;
@@ -128,21 +130,38 @@ int hough_rows_per_band(int n_theta, int n_rho, size_t smem_limit, int *n_bands)
   return (n_theta + nb - 1) / nb;
 }
 
-static bool g_hough_attr[64];
+int hough_plan(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *rpb, int *n_bands,
+               size_t *smem_bytes) {
+  // per CTA: the slice (+16 bytes of alignment shift), rowk, and a margin
+  const size_t fixed = sizeof(uint4) * HV_MAX_ROWS + 1024 + 16;
+  int nb1 = 0, nb2 = 0;
+  const int r1 = rows_per_band(n_theta, n_rho, smem_optin - fixed, &nb1);
+  if (r1 < 1) return 0;
+  const int r2 = rows_per_band(n_theta, n_rho, smem_optin / 2 - fixed, &nb2);
+  const bool two = r2 >= 8 && (smem_optin - fixed) / (static_cast<size_t>(n_rho) * 4u) >= 16;
+  *ctas = two ? 2 : 1;
+  *rpb = two ? r2 : r1;
+  *n_bands = two ? nb2 : nb1;
+  *smem_bytes = ((static_cast<size_t>(*rpb) * n_rho * 4 + 15) / 16) * 16 + 16;
+  return 1;
+}
 
-cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, size_t smem_bytes,
+static bool g_hough_attr[64][3];
+
+cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, size_t smem_bytes,
                          cudaStream_t stream) {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!g_hough_attr[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(hough_vote_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024 - static_cast<int>(sizeof(uint4)) * HV_MAX_ROWS);
+  auto kern = ctas == 2 ? hough_vote_kernel<2> : hough_vote_kernel<1>;
+  if (!g_hough_attr[dev & 63][ctas]) {
+    // the largest slice hough_plan can request for this CTA count (rowk is static)
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024 / ctas - static_cast<int>(sizeof(uint4)) * HV_MAX_ROWS);
     if (e != cudaSuccess) return e;
-    g_hough_attr[dev & 63] = true;
+    g_hough_attr[dev & 63][ctas] = true;
   }
   dim3 grid(p.n_bands, p.batch);
-  hough_vote_kernel<<<grid, HV_THREADS, smem_bytes, stream>>>(p, trig);
+  kern<<<grid, HV_THREADS / ctas, smem_bytes, stream>>>(p, trig);
   note_launch();
   return cudaGetLastError();
 }

@@ -65,12 +65,16 @@ struct HoughParams {
   uint32_t *acc;
 };
 
-constexpr int HV_THREADS = 1024;
+constexpr int HV_THREADS = 1024;  // threads per SM; a CTA has HV_THREADS / CTAS of them
 constexpr int HV_MAX_ROWS = 256;
 
-cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, size_t smem_bytes,
+// CTAs per SM: 2 (half the shared memory each, so one CTA's prologue and
+// write-out overlap the other's voting) when a band then still holds >= 8
+// rows, else 1.  Returns 0 if a single row does not fit.
+int hough_plan(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *rows_per_band,
+               int *n_bands, size_t *smem_bytes);
+cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, size_t smem_bytes,
                          cudaStream_t stream);
-int hough_rows_per_band(int n_theta, int n_rho, size_t smem_limit, int *n_bands);
 
 // ---------------------------------------------------------------------------
 // B4: peaks (ld_peaks.cu)
