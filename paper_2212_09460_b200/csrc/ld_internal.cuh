@@ -21,8 +21,8 @@ constexpr int SB_STRIPS = 16;       // thread strips per tile (vertical)
 constexpr int SB_THREADS = SB_CHUNKS * SB_STRIPS;  // 224 = 7 consumer warps
 constexpr int SB_STAGE_CAP = 1024;  // per-warp edge staging buffer (uint32 entries)
 
-// compile-time variants: SR output rows per strip (tile height 16*SR), TMA ring
-// depth, CTAs per SM; selected on the host (LD_SOBEL_CFG=4 picks the SR=4 one)
+// launch configuration: SR output rows per strip (tile height 16*SR), TMA ring
+// depth, CTAs per SM, per-warp edge staging entries
 struct SobelCfg {
   int sr, stages, ctas_per_sm;
   int cap = SB_STAGE_CAP;  // per-warp edge staging entries (0: direct global stores)

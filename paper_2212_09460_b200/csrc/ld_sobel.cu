@@ -374,47 +374,20 @@ static cudaError_t launch_cfg(const CUtensorMap &tmap, const SobelParams &p, int
   return cudaGetLastError();
 }
 
-SobelCfg sobel_cfg() {
-  const char *env = getenv("LD_SOBEL_CFG");
-  if (env && env[0] == '4') return SobelCfg{4, 3, 3};
-  if (env && env[0] == '6') return SobelCfg{6, 3, 2};
-  if (env && env[0] == 'd') return SobelCfg{8, 3, 2, 0};    // no staging, 3 stages
-  if (env && env[0] == 's') return SobelCfg{8, 3, 2, 256};  // small staging, 3 stages
-  if (env && env[0] == 't') return SobelCfg{8, 3, 2, 448};  // 3 stages, 2 CTAs/SM
-  if (env && env[0] == 'o') return SobelCfg{8, 2, 3, 256};  // 3 CTAs/SM (register-capped)
-  if (env && env[0] == 'q') return SobelCfg{4, 4, 2, 1024};  // short tiles, 4 stages
-  return SobelCfg{8, 2, 2};
-}
+// Launch configuration: SR = 8 rows per thread strip (128-row tiles), 2 TMA
+// stages, 2 CTAs per SM, 1024-entry per-warp edge staging.  Measured on B200
+// (profiles/) against 3 stages (smaller staging), 3 CTAs per SM
+// (register-capped), 64- and 96-row tiles and direct (unstaged) edge stores:
+// all slower on cfg3 and cfg4.
+SobelCfg sobel_cfg() { return SobelCfg{8, 2, 2, SB_STAGE_CAP}; }
 
 cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_count,
                          cudaStream_t stream) {
   const SobelCfg c = sobel_cfg();
   const int64_t max_ctas = static_cast<int64_t>(sm_count) * c.ctas_per_sm;
   const int n_ctas = static_cast<int>(p.n_tiles < max_ctas ? p.n_tiles : max_ctas);
-  const bool wb = p.binary != nullptr;
-  if (c.sr == 4)
-    return wb ? launch_cfg<4, 3, 3, true>(tmap, p, n_ctas, stream)
-              : launch_cfg<4, 3, 3, false>(tmap, p, n_ctas, stream);
-  if (c.sr == 8 && c.cap == 0)
-    return wb ? launch_cfg<8, 3, 2, true, 0>(tmap, p, n_ctas, stream)
-              : launch_cfg<8, 3, 2, false, 0>(tmap, p, n_ctas, stream);
-  if (c.sr == 4 && c.stages == 4)
-    return wb ? launch_cfg<4, 4, 2, true, 1024>(tmap, p, n_ctas, stream)
-              : launch_cfg<4, 4, 2, false, 1024>(tmap, p, n_ctas, stream);
-  if (c.sr == 8 && c.ctas_per_sm == 3)
-    return wb ? launch_cfg<8, 2, 3, true, 256>(tmap, p, n_ctas, stream)
-              : launch_cfg<8, 2, 3, false, 256>(tmap, p, n_ctas, stream);
-  if (c.sr == 8 && c.cap == 448)
-    return wb ? launch_cfg<8, 3, 2, true, 448>(tmap, p, n_ctas, stream)
-              : launch_cfg<8, 3, 2, false, 448>(tmap, p, n_ctas, stream);
-  if (c.sr == 8 && c.cap == 256)
-    return wb ? launch_cfg<8, 3, 2, true, 256>(tmap, p, n_ctas, stream)
-              : launch_cfg<8, 3, 2, false, 256>(tmap, p, n_ctas, stream);
-  if (c.sr == 6)
-    return wb ? launch_cfg<6, 3, 2, true>(tmap, p, n_ctas, stream)
-              : launch_cfg<6, 3, 2, false>(tmap, p, n_ctas, stream);
-  return wb ? launch_cfg<8, 2, 2, true>(tmap, p, n_ctas, stream)
-            : launch_cfg<8, 2, 2, false>(tmap, p, n_ctas, stream);
+  return p.binary != nullptr ? launch_cfg<8, 2, 2, true>(tmap, p, n_ctas, stream)
+                             : launch_cfg<8, 2, 2, false>(tmap, p, n_ctas, stream);
 }
 
 }  // namespace ld
