@@ -733,7 +733,6 @@ static bool peaks_stream_plan(int batch, int n_theta, int n_rho, int half_theta,
 // warp-cooperative exact test of the few survivors.
 // ---------------------------------------------------------------------------
 constexpr int PW_CPT = 8, PW_G = 2, PW_W = 8, PW_COLS = 32 * PW_CPT, PW_KMAX = 64, PW_CBUF = 128;
-constexpr int PW_NPF = 12;  // rows of L2 prefetch beyond the register prefetch
 
 template <int HT>
 struct PwSmem {
