@@ -56,12 +56,15 @@ def lib():
         L.ldo_rho_offset.restype = i32
         L.ldo_sobel_magnitude.argtypes = [P, i32, i32, i64, P]
         L.ldo_sobel_binarize.argtypes = [P, i32, i32, i64, i32, P]
+        L.ldo_sobel_magnitude_ex.argtypes = [P, i32, i32, i64, i32, P]
+        L.ldo_sobel_binarize_ex.argtypes = [P, i32, i32, i64, i32, i32, P]
         L.ldo_compact.argtypes = [P, i32, i32, P, i64, P]
         L.ldo_hough_accumulate.argtypes = [P, i64, i32, i32, i32, P, P, P]
         L.ldo_hough_peaks.argtypes = [P, i32, i32, i32, i32, u32, i32, P, P]
         L.ldo_detect.argtypes = [P, i32, i32, i64, i32, i32, P, P, i32, i32, u32, i32,
                                  P, P, P, P, P, P]
-        for f in ("ldo_sobel_magnitude", "ldo_sobel_binarize", "ldo_compact",
+        for f in ("ldo_sobel_magnitude", "ldo_sobel_binarize", "ldo_sobel_magnitude_ex",
+                  "ldo_sobel_binarize_ex", "ldo_compact",
                   "ldo_hough_accumulate", "ldo_hough_peaks", "ldo_detect"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -105,6 +108,27 @@ def sobel_binarize(gray: np.ndarray, threshold: int) -> np.ndarray:
     out = np.empty((h, w), np.uint8)
     _check(lib().ldo_sobel_binarize(_ptr(g), w, h, w, int(threshold), _ptr(out)),
            "sobel_binarize")
+    return out
+
+
+ZERO_PAD, CLAMP_255 = 1, 2  # ldo_sobel_*_ex flags (NEXT 4)
+
+
+def sobel_magnitude_ex(gray: np.ndarray, flags: int) -> np.ndarray:
+    g = _gray(gray)
+    h, w = g.shape
+    mag = np.empty((h, w), np.int32)
+    _check(lib().ldo_sobel_magnitude_ex(_ptr(g), w, h, w, int(flags), _ptr(mag)),
+           "sobel_magnitude_ex")
+    return mag
+
+
+def sobel_binarize_ex(gray: np.ndarray, threshold: int, flags: int) -> np.ndarray:
+    g = _gray(gray)
+    h, w = g.shape
+    out = np.empty((h, w), np.uint8)
+    _check(lib().ldo_sobel_binarize_ex(_ptr(g), w, h, w, int(threshold), int(flags), _ptr(out)),
+           "sobel_binarize_ex")
     return out
 
 

@@ -68,6 +68,54 @@ int ldo_sobel_binarize(const uint8_t *gray, int32_t width, int32_t height,
   return rc;
 }
 
+int ldo_sobel_magnitude_ex(const uint8_t *gray, int32_t width, int32_t height,
+                           int64_t pitch, int32_t flags, int32_t *mag) {
+  if (!(flags & LDO_ZERO_PAD)) return ldo_sobel_magnitude(gray, width, height, pitch, mag);
+  if (!gray || !mag || width < 1 || height < 1 || pitch < width) return LDO_EARG;
+  for (int32_t y = 0; y < height; y++) {
+    for (int32_t x = 0; x < width; x++) {
+      int32_t gx = 0, gy = 0; /* Eq. 1 on the zero-padded image */
+      for (int i = 0; i < 3; i++) {
+        for (int j = 0; j < 3; j++) {
+          int32_t yy = y - 1 + i, xx = x - 1 + j;
+          int32_t p = (yy < 0 || yy >= height || xx < 0 || xx >= width)
+                          ? 0
+                          : gray[(int64_t)yy * pitch + xx];
+          gx += SOBEL_X[i][j] * p;
+          gy += SOBEL_Y[i][j] * p;
+        }
+      }
+      mag[(int64_t)y * width + x] = iabs32(gx) + iabs32(gy);
+    }
+  }
+  return LDO_OK;
+}
+
+int ldo_sobel_binarize_ex(const uint8_t *gray, int32_t width, int32_t height,
+                          int64_t pitch, int32_t threshold, int32_t flags,
+                          uint8_t *binary) {
+  if (!(flags & LDO_ZERO_PAD) && !(flags & LDO_CLAMP_255))
+    return ldo_sobel_binarize(gray, width, height, pitch, threshold, binary);
+  if (!gray || !binary || width < 1 || height < 1 || pitch < width) return LDO_EARG;
+  int32_t *mag = (int32_t *)malloc(sizeof(int32_t) * (size_t)width * (size_t)height);
+  if (!mag) return LDO_ENOMEM;
+  int rc = ldo_sobel_magnitude_ex(gray, width, height, pitch, flags, mag);
+  if (rc == LDO_OK) {
+    for (int32_t y = 0; y < height; y++) {
+      for (int32_t x = 0; x < width; x++) {
+        int64_t i = (int64_t)y * width + x;
+        int32_t g = mag[i];
+        if ((flags & LDO_CLAMP_255) && g > 255) g = 255;
+        int border = (x == 0 || x == width - 1 || y == 0 || y == height - 1);
+        int forced0 = border && !(flags & LDO_ZERO_PAD); /* R2 unless zero-padded */
+        binary[i] = (!forced0 && g >= threshold) ? 255 : 0;
+      }
+    }
+  }
+  free(mag);
+  return rc;
+}
+
 int ldo_compact(const uint8_t *binary, int32_t width, int32_t height,
                 uint32_t *edges, int64_t cap, int64_t *n_edges) {
   if (!binary || !n_edges || width < 1 || height < 1 || width > 65536 ||

@@ -62,6 +62,23 @@ int ldo_sobel_magnitude(const uint8_t *gray, int32_t width, int32_t height,
 int ldo_sobel_binarize(const uint8_t *gray, int32_t width, int32_t height,
                        int64_t pitch, int32_t threshold, uint8_t *binary);
 
+/* Border and clamp modes (DESIGN R23, R24).
+ * LDO_ZERO_PAD: the paper's own border -- "zero padding" of the input so the
+ *   output has the input's size (P:106 FPGA, P:157 GPU): every
+ *   pixel, border included, is filtered, with 0 for neighbours outside.
+ * LDO_CLAMP_255: |G| is clamped to 255 before the threshold, SPEC's 8-bit
+ *   EdgeImage.
+ * ldo_sobel_magnitude_ex writes the (unclamped) magnitude under the border
+ * mode of `flags`; ldo_sobel_binarize_ex binarizes it with ">=" (R4), applying
+ * the clamp when asked.  flags = 0 is exactly ldo_sobel_binarize. */
+#define LDO_ZERO_PAD 1
+#define LDO_CLAMP_255 2
+int ldo_sobel_magnitude_ex(const uint8_t *gray, int32_t width, int32_t height,
+                           int64_t pitch, int32_t flags, int32_t *mag);
+int ldo_sobel_binarize_ex(const uint8_t *gray, int32_t width, int32_t height,
+                          int64_t pitch, int32_t threshold, int32_t flags,
+                          uint8_t *binary);
+
 /* Edge-coordinate list ("threads read the coordinates of input pixels
  * stored in the global memory"): raster scan (y-major, then x) of binary
  * [height][width]; appends (y << 16) | x for every pixel equal to 255.

@@ -87,6 +87,52 @@ def test_sobel_matches_scipy_correlate(oracle):
         assert np.array_equal(mag[1:-1, 1:-1], np.abs(cx) + np.abs(cy))
 
 
+# ----------------------------------------------------------------------------
+# NEXT 4: the paper's zero-padded border and SPEC's 8-bit clamp
+# (S:111-116); DESIGN R23, R24
+# ----------------------------------------------------------------------------
+def test_zero_pad_hand_computed(oracle):
+    # all-255 3x3, zero-padded: corners see 4 bright pixels, edge midpoints 6
+    img = np.full((3, 3), 255, np.uint8)
+    mag = oracle.sobel_magnitude_ex(img, oracle.ZERO_PAD)
+    assert mag.tolist() == [[1530, 1020, 1530], [1020, 0, 1020], [1530, 1020, 1530]]
+    # a single pixel surrounded by padding: Gx = Gy = 0
+    assert oracle.sobel_magnitude_ex(np.array([[200]], np.uint8), oracle.ZERO_PAD)[0, 0] == 0
+    # 1 x 3 row [0, 0, 255]: the middle pixel sees +255 twice in Gx (rows -1, +1 are 0)
+    row = np.array([[0, 0, 255]], np.uint8)
+    assert oracle.sobel_magnitude_ex(row, oracle.ZERO_PAD)[0, 1] == 2 * 255
+
+
+def test_zero_pad_matches_scipy_constant_mode(oracle):
+    # library routine: scipy correlation over the zero-padded image ('same'
+    # output, fill value 0) with the Fig. 2 kernels, every pixel incl. borders
+    for seed, (h, w) in enumerate([(1, 1), (1, 7), (2, 2), (3, 5), (17, 9), (40, 33)]):
+        img = synth.random_image(100 + seed, w, h).astype(np.int64)
+        gx = signal.correlate2d(img, SX, mode="same", boundary="fill", fillvalue=0)
+        gy = signal.correlate2d(img, SY, mode="same", boundary="fill", fillvalue=0)
+        mag = oracle.sobel_magnitude_ex(img.astype(np.uint8), oracle.ZERO_PAD)
+        assert np.array_equal(mag, np.abs(gx) + np.abs(gy)), (h, w)
+        # interior identical to the forced-zero-border magnitude
+        assert np.array_equal(mag[1:-1, 1:-1], oracle.sobel_magnitude(img.astype(np.uint8))[1:-1, 1:-1])
+
+
+def test_clamp_and_flag_combinations(oracle):
+    img = synth.random_image(5, 50, 31)
+    for t in (-3, 0, 1, 200, 255):
+        # clamping to 255 cannot change a ">= T" decision for T <= 255
+        assert np.array_equal(oracle.sobel_binarize_ex(img, t, oracle.CLAMP_255),
+                              oracle.sobel_binarize(img, t))
+        assert np.array_equal(oracle.sobel_binarize_ex(img, t, oracle.CLAMP_255 | oracle.ZERO_PAD),
+                              oracle.sobel_binarize_ex(img, t, oracle.ZERO_PAD))
+    for t in (256, 1000, 1530):  # above the clamp nothing passes
+        assert not oracle.sobel_binarize_ex(img, t, oracle.CLAMP_255).any()
+        assert not oracle.sobel_binarize_ex(img, t, oracle.CLAMP_255 | oracle.ZERO_PAD).any()
+    assert np.array_equal(oracle.sobel_binarize_ex(img, 200, 0), oracle.sobel_binarize(img, 200))
+    zp = oracle.sobel_binarize_ex(img, 200, oracle.ZERO_PAD)
+    mag = oracle.sobel_magnitude_ex(img, oracle.ZERO_PAD)
+    assert np.array_equal(zp == 255, mag >= 200)
+
+
 def test_sobel_exhaustive_binary_patches(oracle):
     # every {0,255}^9 patch: |G| even, <= 1530, max attained; matches the literal sum
     mags = []
