@@ -105,6 +105,27 @@ int ld_sobel_binarize(const uint8_t *gray, const ld_image *img, int32_t threshol
                       uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
                       uint32_t *edge_count, void *stream);
 
+/* Border / clamp modes of the *_ex entry points (DESIGN
+ * R23, R24).  0 = the default of this ABI (1-px output border forced to 0,
+ * raw |Gx|+|Gy| compared with T).
+ *  LD_FLAG_ZERO_PAD : the paper's own border -- the input is zero-padded by
+ *                     one pixel so the output has the input's size (P:106
+ *                     FPGA, P:157 GPU): every pixel, border included, is
+ *                     filtered with 0 for neighbours outside the image (the
+ *                     banded halo rows inside the image stay real rows).
+ *  LD_FLAG_CLAMP_255: |G| is clamped to 255 before the threshold (SPEC's 8-bit
+ *                     EdgeImage): identical for T <= 255, no edge
+ *                     above. */
+#define LD_FLAG_ZERO_PAD 1u
+#define LD_FLAG_CLAMP_255 2u
+
+/* ld_sobel_binarize with border/clamp flags (any other bit: LD_ERR_INVALID_ARG).
+ * With LD_FLAG_ZERO_PAD every owned pixel can be an edge, so edge_stride must
+ * be >= (row_end-row_begin) * width. */
+int ld_sobel_binarize_ex(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                         uint32_t flags, uint8_t *binary, uint32_t *edge_xy,
+                         int64_t edge_stride, uint32_t *edge_count, void *stream);
+
 /* Step 3 (Eq. 3; GPU design P:171-175): theta-partitioned voting.
  * acc[f][t][r] = #{ edges e of frame f : ((x*C[t] + y*S[t] + 2^14) >> 15) + D == r }
  * (arithmetic shift = floor; i.e. r - D = round-half-up of x cos + y sin in
@@ -160,6 +181,14 @@ int ld_detect_batch(const uint8_t *gray, const ld_image *img, int32_t threshold,
                     int32_t k, ld_peak *peaks, int32_t *n_peaks, uint32_t *edge_count,
                     uint32_t *acc, void *workspace, size_t workspace_bytes,
                     void *stream);
+
+/* ld_detect_batch with border/clamp flags (see LD_FLAG_*); same workspace. */
+int ld_detect_batch_ex(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                       uint32_t flags, int32_t n_theta, const int32_t *cos_q15,
+                       const int32_t *sin_q15, int32_t half_theta, int32_t half_rho,
+                       uint32_t min_votes, int32_t k, ld_peak *peaks, int32_t *n_peaks,
+                       uint32_t *edge_count, uint32_t *acc, void *workspace,
+                       size_t workspace_bytes, void *stream);
 
 /* ld_detect_batch from HOST buffers: gray_host [batch][height][pitch] (pinned
  * host memory for overlap), peaks_host [batch][k], n_peaks_host [batch],

@@ -115,8 +115,8 @@ static int check_image(const uint8_t *gray, const ld_image *img) {
   return LD_OK;
 }
 
-static int64_t max_edges_per_frame(const ld_image *img) {
-  const int64_t w2 = img->width > 2 ? img->width - 2 : 0;
+static int64_t max_edges_per_frame(const ld_image *img, uint32_t flags = 0) {
+  const int64_t w2 = (flags & LD_FLAG_ZERO_PAD) ? img->width : (img->width > 2 ? img->width - 2 : 0);
   return static_cast<int64_t>(img->row_end - img->row_begin) * w2;
 }
 
@@ -148,7 +148,7 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // ---------------------------------------------------------------------------
 static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshold,
-                      uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
+                      uint32_t flags, uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
                       uint32_t *edge_count, cudaStream_t stream) {
   DevInfo dev;
   int rc = device_info(&dev);
@@ -190,7 +190,11 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
   p.n_tiles = static_cast<int32_t>(n_tiles);
   p.batch = img->batch;
   int t2 = threshold <= 0 ? 0 : static_cast<int>((static_cast<int64_t>(threshold) + 1) / 2);
+  // LD_FLAG_CLAMP_255: min(|G|, 255) >= T is |G| >= T for T <= 255
+  // and never true above it (t2 = 766 exceeds max |A|, |B| = 765)
+  if ((flags & LD_FLAG_CLAMP_255) && threshold > 255) t2 = 766;
   p.t2 = t2 > 766 ? 766 : t2;
+  p.zero_pad = (flags & LD_FLAG_ZERO_PAD) ? 1 : 0;
   p.binary = binary;
   p.bin_pitch = img->pitch;
   p.bin_frame_stride = static_cast<int64_t>(img->row_end - img->row_begin) * img->pitch;
@@ -284,7 +288,7 @@ struct DetectLayout {
 
 static DetectLayout detect_layout(const ld_image *img, int32_t n_theta, int32_t k, bool acc_ws) {
   DetectLayout L;
-  const int64_t me = max_edges_per_frame(img);
+  const int64_t me = max_edges_per_frame(img, LD_FLAG_ZERO_PAD);  // any flags
   L.edge_stride = static_cast<int64_t>(align_up(static_cast<size_t>(me > 0 ? me : 1), 4));
   const int32_t d = rho_offset(img->width, img->height);
   const size_t acc_bytes = static_cast<size_t>(img->batch) * n_theta * (2 * static_cast<size_t>(d) + 1) * 4;
@@ -337,20 +341,29 @@ int64_t ld_device_l2_bytes(void) {
   return d.l2;
 }
 
-int ld_sobel_binarize(const uint8_t *gray, const ld_image *img, int32_t threshold,
-                      uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
-                      uint32_t *edge_count, void *stream) {
+int ld_sobel_binarize_ex(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                         uint32_t flags, uint8_t *binary, uint32_t *edge_xy,
+                         int64_t edge_stride, uint32_t *edge_count, void *stream) {
   g_launches = 0;
   int rc = check_image(gray, img);
   if (rc) return rc;
+  if (flags & ~static_cast<uint32_t>(LD_FLAG_ZERO_PAD | LD_FLAG_CLAMP_255))
+    return fail(LD_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
   if (!edge_count) return fail(LD_ERR_INVALID_ARG, "edge_count is NULL");
-  if (edge_xy && edge_stride < max_edges_per_frame(img))
+  if (edge_xy && edge_stride < max_edges_per_frame(img, flags))
     return fail(LD_ERR_INVALID_ARG, "edge_stride %lld < %lld possible edges per frame",
                 static_cast<long long>(edge_stride),
-                static_cast<long long>(max_edges_per_frame(img)));
+                static_cast<long long>(max_edges_per_frame(img, flags)));
   if (binary && !aligned(binary, 16)) return fail(LD_ERR_INVALID_ARG, "binary must be 16-byte aligned");
-  return sobel_impl(gray, img, threshold, binary, edge_xy, edge_stride, edge_count,
+  return sobel_impl(gray, img, threshold, flags, binary, edge_xy, edge_stride, edge_count,
                     static_cast<cudaStream_t>(stream));
+}
+
+int ld_sobel_binarize(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                      uint8_t *binary, uint32_t *edge_xy, int64_t edge_stride,
+                      uint32_t *edge_count, void *stream) {
+  return ld_sobel_binarize_ex(gray, img, threshold, 0u, binary, edge_xy, edge_stride, edge_count,
+                              stream);
 }
 
 int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
@@ -400,14 +413,17 @@ size_t ld_detect_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k
   return detect_layout(&whole, n_theta, k, acc_in_workspace != 0).total;
 }
 
-int ld_detect_batch(const uint8_t *gray, const ld_image *img, int32_t threshold, int32_t n_theta,
-                    const int32_t *cos_q15, const int32_t *sin_q15, int32_t half_theta,
-                    int32_t half_rho, uint32_t min_votes, int32_t k, ld_peak *peaks,
-                    int32_t *n_peaks, uint32_t *edge_count, uint32_t *acc, void *workspace,
-                    size_t workspace_bytes, void *stream) {
+int ld_detect_batch_ex(const uint8_t *gray, const ld_image *img, int32_t threshold,
+                       uint32_t flags, int32_t n_theta, const int32_t *cos_q15,
+                       const int32_t *sin_q15, int32_t half_theta, int32_t half_rho,
+                       uint32_t min_votes, int32_t k, ld_peak *peaks, int32_t *n_peaks,
+                       uint32_t *edge_count, uint32_t *acc, void *workspace,
+                       size_t workspace_bytes, void *stream) {
   g_launches = 0;
   int rc = check_image(gray, img);
   if (rc) return rc;
+  if (flags & ~static_cast<uint32_t>(LD_FLAG_ZERO_PAD | LD_FLAG_CLAMP_255))
+    return fail(LD_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
   if (img->row_begin != 0 || img->row_end != img->height)
     return fail(LD_ERR_INVALID_ARG, "ld_detect_batch takes whole frames (rows [0, height))");
   const int32_t d = rho_offset(img->width, img->height);
@@ -426,7 +442,8 @@ int ld_detect_batch(const uint8_t *gray, const ld_image *img, int32_t threshold,
   uint32_t *A = acc ? acc : reinterpret_cast<uint32_t *>(ws + L.acc_off);
   void *pws = ws + L.peaks_off;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if ((rc = sobel_impl(gray, img, threshold, nullptr, edges, L.edge_stride, counts, s))) return rc;
+  if ((rc = sobel_impl(gray, img, threshold, flags, nullptr, edges, L.edge_stride, counts, s)))
+    return rc;
   if ((rc = hough_impl(edges, counts, L.edge_stride, img->batch, img->width, img->height, n_theta,
                        cos_q15, sin_q15, A, s)))
     return rc;
@@ -439,6 +456,16 @@ int ld_detect_batch(const uint8_t *gray, const ld_image *img, int32_t threshold,
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(edge_count)");
   }
   return LD_OK;
+}
+
+int ld_detect_batch(const uint8_t *gray, const ld_image *img, int32_t threshold, int32_t n_theta,
+                    const int32_t *cos_q15, const int32_t *sin_q15, int32_t half_theta,
+                    int32_t half_rho, uint32_t min_votes, int32_t k, ld_peak *peaks,
+                    int32_t *n_peaks, uint32_t *edge_count, uint32_t *acc, void *workspace,
+                    size_t workspace_bytes, void *stream) {
+  return ld_detect_batch_ex(gray, img, threshold, 0u, n_theta, cos_q15, sin_q15, half_theta,
+                            half_rho, min_votes, k, peaks, n_peaks, edge_count, acc, workspace,
+                            workspace_bytes, stream);
 }
 
 // ---------------------------------------------------------------------------

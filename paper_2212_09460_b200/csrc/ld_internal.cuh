@@ -36,6 +36,7 @@ struct SobelParams {
   int32_t tiles_x, tiles_y, tiles_per_frame, n_tiles;
   int32_t batch;
   int32_t t2;                  // ceil(T/2) clamped to [0, 766]
+  int32_t zero_pad;            // LD_FLAG_ZERO_PAD: filter the border on a zero-padded image
   uint8_t *binary;
   int64_t bin_pitch, bin_frame_stride;
   uint32_t *edges;

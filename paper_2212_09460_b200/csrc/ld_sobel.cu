@@ -10,7 +10,9 @@
 //    columns left, 16 right) is staged by a TMA 3-D box load into a 2-deep
 //    shared-memory ring completed on mbarriers, so HBM reads of later tiles
 //    overlap the arithmetic of the current one.  Out-of-image halo bytes are
-//    zero-filled by TMA and only ever feed border pixels, which are forced to 0.
+//    zero-filled by TMA: they feed only border pixels, which are forced to 0 --
+//    or, in the paper's zero-padded mode (LD_FLAG_ZERO_PAD), are exactly the
+//    padding those border pixels are filtered with.
 //  * Arithmetic: |Gx|+|Gy| = 2 max(|A|, |B|) with
 //      A = (p01+p02+p12) - (p10+p20+p21),  B = (p12+p21+p22) - (p00+p01+p10)
 //    (pRC = row R of y-1..y+1, column C of x-1..x+1), an exact identity
@@ -246,8 +248,11 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
   const int strip = tid / SB_CHUNKS;
   const uint32_t k0 = static_cast<uint32_t>(32768 - p.t2) * 0x00010001u;
   const uint32_t k2 = k0 + k0;
-  const int ylo_g = p.row_begin > 1 ? p.row_begin : 1;
-  const int yhi_g = p.height - 2 < p.row_end - 1 ? p.height - 2 : p.row_end - 1;
+  // output rows: interior rows 1 .. H-2 (forced-zero border, DESIGN R2) or,
+  // zero-padded (R23), every row; always restricted to the owned rows
+  const int bord = p.zero_pad ? 0 : 1;
+  const int ylo_g = p.row_begin > bord ? p.row_begin : bord;
+  const int yhi_g = p.height - 1 - bord < p.row_end - 1 ? p.height - 1 - bord : p.row_end - 1;
   uint32_t *wstage = stage_edges + warp * CAP;
 
   // rank of this lane in (chunk, strip) order within the warp, and the lane
@@ -288,9 +293,9 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
     const int xs = ti.z + chunk * 16;     // first column of this thread's chunk
     const int ybase = ti.y + strip * SR;  // output row of masks[0]
 
-    uint32_t colmask = 0xFFFFu;  // interior columns 1 <= x <= W-2
+    uint32_t colmask = 0xFFFFu;  // output columns bord <= x <= W-1-bord
     {
-      const int lo = 1 - xs, hi = p.width - 2 - xs;
+      const int lo = bord - xs, hi = p.width - 1 - bord - xs;
       if (lo > 0 || hi < 15) {
         colmask = (hi < 0 || lo > 15) ? 0u
                                       : ((0xFFFFu >> (15 - min(hi, 15))) & (0xFFFFu << max(lo, 0)));

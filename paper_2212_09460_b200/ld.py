@@ -50,9 +50,11 @@ class ld_peak(ctypes.Structure):
 
 PEAK_DTYPE = np.dtype([("theta_bin", "<i4"), ("rho_bin", "<i4"), ("votes", "<u4")])
 
-EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_hough_accumulate",
+LD_FLAG_ZERO_PAD, LD_FLAG_CLAMP_255 = 1, 2
+
+EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",
            "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_detect_workspace_bytes",
-           "ld_detect_batch", "ld_detect_host_workspace_bytes", "ld_detect_batch_host",
+           "ld_detect_batch", "ld_detect_batch_ex", "ld_detect_host_workspace_bytes", "ld_detect_batch_host",
            "ld_bench_smem_atomics", "ld_device_sm_count", "ld_device_l2_bytes",
            "ld_status_string", "ld_last_error_detail", "ld_last_launch_count"]
 
@@ -73,6 +75,7 @@ def lib():
         sig = {
             "ld_rho_offset": ([i32, i32], i32),
             "ld_sobel_binarize": ([P, IMG, i32, P, P, i64, P, P], ctypes.c_int),
+            "ld_sobel_binarize_ex": ([P, IMG, i32, u32, P, P, i64, P, P], ctypes.c_int),
             "ld_hough_accumulate": ([P, P, i64, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
             "ld_hough_peaks_workspace_bytes": ([i32, i32, i32, i32], sz),
             "ld_hough_peaks": ([P, i32, i32, i32, i32, i32, u32, i32, P, P, P, sz, P],
@@ -80,6 +83,8 @@ def lib():
             "ld_detect_workspace_bytes": ([IMG, i32, i32, i32], sz),
             "ld_detect_batch": ([P, IMG, i32, i32, P, P, i32, i32, u32, i32, P, P, P, P, P, sz, P],
                                 ctypes.c_int),
+            "ld_detect_batch_ex": ([P, IMG, i32, u32, i32, P, P, i32, i32, u32, i32, P, P, P, P, P,
+                                    sz, P], ctypes.c_int),
             "ld_detect_host_workspace_bytes": ([IMG, i32, i32, i32], sz),
             "ld_detect_batch_host": ([P, IMG, i32, i32, P, P, i32, i32, u32, i32, P, P, P, i32, P,
                                       sz, P], ctypes.c_int),
@@ -158,6 +163,13 @@ def ld_sobel_binarize(gray, img: ld_image, threshold, binary, edge_xy, edge_stri
                                    _stream(stream)))
 
 
+def ld_sobel_binarize_ex(gray, img: ld_image, threshold, flags, binary, edge_xy, edge_stride,
+                         edge_count, stream=None):
+    _check(lib().ld_sobel_binarize_ex(_addr(gray), ctypes.byref(img), int(threshold), int(flags),
+                                      _addr(binary), _addr(edge_xy), int(edge_stride),
+                                      _addr(edge_count), _stream(stream)))
+
+
 def ld_hough_accumulate(edge_xy, edge_count, edge_stride, batch, width, height, n_theta,
                         cos_q15, sin_q15, acc, stream=None):
     c, s = _host_i32(cos_q15), _host_i32(sin_q15)
@@ -192,6 +204,17 @@ def ld_detect_batch(gray, img: ld_image, threshold, n_theta, cos_q15, sin_q15, h
                                  int(min_votes), int(k), _addr(peaks), _addr(n_peaks),
                                  _addr(edge_count), _addr(acc), _addr(workspace),
                                  int(workspace_bytes), _stream(stream)))
+
+
+def ld_detect_batch_ex(gray, img: ld_image, threshold, flags, n_theta, cos_q15, sin_q15,
+                       half_theta, half_rho, min_votes, k, peaks, n_peaks, edge_count, acc,
+                       workspace, workspace_bytes, stream=None):
+    c, s = _host_i32(cos_q15), _host_i32(sin_q15)
+    _check(lib().ld_detect_batch_ex(_addr(gray), ctypes.byref(img), int(threshold), int(flags),
+                                    int(n_theta), _addr(c), _addr(s), int(half_theta),
+                                    int(half_rho), int(min_votes), int(k), _addr(peaks),
+                                    _addr(n_peaks), _addr(edge_count), _addr(acc),
+                                    _addr(workspace), int(workspace_bytes), _stream(stream)))
 
 
 def ld_detect_host_workspace_bytes(img: ld_image, n_theta, k, chunk_frames) -> int:
@@ -248,19 +271,21 @@ def pitched(gray):
     return out, pitch
 
 
-def sobel_binarize(gray, threshold: int, want_binary=True, want_edges=True, stream=None):
+def sobel_binarize(gray, threshold: int, want_binary=True, want_edges=True, stream=None,
+                   flags: int = 0):
     """gray: uint8 CUDA [B][H][W] (whole frames).  Returns (binary [B][H][W] or
-    None, edges [B][edge_stride] or None, counts [B], edge_stride)."""
+    None, edges [B][edge_stride] or None, counts [B], edge_stride).  flags:
+    LD_FLAG_ZERO_PAD / LD_FLAG_CLAMP_255 (ld_sobel_binarize_ex)."""
     import torch
     b, h, w = gray.shape
     g, pitch = pitched(gray)
     img = make_image(w, h, pitch, h * pitch, b)
     dev = gray.device
-    stride = _round_up(max(h * max(w - 2, 0), 1), 4)
+    stride = _round_up(max(h * (w if flags & LD_FLAG_ZERO_PAD else max(w - 2, 0)), 1), 4)
     binary = torch.empty((b, h, pitch), dtype=torch.uint8, device=dev) if want_binary else None
     edges = torch.empty((b, stride), dtype=torch.int32, device=dev) if want_edges else None
     counts = torch.empty((b,), dtype=torch.int32, device=dev)
-    ld_sobel_binarize(g, img, threshold, binary, edges, stride, counts, stream)
+    ld_sobel_binarize_ex(g, img, threshold, flags, binary, edges, stride, counts, stream)
     if binary is not None:
         binary = binary[:, :, :w]
     return binary, edges, counts, stride
@@ -293,8 +318,9 @@ class Detector:
     """Owns the device workspace for repeated ld_detect_batch calls on one shape."""
 
     def __init__(self, width, height, batch, n_theta, cos_q15, sin_q15, threshold, k,
-                 half_theta, half_rho, min_votes=1, export_acc=False, device=None):
+                 half_theta, half_rho, min_votes=1, export_acc=False, device=None, flags=0):
         import torch
+        self.flags = int(flags)
         self.device = torch.device("cuda") if device is None else device
         self.w, self.h, self.b = width, height, batch
         self.pitch = _round_up(width, 16)
@@ -314,9 +340,10 @@ class Detector:
 
     def __call__(self, gray, stream=None):
         """gray: uint8 CUDA [B][H][pitch] with pitch = round_up(W, 16)."""
-        ld_detect_batch(gray, self.img, self.threshold, self.n_theta, self.cos, self.sin,
-                        self.half_theta, self.half_rho, self.min_votes, self.k, self.peaks,
-                        self.n_peaks, self.counts, self.acc, self.ws, self.ws_bytes, stream)
+        ld_detect_batch_ex(gray, self.img, self.threshold, self.flags, self.n_theta, self.cos,
+                           self.sin, self.half_theta, self.half_rho, self.min_votes, self.k,
+                           self.peaks, self.n_peaks, self.counts, self.acc, self.ws,
+                           self.ws_bytes, stream)
         return self.peaks, self.n_peaks, self.counts, self.acc
 
 

@@ -432,3 +432,96 @@ def test_peaks_stream_theta_chunks_single_frame(ld, oracle):
         peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, k)
         want, wn = oracle.hough_peaks(acc[0], ht, hr, 1, k)
         assert int(npk[0]) == wn and peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(want)
+
+
+# ----------------------------------------------------------------------------
+# NEXT 4: paper-literal zero-padded border and SPEC 8-bit clamp (DESIGN R23, R24)
+# ----------------------------------------------------------------------------
+def gpu_sobel_ex(ld, frames, threshold, flags, pitch_pad=0):
+    b, h, w = frames.shape
+    pitch = ld._round_up(w, 16) + pitch_pad
+    buf = np.zeros((b, h, pitch), np.uint8)
+    buf[:, :, :w] = frames
+    g = cuda(buf)
+    img = ld.make_image(w, h, pitch, h * pitch, b)
+    stride = ld._round_up(max(h * w, 1), 4)
+    binary = torch.full((b, h, pitch), 7, dtype=torch.uint8, device="cuda")
+    edges = torch.full((b, stride), -1, dtype=torch.int32, device="cuda")
+    counts = torch.full((b,), -1, dtype=torch.int32, device="cuda")
+    ld.ld_sobel_binarize_ex(g, img, threshold, flags, binary, edges, stride, counts)
+    torch.cuda.synchronize()
+    cnt = counts.cpu().numpy()
+    el = edges.cpu().numpy().view(np.uint32)
+    return binary.cpu().numpy()[:, :, :w], [np.sort(el[i, :cnt[i]]) for i in range(b)], cnt
+
+
+@pytest.mark.parametrize("flags", [1, 2, 3])
+@pytest.mark.parametrize("w,h", [(1, 1), (2, 3), (5, 7), (16, 16), (17, 17), (223, 65),
+                                 (225, 66), (256, 300), (300, 1)])
+def test_sobel_flags_fuzz(ld, oracle, flags, w, h):
+    img = synth.random_image(w * 7 + h, w, h, "uniform")
+    for t in (-1, 0, 1, 200, 255, 256, 1530, 1531):
+        binary, lists, cnt = gpu_sobel_ex(ld, img[None], t, flags, pitch_pad=16 if w % 3 else 0)
+        want = oracle.sobel_binarize_ex(img, t, flags)
+        assert np.array_equal(binary[0], want), (w, h, t, flags)
+        assert np.array_equal(lists[0], np.sort(oracle.compact(want))), (w, h, t, flags)
+
+
+def test_sobel_zero_pad_bands_match_whole(ld, oracle):
+    # row bands (1-row halo) in zero-padded mode == the whole frame: halo rows
+    # inside the image are real rows, only rows -1 and H are padding
+    img = synth.random_image(91, 200, 150, "uniform")
+    want = oracle.sobel_binarize_ex(img, 300, oracle.ZERO_PAD)
+    pitch = 208
+    full = np.zeros((150, pitch), np.uint8)
+    full[:, :200] = img
+    rows, edges = [], []
+    for rb, re in [(0, 1), (1, 37), (37, 64), (64, 149), (149, 150)]:
+        r0, r1 = max(rb - 1, 0), min(re + 1, 150)
+        g = cuda(full[r0:r1].copy())
+        im = ld.make_image(200, 150, pitch, (r1 - r0) * pitch, 1, rb, re)
+        stride = ld._round_up((re - rb) * 200, 4)
+        b = torch.zeros((re - rb, pitch), dtype=torch.uint8, device="cuda")
+        e = torch.zeros((stride,), dtype=torch.int32, device="cuda")
+        c = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        ld.ld_sobel_binarize_ex(g, im, 300, ld.LD_FLAG_ZERO_PAD, b, e, stride, c)
+        torch.cuda.synchronize()
+        rows.append(b.cpu().numpy()[:, :200])
+        edges.append(e.cpu().numpy().view(np.uint32)[: int(c.item())])
+    assert np.array_equal(np.concatenate(rows), want)
+    assert np.array_equal(np.sort(np.concatenate(edges)), np.sort(oracle.compact(want)))
+
+
+def test_sobel_flags_reject_unknown_bits_and_short_stride(ld):
+    g = torch.zeros((4, 16), dtype=torch.uint8, device="cuda")
+    img = ld.make_image(10, 4, 16, 64, 1)
+    c = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    e = torch.zeros((64,), dtype=torch.int32, device="cuda")
+    with pytest.raises(ld.LdError):
+        ld.ld_sobel_binarize_ex(g, img, 10, 4, None, e, 64, c)
+    with pytest.raises(ld.LdError):  # zero-pad needs rows * width = 40 > 32
+        ld.ld_sobel_binarize_ex(g, img, 10, ld.LD_FLAG_ZERO_PAD, None, e, 32, c)
+    ld.ld_sobel_binarize_ex(g, img, 10, 0, None, e, 32, c)  # 4 * 8 = 32 is enough
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_detect_zero_pad_end_to_end(ld, oracle, name):
+    cfg = synth.CONFIGS[name]
+    c, s = synth.q15_table(cfg.n_theta)
+    frame = synth.gen_frame(name, 0)
+    h, w = frame.shape
+    det = ld.Detector(w, h, 1, cfg.n_theta, c, s, cfg.threshold, cfg.k, cfg.half_theta,
+                      cfg.half_rho, cfg.min_votes, export_acc=True, flags=ld.LD_FLAG_ZERO_PAD)
+    g = torch.zeros((1, h, det.pitch), dtype=torch.uint8, device="cuda")
+    g[:, :, :w] = cuda(frame[None])
+    peaks, npk, counts, acc = det(g)
+    torch.cuda.synchronize()
+    b = oracle.sobel_binarize_ex(frame, cfg.threshold, oracle.ZERO_PAD)
+    e = oracle.compact(b)
+    want_acc = oracle.hough_accumulate(e, w, h, c, s)
+    want_pk, want_n = oracle.hough_peaks(want_acc, cfg.half_theta, cfg.half_rho, cfg.min_votes,
+                                         cfg.k)
+    assert int(counts[0]) == len(e)
+    assert np.array_equal(acc[0].cpu().numpy().view(np.uint32), want_acc)
+    assert int(npk[0]) == want_n
+    assert peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(want_pk)
