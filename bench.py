@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: plumbing check of N ranks on fewer GPUs)")
     return ap.parse_args()
 
 
@@ -206,9 +208,15 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
     from paper_2212_09460_b200 import ld
 
-    torch.cuda.set_device(local)
+    # one process per GPU; with fewer GPUs than ranks (plumbing checks with the
+    # gloo backend only) ranks share devices round-robin
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     cfg = synth.CONFIGS[args.workload]
     if args.workload == "cfg5":
         return run_banded(args, rank, world, local)
@@ -500,8 +508,8 @@ def run_banded(args, rank, world, local):
         "dtype": "u8/int32", "data": "synthetic",
         "config": {"workload": "cfg5", "width": W, "height": H, "threshold": cfg.threshold,
                    "n_theta": cfg.n_theta, "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
-                   "parallelism": "row-band x%d + NCCL all_reduce(SUM) of %d B" %
-                                  (world, det.acc.numel() * 4),
+                   "parallelism": "row-band x%d + %s all_reduce(SUM) of %d B" %
+                                  (world, args.dist_backend.upper(), det.acc.numel() * 4),
                    "l2": "single image (16.8 MB) + acc (47.5 MB) fit in L2: latency measurement"},
         "gvotes_per_s": votes / (ms_per_step / 1e3) / 1e9,
         "edges_total": edges_total,
