@@ -164,6 +164,22 @@ int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t 
                    ld_peak *peaks, int32_t *n_peaks, void *workspace,
                    size_t workspace_bytes, void *stream);
 
+/* ld_hough_peaks over a theta slice of a larger accumulator (the theta-sharded
+ * multi-GPU path): acc holds rows g0 .. g0+n_theta-1 of the
+ * full accumulator (theta_offset = g0), including every existing row within
+ * half_theta of the candidate rows.  Only cells in rows [cand_row_begin,
+ * cand_row_end) (local indices) can be candidates; their windows read any row
+ * of acc (clipped to acc, i.e. to the full accumulator when the halo rows are
+ * present).  Keys and the reported theta_bin use the global row
+ * (local + theta_offset), so per-slice top-k lists merge into the global one
+ * exactly.  Requires (theta_offset + n_theta) * n_rho < 2^32 - 1.  An empty
+ * row range gives n_peaks = 0. */
+int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                      int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                      int32_t cand_row_begin, int32_t cand_row_end, int32_t theta_offset,
+                      ld_peak *peaks, int32_t *n_peaks, void *workspace,
+                      size_t workspace_bytes, void *stream);
+
 /* Steps 1-4 for a batch of whole frames (img->row_begin = 0, row_end = height):
  * ld_sobel_binarize (no binary map) -> ld_hough_accumulate -> ld_hough_peaks,
  * stream-ordered, no host synchronisation.

@@ -245,7 +245,8 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
 static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
                       int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
                       ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t ws_bytes,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, int32_t cand_t0 = 0, int32_t cand_t1 = -1,
+                      int32_t theta_offset = 0) {
   PeaksParams p;
   p.acc = acc;
   p.batch = batch;
@@ -256,6 +257,9 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   p.floor_votes = min_votes > 1 ? min_votes : 1u;
   p.k = k;
   p.n_units = 0;
+  p.cand_t0 = cand_t0;
+  p.cand_t1 = cand_t1 < 0 ? n_theta : cand_t1;
+  p.theta_offset = theta_offset;
   // workspace: [batch] uint32 per-frame thresholds (256-B padded), then the keys
   p.gtau = static_cast<uint32_t *>(workspace);
   p.band_keys = reinterpret_cast<unsigned long long *>(
@@ -387,13 +391,21 @@ size_t ld_hough_peaks_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_
   return peaks_workspace_bytes(batch, n_theta, n_rho, k);
 }
 
-int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
-                   int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
-                   ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t workspace_bytes,
-                   void *stream) {
+int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                      int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                      int32_t cand_row_begin, int32_t cand_row_end, int32_t theta_offset,
+                      ld_peak *peaks, int32_t *n_peaks, void *workspace,
+                      size_t workspace_bytes, void *stream) {
   g_launches = 0;
   int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
   if (rc) return rc;
+  if (cand_row_begin < 0 || cand_row_end < cand_row_begin || cand_row_end > n_theta)
+    return fail(LD_ERR_INVALID_ARG, "candidate rows [%d, %d) outside [0, %d]", cand_row_begin,
+                cand_row_end, n_theta);
+  if (theta_offset < 0 ||
+      (static_cast<int64_t>(theta_offset) + n_theta) * n_rho >= (1ll << 32) - 1)
+    return fail(LD_ERR_INVALID_ARG, "theta_offset %d: global cell index exceeds 32 bits",
+                theta_offset);
   DevInfo dev;
   if ((rc = device_info(&dev))) return rc;
   if (!workspace || !aligned(workspace, 16) ||
@@ -401,7 +413,16 @@ int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t 
     return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 16-byte aligned",
                 peaks_workspace_bytes(batch, n_theta, n_rho, k));
   return peaks_impl(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
-                    n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+                    n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
+                    cand_row_begin, cand_row_end, theta_offset);
+}
+
+int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                   int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                   ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t workspace_bytes,
+                   void *stream) {
+  return ld_hough_peaks_ex(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, 0,
+                           n_theta, 0, peaks, n_peaks, workspace, workspace_bytes, stream);
 }
 
 size_t ld_detect_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k,

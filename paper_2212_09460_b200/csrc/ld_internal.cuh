@@ -97,6 +97,8 @@ struct PeaksParams {
   int32_t st_nt, st_sw, st_strips, st_tb, st_chunks, st_buf;  // streaming kernel geometry
   unsigned long long *band_keys;  // [batch][n_units][k]
   uint32_t *gtau;                 // [batch] per-frame running k-th candidate value (stream kernel)
+  int32_t cand_t0, cand_t1;       // candidate rows [cand_t0, cand_t1) (windows read every row)
+  int32_t theta_offset;           // added to the row index in keys and reported theta bins
   ld_peak *peaks;
   int32_t *n_peaks;
 };

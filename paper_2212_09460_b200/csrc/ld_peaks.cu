@@ -105,8 +105,8 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
   __shared__ int s_nbuf, s_ntop;
 
   const int band = blockIdx.x, f = blockIdx.y;
-  const int t0 = band * PK_ROWS;
-  const int nr = min(PK_ROWS, p.n_theta - t0);
+  const int t0 = p.cand_t0 + band * PK_ROWS;
+  const int nr = min(PK_ROWS, p.cand_t1 - t0);
   const int ncell = nr * p.n_rho;
   const uint32_t *A = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
 
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
         const int r = c - (t - t0) * p.n_rho;
         const uint32_t v = __ldg(A + static_cast<int64_t>(t) * p.n_rho + r);
         if (v >= p.floor_votes) {
-          const u64 key = mk_key(v, static_cast<uint32_t>(t * p.n_rho + r));
+          const u64 key = mk_key(v, static_cast<uint32_t>((t + p.theta_offset) * p.n_rho + r));
           if (key > kth &&
               is_window_max(A, p.n_theta, p.n_rho, t, r, v, p.half_theta, p.half_rho)) {
             const int slot = atomicAdd(&s_nbuf, 1);
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
   const int strip = unit / p.st_chunks, chunk = unit - strip * p.st_chunks;
   const int hr = p.half_rho, n_rho = p.n_rho, n_theta = p.n_theta;
   const int cbase = strip * p.st_sw - hr;  // global column of loaded column 0
-  const int tb0 = chunk * p.st_tb;
-  const int tb1 = min(tb0 + p.st_tb, n_theta);
+  const int tb0 = p.cand_t0 + chunk * p.st_tb;
+  const int tb1 = min(tb0 + p.st_tb, p.cand_t1);
   const int tid = threadIdx.x;
 
   const int j0 = tid * CPT;  // loaded columns j0 .. j0+CPT-1
@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
         if (!__any_sync(0xffffffffu, bad) && lane == 0) {
           const int slot = atomicAdd(&s_nbuf, 1);
           if (LD_CHK(slot < p.st_buf))
-            buf[slot] = mk_key(v, static_cast<uint32_t>((g0 + i) * n_rho + cbase + j));
+            buf[slot] = mk_key(v, static_cast<uint32_t>((g0 + i + p.theta_offset) * n_rho + cbase + j));
         }
       }
     }
@@ -753,8 +753,8 @@ __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksPar
   const int strip = unit / p.st_chunks, chunk = unit - strip * p.st_chunks;
   const int hr = p.half_rho, n_rho = p.n_rho, n_theta = p.n_theta;
   const int cbase = strip * p.st_sw - hr;  // global column of loaded column 0
-  const int tb0 = chunk * p.st_tb;
-  const int tb1 = min(tb0 + p.st_tb, n_theta);
+  const int tb0 = p.cand_t0 + chunk * p.st_tb;
+  const int tb1 = min(tb0 + p.st_tb, p.cand_t1);
   // lane l owns loaded columns l + 32 q (q < PW_CPT): every load instruction
   // of the warp reads 32 consecutive words (fully coalesced)
   const bool all_in = cbase >= 0 && cbase + PW_COLS <= n_rho;  // warp-uniform
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksPar
       }
       if (!__any_sync(0xffffffffu, bad)) {
         if (lane == 0 && LD_CHK(ncand < PW_CBUF))
-          S.cbuf[ncand] = mk_key(v, static_cast<uint32_t>((g0 + i) * n_rho + cbase + j));
+          S.cbuf[ncand] = mk_key(v, static_cast<uint32_t>((g0 + i + p.theta_offset) * n_rho + cbase + j));
         ++ncand;
       }
     }
@@ -1052,8 +1052,18 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int cpt = 0;
+  // candidate rows [cand_t0, cand_t1): the planners chunk those rows only;
+  // the tiled kernel has no row restriction and is skipped when one is set
+  const int n_cand = p.cand_t1 - p.cand_t0;
+  const bool restricted = p.cand_t0 != 0 || p.cand_t1 != p.n_theta || p.theta_offset != 0;
+  if (n_cand <= 0) {  // no candidate rows: the merge writes sentinels and 0 peaks
+    p.n_units = 0;
+    peaks_merge_kernel<<<p.batch, PK_THREADS, 0, stream>>>(p);
+    note_launch();
+    return cudaGetLastError();
+  }
   if (!force_band && !force_tile &&
-      peaks_warp_plan(p.batch, p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem)) {
+      peaks_warp_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem)) {
     cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
     if (em != cudaSuccess) return em;
     WarpKernel kern = warp_kernel(p.half_theta);
@@ -1066,7 +1076,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
     dim3 g1((p.n_units + PW_W - 1) / PW_W, p.batch);
     kern<<<g1, 32 * PW_W, smem, stream>>>(p);
   } else if (!force_band && !force_tile &&
-      peaks_stream_plan(p.batch, p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
+      peaks_stream_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
                         &smem)) {
     cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
     if (em != cudaSuccess) return em;
@@ -1080,7 +1090,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
     }
     dim3 g1(p.n_units, p.batch);
     kern<<<g1, p.st_nt, smem, stream>>>(p);
-  } else if (!force_band &&
+  } else if (!force_band && !restricted &&
              peaks_tile_plan(p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, &p, &smem)) {
     TileKernel kern = tile_kernel(p.half_theta);
     if (!g_tile_attr[dev & 63][p.half_theta]) {
@@ -1092,7 +1102,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
     dim3 g1(p.n_units, p.batch);
     kern<<<g1, p.tch, smem, stream>>>(p);
   } else {
-    p.n_units = (p.n_theta + PK_ROWS - 1) / PK_ROWS;
+    p.n_units = (n_cand + PK_ROWS - 1) / PK_ROWS;
     dim3 g1(p.n_units, p.batch);
     peaks_band_kernel<<<g1, PK_THREADS, 0, stream>>>(p);
   }

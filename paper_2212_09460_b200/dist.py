@@ -154,3 +154,161 @@ class BandedDetector:
                           stream)
         self.launches += ld.ld_last_launch_count()
         return self.peaks, self.n_peaks, self.acc, self.count
+
+
+# ----------------------------------------------------------------------------
+# theta-sharded banded detection
+# ----------------------------------------------------------------------------
+def theta_shard(n_theta: int, rank: int, world: int) -> tuple[int, int]:
+    """Theta rows [t0, t1) whose candidates ``rank`` owns (balanced, in order)."""
+    return row_band(n_theta, rank, world)
+
+
+def theta_slice(n_theta: int, half_theta: int, t0: int, t1: int) -> tuple[int, int]:
+    """Rows [g0, g1) a shard must vote: its own rows plus every existing row
+    within half_theta of them (the peak windows, DESIGN R13)."""
+    return max(t0 - half_theta, 0), min(t1 + half_theta, n_theta)
+
+
+def merge_peak_lists(peaks, n_peaks, n_rho: int, k: int):
+    """Merge per-shard top-k lists (global theta bins) into the global top-k.
+
+    peaks: int32 [S][k][3] (theta_bin, rho_bin, votes as uint32 bits), n_peaks
+    int32 [S].  Keys are (votes, -theta, -rho) (DESIGN R14) as one int64
+    votes * 2^32 + (2^32 - 1 - (theta * n_rho + rho)); runs on the tensors'
+    device (no host synchronisation).  Returns (peaks [k][3], n_peaks [1])."""
+    import torch
+    s, kk, _ = peaks.shape
+    p = peaks.reshape(s * kk, 3).to(torch.int64)
+    valid = (torch.arange(kk, device=peaks.device)[None, :] < n_peaks[:, None].to(torch.int64))
+    valid = valid.reshape(-1)
+    votes = p[:, 2] & 0xFFFFFFFF
+    idx = p[:, 0] * n_rho + p[:, 1]
+    key = votes * (1 << 32) + (0xFFFFFFFF - idx)
+    key = torch.where(valid, key, torch.full_like(key, -1))
+    top = torch.topk(key, min(k, key.numel())).values
+    ok = top >= 0
+    idx_out = 0xFFFFFFFF - (top & 0xFFFFFFFF)
+    out = torch.full((k, 3), -1, dtype=torch.int64, device=peaks.device)
+    out[:, 2] = 0
+    n = top.numel()
+    out[:n, 0] = torch.where(ok, idx_out // n_rho, torch.full_like(top, -1))
+    out[:n, 1] = torch.where(ok, idx_out % n_rho, torch.full_like(top, -1))
+    out[:n, 2] = torch.where(ok, top >> 32, torch.zeros_like(top))
+    cnt = ok.sum().to(torch.int32).reshape(1)
+    return out.to(torch.int32), cnt
+
+
+class ThetaShardedDetector:
+    """Theta-sharded detection of one large image (cfg5, NEXT 1).
+
+    Sobel + binarize + compaction run on this rank's row band (as in
+    BandedDetector); the band edge lists are all-gathered (4 B per edge), every
+    rank votes ALL edges into only its theta shard plus half_theta halo rows
+    (ld_hough_accumulate on a slice of the trig table), finds the candidates of
+    its own rows (ld_hough_peaks_ex with global theta bins), and the per-rank
+    top-k lists are all-gathered (12 B x k per rank) and merged.  Compared with
+    the row-band all_reduce of the 4 n_theta n_rho-byte accumulator this
+    exchanges ~4 E bytes, and voting and peaks both scale with the rank count.
+    Results are bit-identical to the single-GPU path and the oracle.
+    """
+
+    def __init__(self, width, height, n_theta, cos_q15, sin_q15, threshold, k, half_theta,
+                 half_rho, min_votes=1, rank=0, world=1, group=None, device=None):
+        import torch
+        from . import ld
+        self.ld = ld
+        self.band = BandedDetector(width, height, n_theta, cos_q15, sin_q15, threshold, k,
+                                   half_theta, half_rho, min_votes, rank, world, group, device)
+        self.device = self.band.device
+        self.group, self.rank, self.world = group, rank, world
+        self.w, self.h, self.n_theta, self.k = width, height, n_theta, k
+        self.half_theta, self.half_rho, self.min_votes = half_theta, half_rho, min_votes
+        self.n_rho = self.band.n_rho
+        self.t0, self.t1 = theta_shard(n_theta, rank, world)
+        self.g0, self.g1 = theta_slice(n_theta, half_theta, self.t0, self.t1)
+        c = ld._host_i32(cos_q15)
+        s = ld._host_i32(sin_q15)
+        self.cos_s, self.sin_s = c[self.g0:self.g1].copy(), s[self.g0:self.g1].copy()
+        # gathered edge lists: every rank's band holds at most rows * (W - 2) edges
+        self.max_band_edges = max(BandPlan.make(width, height, r, world).max_edges
+                                  for r in range(world))
+        self.gathered = torch.empty((world, max(self.max_band_edges, 1)), dtype=torch.int32,
+                                    device=self.device)
+        self.send = torch.zeros((max(self.max_band_edges, 1),), dtype=torch.int32,
+                                device=self.device)
+        self.all_stride = ld._round_up(max(world * self.max_band_edges, 1), 4)
+        self.all_edges = torch.zeros((self.all_stride,), dtype=torch.int32, device=self.device)
+        self.total = torch.zeros((1,), dtype=torch.int32, device=self.device)
+        ns = max(self.g1 - self.g0, 1)
+        self.acc = torch.empty((1, ns, self.n_rho), dtype=torch.int32, device=self.device)
+        self.ws_bytes = ld.ld_hough_peaks_workspace_bytes(1, ns, self.n_rho, k)
+        self.ws = torch.empty((max(self.ws_bytes, 16),), dtype=torch.uint8, device=self.device)
+        self.peaks = torch.empty((1, k, 3), dtype=torch.int32, device=self.device)
+        self.n_peaks = torch.empty((1,), dtype=torch.int32, device=self.device)
+        self.launches = 0
+
+    def load(self, gray_full):
+        self.band.load(gray_full)
+
+    def __call__(self):
+        """Returns (peaks [1][k][3], n_peaks [1]) on every rank."""
+        import torch
+        import torch.distributed as dist
+        ld, b = self.ld, self.band
+        self.launches = 0
+        if b.plan.rows > 0:
+            ld.ld_sobel_binarize(b.gray, b.img, b.threshold, None, b.edges, b.edge_stride,
+                                 b.count, None)
+            self.launches += ld.ld_last_launch_count()
+        else:
+            b.count.zero_()
+        multi = dist.is_initialized() and self.world > 1
+        if multi:
+            counts = torch.empty((self.world,), dtype=torch.int32, device=self.device)
+            dist.all_gather_into_tensor(counts, b.count, group=self.group)
+            cl = counts.tolist()  # host sizes for the variable-length gather
+            m = max(max(cl), 1)
+            mine = cl[self.rank]
+            if mine:
+                self.send[:mine].copy_(b.edges[:mine])
+            dist.all_gather_into_tensor(self._gbuf(m), self.send[:m], group=self.group)
+            parts = [self._gview(m)[r, :cl[r]] for r in range(self.world)]
+            n = sum(cl)
+            if n:
+                torch.cat(parts, out=self.all_edges[:n])
+            self.total.fill_(n)
+            edges, count, stride = self.all_edges, self.total, self.all_stride
+        else:
+            edges, count, stride = b.edges, b.count, b.edge_stride
+        self.vote_and_peaks(edges, count, stride)
+        if not multi:
+            return self.peaks, self.n_peaks
+        allp = torch.empty((self.world, self.k, 3), dtype=torch.int32, device=self.device)
+        alln = torch.empty((self.world,), dtype=torch.int32, device=self.device)
+        dist.all_gather_into_tensor(allp, self.peaks, group=self.group)
+        dist.all_gather_into_tensor(alln, self.n_peaks, group=self.group)
+        p, n = merge_peak_lists(allp, alln, self.n_rho, self.k)
+        return p[None], n
+
+    def vote_and_peaks(self, edges, count, stride):
+        """This rank's theta shard: vote every edge of the image (device list
+        `edges`, device `count`) into rows g0 .. g1-1, then the top-k of the
+        shard's own rows with global theta bins -> self.peaks, self.n_peaks."""
+        ld = self.ld
+        if self.g1 > self.g0:
+            ld.ld_hough_accumulate(edges, count, stride, 1, self.w, self.h, self.g1 - self.g0,
+                                   self.cos_s, self.sin_s, self.acc, None)
+            self.launches += ld.ld_last_launch_count()
+        ld.ld_hough_peaks_ex(self.acc, 1, max(self.g1 - self.g0, 1), self.n_rho, self.half_theta,
+                             self.half_rho, self.min_votes, self.k, self.t0 - self.g0,
+                             self.t1 - self.g0, self.g0, self.peaks, self.n_peaks, self.ws,
+                             self.ws_bytes, None)
+        self.launches += ld.ld_last_launch_count()
+
+    def _gbuf(self, m):
+        self._gflat = self.gathered.reshape(-1)[: self.world * m]
+        return self._gflat
+
+    def _gview(self, m):
+        return self._gflat.reshape(self.world, m)

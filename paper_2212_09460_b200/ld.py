@@ -53,7 +53,8 @@ PEAK_DTYPE = np.dtype([("theta_bin", "<i4"), ("rho_bin", "<i4"), ("votes", "<u4"
 LD_FLAG_ZERO_PAD, LD_FLAG_CLAMP_255 = 1, 2
 
 EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",
-           "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_detect_workspace_bytes",
+           "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_hough_peaks_ex",
+           "ld_detect_workspace_bytes",
            "ld_detect_batch", "ld_detect_batch_ex", "ld_detect_host_workspace_bytes", "ld_detect_batch_host",
            "ld_bench_smem_atomics", "ld_device_sm_count", "ld_device_l2_bytes",
            "ld_status_string", "ld_last_error_detail", "ld_last_launch_count"]
@@ -80,6 +81,8 @@ def lib():
             "ld_hough_peaks_workspace_bytes": ([i32, i32, i32, i32], sz),
             "ld_hough_peaks": ([P, i32, i32, i32, i32, i32, u32, i32, P, P, P, sz, P],
                                ctypes.c_int),
+            "ld_hough_peaks_ex": ([P, i32, i32, i32, i32, i32, u32, i32, i32, i32, i32, P, P, P,
+                                   sz, P], ctypes.c_int),
             "ld_detect_workspace_bytes": ([IMG, i32, i32, i32], sz),
             "ld_detect_batch": ([P, IMG, i32, i32, P, P, i32, i32, u32, i32, P, P, P, P, P, sz, P],
                                 ctypes.c_int),
@@ -188,6 +191,16 @@ def ld_hough_peaks(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, 
                                 int(half_theta), int(half_rho), int(min_votes), int(k),
                                 _addr(peaks), _addr(n_peaks), _addr(workspace),
                                 int(workspace_bytes), _stream(stream)))
+
+
+def ld_hough_peaks_ex(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k,
+                      cand_row_begin, cand_row_end, theta_offset, peaks, n_peaks, workspace,
+                      workspace_bytes, stream=None):
+    _check(lib().ld_hough_peaks_ex(_addr(acc), int(batch), int(n_theta), int(n_rho),
+                                   int(half_theta), int(half_rho), int(min_votes), int(k),
+                                   int(cand_row_begin), int(cand_row_end), int(theta_offset),
+                                   _addr(peaks), _addr(n_peaks), _addr(workspace),
+                                   int(workspace_bytes), _stream(stream)))
 
 
 def ld_detect_workspace_bytes(img: ld_image, n_theta, k, acc_in_workspace) -> int:
@@ -302,15 +315,24 @@ def hough_accumulate(edges, counts, edge_stride, width, height, cos_q15, sin_q15
     return acc
 
 
-def hough_peaks(acc, half_theta, half_rho, min_votes, k, stream=None):
+def hough_peaks(acc, half_theta, half_rho, min_votes, k, stream=None, cand_rows=None,
+                theta_offset=0):
+    """acc: int32 CUDA [B][n_theta][n_rho] (uint32 bits).  cand_rows=(begin, end)
+    and theta_offset select ld_hough_peaks_ex (a theta slice of a larger
+    accumulator)."""
     import torch
     b, n_theta, n_rho = acc.shape
     ws_bytes = ld_hough_peaks_workspace_bytes(b, n_theta, n_rho, k)
     ws = torch.empty((max(ws_bytes, 16),), dtype=torch.uint8, device=acc.device)
     peaks = torch.empty((b, k, 3), dtype=torch.int32, device=acc.device)
     n_peaks = torch.empty((b,), dtype=torch.int32, device=acc.device)
-    ld_hough_peaks(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks, n_peaks,
-                   ws, ws_bytes, stream)
+    if cand_rows is None and theta_offset == 0:
+        ld_hough_peaks(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
+                       n_peaks, ws, ws_bytes, stream)
+    else:
+        c0, c1 = cand_rows if cand_rows is not None else (0, n_theta)
+        ld_hough_peaks_ex(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, c0, c1,
+                          theta_offset, peaks, n_peaks, ws, ws_bytes, stream)
     return peaks, n_peaks
 
 

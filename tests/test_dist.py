@@ -114,3 +114,72 @@ def test_band_accumulators_sum_to_whole_without_collective(oracle):
         tot = sum(band_accumulator(oracle, img, pdist.BandPlan.make(40, 6, r, world), c, s)
                   .astype(np.int64) for r in range(world))
         assert np.array_equal(tot, want.astype(np.int64)), world
+
+
+# ----------------------------------------------------------------------------
+# theta-sharded detection (NEXT 1): partition, halo slices and the device-side
+# merge of per-shard top-k lists, through a real gloo process group
+# ----------------------------------------------------------------------------
+def test_theta_slices_cover_with_halo():
+    for nt, ht in [(180, 2), (1024, 10), (7, 3), (3, 0)]:
+        for world in (1, 2, 3, 8):
+            owned = []
+            for r in range(world):
+                t0, t1 = pdist.theta_shard(nt, r, world)
+                g0, g1 = pdist.theta_slice(nt, ht, t0, t1)
+                owned.extend(range(t0, t1))
+                assert g0 == max(t0 - ht, 0) and g1 == min(t1 + ht, nt)
+            assert owned == list(range(nt))
+
+
+def _shard_peaks(oracle, big, t0, t1, ht, hr, k):
+    g0, g1 = pdist.theta_slice(big.shape[0], ht, t0, t1)
+    sl = np.ascontiguousarray(big[g0:g1])
+    pk, _ = oracle.hough_peaks(sl, ht, hr, 1, sl.size)  # every candidate of the slice
+    own = [(int(p["theta_bin"]) + g0, int(p["rho_bin"]), int(p["votes"])) for p in pk
+           if t0 - g0 <= int(p["theta_bin"]) < t1 - g0][:k]
+    out = np.full((k, 3), -1, np.int32)
+    out[:, 2] = 0
+    for i, t in enumerate(own):
+        out[i] = t
+    return out, len(own)
+
+
+def _theta_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img = synth.random_image(17, 90, 70, "uniform")
+        c, s = synth.q15_table(60)
+        e = oracle.compact(oracle.sobel_binarize(img, 300))
+        big = oracle.hough_accumulate(e, 90, 70, c, s)
+        t0, t1 = pdist.theta_shard(60, rank, world)
+        p, n = _shard_peaks(oracle, big, t0, t1, 2, 5, 6)
+        allp = [torch.zeros((6, 3), dtype=torch.int32) for _ in range(world)]
+        alln = [torch.zeros((1,), dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(allp, torch.from_numpy(p))
+        dist.all_gather(alln, torch.tensor([n], dtype=torch.int32))
+        mp, mn = pdist.merge_peak_lists(torch.stack(allp), torch.cat(alln), big.shape[1], 6)
+        np.save(os.path.join(outdir, "tp%d.npy" % rank), mp.numpy())
+        np.save(os.path.join(outdir, "tn%d.npy" % rank), mn.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_theta_sharded_merge_gloo_equals_whole_oracle(oracle, tmp_path, world):
+    import torch.multiprocessing as mp
+    mp.spawn(_theta_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    img = synth.random_image(17, 90, 70, "uniform")
+    c, s = synth.q15_table(60)
+    big = oracle.hough_accumulate(oracle.compact(oracle.sobel_binarize(img, 300)), 90, 70, c, s)
+    want, wn = oracle.hough_peaks(big, 2, 5, 1, 6)
+    want = np.array([(p["theta_bin"], p["rho_bin"], p["votes"]) for p in want], np.int64)
+    for r in range(world):
+        got = np.load(tmp_path / ("tp%d.npy" % r)).astype(np.int64)
+        assert int(np.load(tmp_path / ("tn%d.npy" % r))[0]) == wn
+        assert np.array_equal(got[:wn], want[:wn]) and (got[wn:, 0] == -1).all(), r

@@ -525,3 +525,68 @@ def test_detect_zero_pad_end_to_end(ld, oracle, name):
     assert np.array_equal(acc[0].cpu().numpy().view(np.uint32), want_acc)
     assert int(npk[0]) == want_n
     assert peak_tuples(peaks[0].cpu()) == oracle_peak_tuples(want_pk)
+
+
+# ----------------------------------------------------------------------------
+# NEXT 1: theta slices of an accumulator (ld_hough_peaks_ex) and theta-sharded
+# detection (dist.ThetaShardedDetector)
+# ----------------------------------------------------------------------------
+def oracle_all_candidates(oracle, big, ht, hr, mv):
+    allp, n = oracle.hough_peaks(big, ht, hr, mv, big.size)
+    return [(int(p["theta_bin"]), int(p["rho_bin"]), int(p["votes"])) for p in allp[:n]]
+
+
+def oracle_slice_peaks(cands, t0, t1, k):
+    # the definition restricted to candidate rows [t0, t1) of the full accumulator
+    return [c for c in cands if t0 <= c[0] < t1][:k]
+
+
+@pytest.mark.parametrize("kernel", ["auto", "stream", "band"])
+def test_peaks_ex_theta_slices(ld, oracle, kernel, monkeypatch):
+    if kernel != "auto":
+        monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
+    rng = np.random.default_rng(123)
+    for trial, (nt, ht, hr, k) in enumerate([(180, 2, 29, 4), (1024, 10, 116, 64),
+                                              (97, 3, 5, 16), (60, 0, 0, 8), (33, 7, 44, 8)]):
+        big = rng.integers(0, 12 if trial % 2 else 5000, size=(nt, 1201)).astype(np.uint32)
+        cands = oracle_all_candidates(oracle, big, ht, hr, 1)
+        for (t0, t1) in [(0, nt), (0, nt // 3), (nt // 3, 2 * nt // 3), (2 * nt // 3, nt),
+                         (nt // 2, nt // 2), (nt - 1, nt)]:
+            g0, g1 = max(t0 - ht, 0), min(t1 + ht, nt)
+            # an empty shard with no halo still passes a 1-row accumulator
+            # (the ABI requires n_theta >= 1); its candidate range is empty
+            sl = np.ascontiguousarray(big[g0:max(g1, g0 + 1)])[None]
+            peaks, npk = ld.hough_peaks(cuda(sl.view(np.int32)), ht, hr, 1, k,
+                                        cand_rows=(t0 - g0, t1 - g0), theta_offset=g0)
+            torch.cuda.synchronize()
+            want = oracle_slice_peaks(cands, t0, t1, k)
+            assert int(npk[0]) == len(want), (kernel, trial, t0, t1)
+            got = peak_tuples(peaks[0].cpu())[:len(want)]
+            assert got == want, (kernel, trial, t0, t1)
+
+
+def test_theta_sharded_detector_emulated(ld, oracle):
+    # every rank of world N in one process: the whole-image edge list stands in
+    # for the all-gathered band lists; per-rank top-k lists merged on device
+    from paper_2212_09460_b200 import dist as pdist
+    cfg = synth.CONFIGS["cfg5"]
+    c, s = synth.q15_table(cfg.n_theta)
+    img = synth.gen_frame("cfg5", 0)
+    W = H = 4096
+    r = oracle.detect(img, cfg.threshold, c, s, cfg.half_theta, cfg.half_rho, cfg.min_votes,
+                      cfg.k, want_binary=False, want_acc=False)
+    _, edges, counts, stride = ld.sobel_binarize(cuda(img[None]), cfg.threshold, want_binary=False)
+    assert int(counts[0]) == r["n_edges"]
+    for world in (1, 2, 3, 8):
+        allp, alln = [], []
+        for rank in range(world):
+            det = pdist.ThetaShardedDetector(W, H, cfg.n_theta, c, s, cfg.threshold, cfg.k,
+                                             cfg.half_theta, cfg.half_rho, cfg.min_votes,
+                                             rank, world)
+            det.vote_and_peaks(edges[0], counts, stride)
+            allp.append(det.peaks[0].clone())
+            alln.append(det.n_peaks.clone())
+        p, n = pdist.merge_peak_lists(torch.stack(allp), torch.cat(alln), det.n_rho, cfg.k)
+        torch.cuda.synchronize()
+        assert int(n[0]) == r["n_peaks"], world
+        assert peak_tuples(p.cpu()) == oracle_peak_tuples(r["peaks"]), world
