@@ -45,6 +45,14 @@ __device__ __forceinline__ u64 mk_key(uint32_t v, uint32_t idx) {
   return (static_cast<u64>(v) << 32) | static_cast<u64>(0xFFFFFFFFu - idx);
 }
 
+// Per-frame threshold read: gpu-scope relaxed (a plain volatile load would be
+// a system-scope strong load, a far longer round trip)
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Sort a[0..n) descending (n a power of two); all threads participate.
 __device__ void bitonic_desc(u64 *a, int n) {
   for (int k = 2; k <= n; k <<= 1) {
@@ -488,7 +496,7 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
     // thread 0 prefetches the per-frame threshold now; it is used after the
     // group, so the global round trip overlaps the group's work
     uint32_t gt = 0;
-    if (tid == 0) gt = *reinterpret_cast<volatile uint32_t *>(p.gtau + f);
+    if (tid == 0) gt = ld_relaxed_u32(p.gtau + f);
     uint32_t tq[CPT];  // per column: tau if owned, else "never"
     const uint32_t tau = s_tau;
 #pragma unroll
@@ -724,23 +732,134 @@ static bool peaks_stream_plan(int batch, int n_theta, int n_rho, int half_theta,
 // Warp-strip kernel (narrow windows: half_theta <= 3, 4 <= half_rho <= 64,
 // k <= 64).  Every WARP is an independent unit: one strip of 256 loaded
 // columns (owned: 256 - 2 half_rho) x one chunk of theta rows of one frame,
-// 8 consecutive columns per lane.  Nothing is shared between warps, so there
-// is no CTA barrier at all: the latency of one warp's loads is hidden by the
-// other warps instead of stalling a whole CTA at every row group.  The halo
-// columns are read twice (by neighbouring warps), mostly from L2.  Same tests
-// as the streaming kernel: column maxima in registers, in-lane / neighbour-
-// lane prefilter, per-warp and per-frame running k-th best threshold tau,
-// warp-cooperative exact test of the few survivors.
+// 8 lane-strided columns per lane (each load instruction reads 32 consecutive
+// words).  Nothing is shared between warps, so there is no CTA barrier: the
+// latency of one warp's loads is hidden by the other warps.  (Measured on
+// B200, tools/stream_probe.cu: this pattern streams at ~5.8 TB/s; per-warp
+// cp.async.bulk row copies into a shared ring only reach ~2.6 TB/s.)
+//
+// Rows stream through a register ring of R = 2 PW_G + 2 HT rows; the row loop
+// is unrolled over one ring period, so every ring index is a compile-time
+// constant and no register is ever copied.  Per cell, in registers: the
+// maximum of the HT rows above (mu) and of the HT rows below (md); the cell
+// survives iff v > mu, v >= md and v >= tau -- i.e. it beats its own column
+// of the window with the lowest-(theta, rho) tie rule already applied (an
+// equal value above has a lower index, one below a higher one).  A group
+// whose centre values are all below tau (the running k-th best candidate of
+// the warp, raised by the per-frame threshold other warps publish) costs only
+// its loads and one max per cell.  The per-frame threshold is polled once per
+// ring period and used one period later, so its round trip never stalls the
+// warp.  Survivors are
+// tested against the column maxima of the +-half_rho neighbouring columns
+// (pw_survivors, out of line to keep the unrolled loop small): in-lane +-2
+// prefilter, then a warp-cooperative scan; an equal neighbouring maximum is
+// resolved exactly from the frame.
 // ---------------------------------------------------------------------------
 constexpr int PW_CPT = 8, PW_G = 2, PW_W = 8, PW_COLS = 32 * PW_CPT, PW_KMAX = 64, PW_CBUF = 128;
+#ifndef LD_PW_POLL_EVERY_GROUP
+#define LD_PW_POLL_EVERY_GROUP 1
+#endif
 
-template <int HT>
 struct PwSmem {
-  uint32_t CM[PW_G][PW_COLS];        // column maxima of the group's rows
-  uint32_t RAW[PW_G + HT][PW_COLS];  // rows g0-HT .. g0+PW_G-1 (tie checks)
-  u64 top[PW_KMAX];                  // the warp's top-k, descending
-  u64 cbuf[PW_CBUF];                 // candidates of the group
+  uint32_t CM[PW_G][PW_COLS];  // column maxima of the group's rows (when a survivor exists)
+  u64 top[PW_KMAX];            // the warp's top-k, descending
+  u64 cbuf[PW_CBUF];           // candidates of the group
 };
+
+struct PwState {
+  int ntop;
+  uint32_t gt;
+};
+
+// The rare path of the warp-strip kernel, kept out of its unrolled row loop
+// (instruction-cache footprint): exact +-hr test of the group's survivors
+// against the column maxima in S.CM, tie resolution from the frame, insertion
+// into the warp's top-k and publication of the k-th best value.  `gt` is the
+// warp's threshold on entry; the returned one includes the warp's own k-th
+// best (warp-uniform).
+template <int HT>
+__device__ __noinline__ PwState pw_survivors(PwSmem &S, uint32_t surv, int lane, int g0, int hr,
+                                             int cbase, const uint32_t *frame, int n_rho, int k,
+                                             int theta_offset, uint32_t *gtau_f, int ntop,
+                                             uint32_t gt) {
+  {  // per-lane prefilter on the nearest column maxima
+    uint32_t t = surv;
+    while (t) {
+      const int b = __ffs(t) - 1;
+      t &= t - 1u;
+      const int i = b / PW_CPT, q = b - i * PW_CPT;
+      const int j = lane + 32 * q;
+      const uint32_t v = S.CM[i][j];
+      bool ok = true;
+#pragma unroll
+      for (int d = 1; d <= 2; ++d) ok = ok && S.CM[i][j - d] <= v && S.CM[i][j + d] <= v;
+      if (!ok) surv &= ~(1u << b);
+    }
+  }
+  int ncand = 0;
+  for (;;) {  // warp-cooperative exact test of each remaining survivor
+    const uint32_t bal = __ballot_sync(0xffffffffu, surv != 0u);
+    if (!bal) break;
+    const int src = __ffs(bal) - 1;
+    const int b = __shfl_sync(0xffffffffu, __ffs(surv) - 1, src);
+    if (lane == src) surv &= surv - 1u;
+    const int i = b / PW_CPT, q = b - i * PW_CPT;
+    const int j = src + 32 * q;
+    const uint32_t *cmr = S.CM[i] + j;
+    const uint32_t v = *cmr;
+    bool bad = false, tie = false;
+    for (int d = 1 + lane; d <= hr; d += 32) {
+      const uint32_t l = cmr[-d], r = cmr[d];
+      bad = bad || l > v || r > v;
+      tie = tie || l == v || r == v;
+    }
+    if (!__any_sync(0xffffffffu, bad) && __any_sync(0xffffffffu, tie)) {
+      // an equal column maximum: reject iff an equal cell has a lower
+      // (theta, rho) index -- to the left rows up to the cell's own, to
+      // the right rows strictly above (values re-read from the frame)
+      const int t = g0 + i;
+      for (int d = 1 + lane; d <= hr && !bad; d += 32) {
+        if (cmr[-d] == v) {
+          const int c = cbase + j - d;
+          for (int row = max(t - HT, 0); row <= t && !bad; ++row)
+            bad = __ldg(frame + static_cast<int64_t>(row) * n_rho + c) == v;
+        }
+        if (!bad && cmr[d] == v) {
+          const int c = cbase + j + d;
+          for (int row = max(t - HT, 0); row < t && !bad; ++row)
+            bad = __ldg(frame + static_cast<int64_t>(row) * n_rho + c) == v;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, bad)) {
+      if (lane == 0 && LD_CHK(ncand < PW_CBUF))
+        S.cbuf[ncand] = mk_key(v, static_cast<uint32_t>((g0 + i + theta_offset) * n_rho + cbase + j));
+      ++ncand;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {  // insertion into the warp's top-k (candidates are rare)
+    for (int c = 0; c < ncand; ++c) {
+      const u64 key = S.cbuf[c];
+      if (ntop == k && key <= S.top[ntop - 1]) continue;
+      int pos = ntop < k ? ntop : k - 1;
+      while (pos > 0 && S.top[pos - 1] < key) {
+        S.top[pos] = S.top[pos - 1];
+        --pos;
+      }
+      S.top[pos] = key;
+      if (ntop < k) ++ntop;
+    }
+    if (ncand > 0 && ntop == k) {
+      const uint32_t kth = static_cast<uint32_t>(S.top[k - 1] >> 32);
+      if (kth > gt) atomicMax(gtau_f, kth);
+      gt = max(gt, kth);
+    }
+  }
+  ntop = __shfl_sync(0xffffffffu, ntop, 0);
+  gt = __shfl_sync(0xffffffffu, gt, 0);
+  return PwState{ntop, gt};
+}
 
 template <int HT>
 __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksParams p) {
@@ -748,15 +867,17 @@ __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksPar
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x * PW_W + warp, f = blockIdx.y;
   if (unit >= p.n_units) return;  // whole warp; no CTA-wide synchronisation below
-  PwSmem<HT> &S = reinterpret_cast<PwSmem<HT> *>(psm)[warp];
-  constexpr int NV = PW_G + 2 * HT;
+  PwSmem &S = reinterpret_cast<PwSmem *>(psm)[warp];
+  constexpr int NV = PW_G + 2 * HT;  // rows one group reads
+  constexpr int R = NV + PW_G;       // ring: + the next group's rows in flight
+  constexpr int U = R / PW_G;        // groups per ring period
+  static_assert(R % PW_G == 0, "ring must hold whole groups");
   const int strip = unit / p.st_chunks, chunk = unit - strip * p.st_chunks;
   const int hr = p.half_rho, n_rho = p.n_rho, n_theta = p.n_theta;
   const int cbase = strip * p.st_sw - hr;  // global column of loaded column 0
   const int tb0 = p.cand_t0 + chunk * p.st_tb;
   const int tb1 = min(tb0 + p.st_tb, p.cand_t1);
-  // lane l owns loaded columns l + 32 q (q < PW_CPT): every load instruction
-  // of the warp reads 32 consecutive words (fully coalesced)
+  const uint32_t *frame = p.acc + static_cast<int64_t>(f) * n_theta * n_rho;
   const bool all_in = cbase >= 0 && cbase + PW_COLS <= n_rho;  // warp-uniform
   uint32_t cinm = 0, ownm = 0;
 #pragma unroll
@@ -766,7 +887,8 @@ __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksPar
     cinm |= static_cast<uint32_t>(in) << q;
     ownm |= static_cast<uint32_t>(in && j >= hr && j < hr + p.st_sw) << q;
   }
-  const uint32_t *rowp = p.acc + (static_cast<int64_t>(f) * n_theta + (tb0 - HT)) * n_rho + cbase + lane;
+  const uint32_t own2 = ownm | (ownm << PW_CPT);
+  const uint32_t *rowp = frame + static_cast<int64_t>(tb0 - HT) * n_rho + cbase + lane;
   int rnext = tb0 - HT;
   auto load_row = [&](uint32_t (&dst)[PW_CPT]) {
     if (rnext >= 0 && rnext < n_theta) {
@@ -785,118 +907,74 @@ __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksPar
     ++rnext;
   };
 
-  int ntop = 0;                 // warp-uniform
+  int ntop = 0;                  // warp-uniform
   uint32_t tau = p.floor_votes;  // warp-uniform
-  uint32_t V[NV][PW_CPT], N[PW_G][PW_CPT];
+  uint32_t gt_next = 0;          // lane 0: per-frame threshold read last group
+  if (lane == 0) gt_next = ld_relaxed_u32(p.gtau + f);  // first poll, before the row loads
+  uint32_t ring[R][PW_CPT];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) load_row(V[k]);
+  for (int k = 0; k < NV; ++k) load_row(ring[k]);
 
-  for (int g0 = tb0; g0 < tb1; g0 += PW_G) {
-    if (g0 + PW_G < tb1) {
+  for (int gp = tb0; gp < tb1; gp += U * PW_G) {
 #pragma unroll
-      for (int k = 0; k < PW_G; ++k) load_row(N[k]);
-    }
-    uint32_t gt = 0;
-    if (lane == 0) gt = *reinterpret_cast<volatile uint32_t *>(p.gtau + f);
-    const int nrows = min(PW_G, tb1 - g0);
-    uint32_t surv = 0;
+    for (int u = 0; u < U; ++u) {
+      const int g0 = gp + u * PW_G;
+      if (g0 >= tb1) break;  // warp-uniform
+#define RG(k) ring[(u * PW_G + (k)) % R]
+      if (g0 + PW_G < tb1) {
 #pragma unroll
-    for (int i = 0; i < PW_G; ++i) {
-#pragma unroll
-      for (int q = 0; q < PW_CPT; ++q) {
-        uint32_t mm = V[i][q];
-#pragma unroll
-        for (int k = 1; k <= 2 * HT; ++k) mm = max(mm, V[i + k][q]);
-        S.CM[i][lane + 32 * q] = mm;
-        // v <= mm always: v >= max(mm, tau) <=> v == its column maximum and >= tau
-        surv |= static_cast<uint32_t>(V[i + HT][q] >= max(mm, tau)) << (i * PW_CPT + q);
+        for (int k = 0; k < PW_G; ++k) load_row(RG(NV + k));
       }
-    }
-    surv &= (ownm | (ownm << PW_CPT));
-    if (nrows < PW_G) surv &= (1u << (nrows * PW_CPT)) - 1u;
-#pragma unroll
-    for (int k = 0; k < PW_G + HT; ++k)
-#pragma unroll
-      for (int q = 0; q < PW_CPT; ++q) S.RAW[k][lane + 32 * q] = V[k][q];
-    __syncwarp();
-    // cheap per-lane prefilter on the nearest column maxima, then a
-    // warp-cooperative exact test of every remaining survivor
-    {
-      uint32_t t = surv;
-      while (t) {
-        const int b = __ffs(t) - 1;
-        t &= t - 1u;
-        const int i = b / PW_CPT, q = b - i * PW_CPT;
-        const int j = lane + 32 * q;
-        const uint32_t v = S.CM[i][j];
-        const int dmax = min(hr, 2);
-        bool ok = true;
-        for (int d = 1; d <= dmax; ++d) ok = ok && S.CM[i][j - d] <= v && S.CM[i][j + d] <= v;
-        if (!ok) surv &= ~(1u << b);
+      if (LD_PW_POLL_EVERY_GROUP || u == 0) {
+        // the threshold read one poll ago has arrived; read the next one
+        const uint32_t gt = gt_next;
+        if (lane == 0) gt_next = ld_relaxed_u32(p.gtau + f);
+        tau = max(tau, __shfl_sync(0xffffffffu, gt, 0));
       }
-    }
-    int ncand = 0;
-    for (;;) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, surv != 0u);
-      if (!bal) break;
-      const int src = __ffs(bal) - 1;
-      const int b = __shfl_sync(0xffffffffu, __ffs(surv) - 1, src);
-      if (lane == src) surv &= surv - 1u;
-      const int i = b / PW_CPT, q = b - i * PW_CPT;
-      const int j = src + 32 * q;
-      const uint32_t *cmr = S.CM[i] + j;
-      const uint32_t v = *cmr;
-      bool bad = lane < HT && S.RAW[i + lane][j] == v;
-      bool tie = false;
-      for (int d = 1 + lane; d <= hr; d += 32) {
-        const uint32_t l = cmr[-d], r = cmr[d];
-        bad = bad || l > v || r > v;
-        tie = tie || l == v || r == v;
-      }
-      if (!__any_sync(0xffffffffu, bad) && __any_sync(0xffffffffu, tie)) {
-        for (int d = 1 + lane; d <= hr && !bad; d += 32) {
-          if (cmr[-d] == v)
-            for (int k = i; k <= i + HT && !bad; ++k) bad = S.RAW[k][j - d] == v;
-          if (!bad && cmr[d] == v)
-            for (int k = i; k < i + HT && !bad; ++k) bad = S.RAW[k][j + d] == v;
+      const int nrows = min(PW_G, tb1 - g0);
+      const uint32_t rmask = nrows < PW_G ? ((1u << (nrows * PW_CPT)) - 1u) : 0xFFFFu;
+      // quick reject: no centre value of the warp reaches tau
+      uint32_t hm = 0;
+#pragma unroll
+      for (int i = 0; i < PW_G; ++i)
+#pragma unroll
+        for (int q = 0; q < PW_CPT; ++q) hm = max(hm, RG(i + HT)[q]);
+      uint32_t surv = 0;
+      if (__any_sync(0xffffffffu, hm >= tau)) {
+#pragma unroll
+        for (int i = 0; i < PW_G; ++i) {
+#pragma unroll
+          for (int q = 0; q < PW_CPT; ++q) {
+            const uint32_t v = RG(i + HT)[q];
+            uint32_t mu = 0, md = tau;
+#pragma unroll
+            for (int k = 0; k < HT; ++k) mu = max(mu, RG(i + k)[q]);
+#pragma unroll
+            for (int k = 1; k <= HT; ++k) md = max(md, RG(i + HT + k)[q]);
+            surv |= static_cast<uint32_t>(v > mu && v >= md) << (i * PW_CPT + q);
+          }
         }
+        surv &= own2 & rmask;
       }
-      if (!__any_sync(0xffffffffu, bad)) {
-        if (lane == 0 && LD_CHK(ncand < PW_CBUF))
-          S.cbuf[ncand] = mk_key(v, static_cast<uint32_t>((g0 + i + p.theta_offset) * n_rho + cbase + j));
-        ++ncand;
+      if (__any_sync(0xffffffffu, surv != 0u)) {
+        // column maxima of the group for the +-hr neighbour tests
+#pragma unroll
+        for (int i = 0; i < PW_G; ++i)
+#pragma unroll
+          for (int q = 0; q < PW_CPT; ++q) {
+            uint32_t mm = RG(i)[q];
+#pragma unroll
+            for (int k = 1; k <= 2 * HT; ++k) mm = max(mm, RG(i + k)[q]);
+            S.CM[i][lane + 32 * q] = mm;
+          }
+        __syncwarp();
+        const PwState st = pw_survivors<HT>(S, surv, lane, g0, hr, cbase, frame, n_rho, p.k,
+                                            p.theta_offset, p.gtau + f, ntop, tau);
+        ntop = st.ntop;
+        tau = st.gt;  // the warp's own k-th best, if its list is full (uniform)
       }
+#undef RG
     }
-    __syncwarp();
-    if (lane == 0) {  // insertion into the warp's top-k (candidates are rare)
-      for (int c = 0; c < ncand; ++c) {
-        const u64 key = S.cbuf[c];
-        if (ntop == p.k && key <= S.top[ntop - 1]) continue;
-        int pos = ntop < p.k ? ntop : p.k - 1;
-        while (pos > 0 && S.top[pos - 1] < key) {
-          S.top[pos] = S.top[pos - 1];
-          --pos;
-        }
-        S.top[pos] = key;
-        if (ntop < p.k) ++ntop;
-      }
-      if (ncand > 0 && ntop == p.k) {
-        const uint32_t kth = static_cast<uint32_t>(S.top[p.k - 1] >> 32);
-        if (kth > gt) atomicMax(p.gtau + f, kth);
-        gt = max(gt, kth);
-      }
-    }
-    ntop = __shfl_sync(0xffffffffu, ntop, 0);
-    tau = max(tau, __shfl_sync(0xffffffffu, gt, 0));
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 2 * HT; ++k)
-#pragma unroll
-      for (int q = 0; q < PW_CPT; ++q) V[k][q] = V[k + PW_G][q];
-#pragma unroll
-    for (int k = 0; k < PW_G; ++k)
-#pragma unroll
-      for (int q = 0; q < PW_CPT; ++q) V[2 * HT + k][q] = N[k][q];
   }
   u64 *out = p.band_keys + (static_cast<int64_t>(f) * p.n_units + unit) * p.k;
   for (int i = lane; i < p.k; i += 32) out[i] = i < ntop ? S.top[i] : 0ull;
@@ -912,14 +990,7 @@ static WarpKernel warp_kernel(int ht) {
     default: return nullptr;
   }
 }
-static size_t warp_smem_bytes(int ht) {
-  switch (ht) {
-    case 0: return PW_W * sizeof(PwSmem<0>);
-    case 1: return PW_W * sizeof(PwSmem<1>);
-    case 2: return PW_W * sizeof(PwSmem<2>);
-    default: return PW_W * sizeof(PwSmem<3>);
-  }
-}
+static size_t warp_smem_bytes(int) { return PW_W * sizeof(PwSmem); }
 
 // Warp-strip geometry; false when the window or k do not fit the kernel.
 static bool peaks_warp_plan(int batch, int n_theta, int n_rho, int half_theta, int half_rho, int k,
@@ -1064,7 +1135,8 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   }
   if (!force_band && !force_tile &&
       peaks_warp_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem)) {
-    cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+    cudaError_t em = getenv("LD_PEAKS_GTAU_KEEP") ? cudaSuccess
+                     : cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
     if (em != cudaSuccess) return em;
     WarpKernel kern = warp_kernel(p.half_theta);
     if (!g_warp_attr[dev & 63][p.half_theta]) {
@@ -1078,7 +1150,8 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   } else if (!force_band && !force_tile &&
       peaks_stream_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
                         &smem)) {
-    cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+    cudaError_t em = getenv("LD_PEAKS_GTAU_KEEP") ? cudaSuccess
+                     : cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
     if (em != cudaSuccess) return em;
     StreamKernel kern = stream_kernel(p.half_theta, cpt);
     bool &attr = g_stream_attr[dev & 63][cpt == 4][p.half_theta];

@@ -251,18 +251,25 @@ class ThetaShardedDetector:
     def load(self, gray_full):
         self.band.load(gray_full)
 
-    def __call__(self):
-        """Returns (peaks [1][k][3], n_peaks [1]) on every rank."""
+    def __call__(self, mark=None):
+        """Returns (peaks [1][k][3], n_peaks [1]) on every rank.  `mark(j)`, if
+        given, is called at the stage boundaries j = 0 (start), 1 (after
+        Sobel), 2 (after the edge exchange), 3 (after voting), 4 (after
+        peaks), 5 (after the top-k exchange and merge) -- bench.py records
+        CUDA events there."""
         import torch
         import torch.distributed as dist
         ld, b = self.ld, self.band
+        mark = mark or (lambda j: None)
         self.launches = 0
+        mark(0)
         if b.plan.rows > 0:
             ld.ld_sobel_binarize(b.gray, b.img, b.threshold, None, b.edges, b.edge_stride,
                                  b.count, None)
             self.launches += ld.ld_last_launch_count()
         else:
             b.count.zero_()
+        mark(1)
         multi = dist.is_initialized() and self.world > 1
         if multi:
             counts = torch.empty((self.world,), dtype=torch.int32, device=self.device)
@@ -281,17 +288,20 @@ class ThetaShardedDetector:
             edges, count, stride = self.all_edges, self.total, self.all_stride
         else:
             edges, count, stride = b.edges, b.count, b.edge_stride
-        self.vote_and_peaks(edges, count, stride)
+        mark(2)
+        self.vote_and_peaks(edges, count, stride, mark)
         if not multi:
+            mark(5)
             return self.peaks, self.n_peaks
         allp = torch.empty((self.world, self.k, 3), dtype=torch.int32, device=self.device)
         alln = torch.empty((self.world,), dtype=torch.int32, device=self.device)
         dist.all_gather_into_tensor(allp, self.peaks, group=self.group)
         dist.all_gather_into_tensor(alln, self.n_peaks, group=self.group)
         p, n = merge_peak_lists(allp, alln, self.n_rho, self.k)
+        mark(5)
         return p[None], n
 
-    def vote_and_peaks(self, edges, count, stride):
+    def vote_and_peaks(self, edges, count, stride, mark=None):
         """This rank's theta shard: vote every edge of the image (device list
         `edges`, device `count`) into rows g0 .. g1-1, then the top-k of the
         shard's own rows with global theta bins -> self.peaks, self.n_peaks."""
@@ -300,11 +310,15 @@ class ThetaShardedDetector:
             ld.ld_hough_accumulate(edges, count, stride, 1, self.w, self.h, self.g1 - self.g0,
                                    self.cos_s, self.sin_s, self.acc, None)
             self.launches += ld.ld_last_launch_count()
+        if mark:
+            mark(3)
         ld.ld_hough_peaks_ex(self.acc, 1, max(self.g1 - self.g0, 1), self.n_rho, self.half_theta,
                              self.half_rho, self.min_votes, self.k, self.t0 - self.g0,
                              self.t1 - self.g0, self.g0, self.peaks, self.n_peaks, self.ws,
                              self.ws_bytes, None)
         self.launches += ld.ld_last_launch_count()
+        if mark:
+            mark(4)
 
     def _gbuf(self, m):
         self._gflat = self.gathered.reshape(-1)[: self.world * m]
