@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--no-hint", action="store_true",
+                    help="plain ld_hough_accumulate + ld_hough_peaks (no peak hint)")
     ap.add_argument("--shard", default="band", choices=["band", "theta"],
                     help="cfg5 multi-GPU decomposition: row bands + all_reduce of the "
                          "accumulator, or theta shards + all_gather of edge lists")
@@ -246,6 +248,9 @@ def run_ours(args, rank, world, local):
     acc = torch.empty((B, cfg.n_theta, n_rho), dtype=torch.int32, device="cuda")
     pws_bytes = ld.ld_hough_peaks_workspace_bytes(B, cfg.n_theta, n_rho, cfg.k)
     pws = torch.empty((pws_bytes,), dtype=torch.uint8, device="cuda")
+    use_hint = not args.no_hint
+    hint_bytes = ld.ld_hough_hint_bytes(B, W, H, cfg.n_theta)
+    hint = torch.empty((hint_bytes,), dtype=torch.uint8, device="cuda")
     peaks = torch.empty((B, cfg.k, 3), dtype=torch.int32, device="cuda")
     npk = torch.empty((B,), dtype=torch.int32, device="cuda")
 
@@ -258,12 +263,21 @@ def run_ours(args, rank, world, local):
         launches[0] += ld.ld_last_launch_count()
         if ev is not None:
             ev[1].record(stream)
-        ld.ld_hough_accumulate(edges, counts, stride, B, W, H, cfg.n_theta, c, s, acc, stream)
+        if use_hint:
+            ld.ld_hough_accumulate_hint(edges, counts, stride, B, W, H, cfg.n_theta, c, s, acc,
+                                        hint, hint_bytes, stream)
+        else:
+            ld.ld_hough_accumulate(edges, counts, stride, B, W, H, cfg.n_theta, c, s, acc, stream)
         launches[0] += ld.ld_last_launch_count()
         if ev is not None:
             ev[2].record(stream)
-        ld.ld_hough_peaks(acc, B, cfg.n_theta, n_rho, cfg.half_theta, cfg.half_rho,
-                          cfg.min_votes, cfg.k, peaks, npk, pws, pws_bytes, stream)
+        if use_hint:
+            ld.ld_hough_peaks_hinted(acc, B, cfg.n_theta, n_rho, cfg.half_theta, cfg.half_rho,
+                                     cfg.min_votes, cfg.k, hint, hint_bytes, peaks, npk, pws,
+                                     pws_bytes, stream)
+        else:
+            ld.ld_hough_peaks(acc, B, cfg.n_theta, n_rho, cfg.half_theta, cfg.half_rho,
+                              cfg.min_votes, cfg.k, peaks, npk, pws, pws_bytes, stream)
         launches[0] += ld.ld_last_launch_count()
         if ev is not None:
             ev[3].record(stream)
@@ -372,6 +386,7 @@ def run_ours(args, rank, world, local):
                    "width": W, "height": H, "threshold": cfg.threshold, "n_theta": cfg.n_theta,
                    "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
                    "parallelism": "frame-shard dp%d" % world,
+                   "peak_hint": use_hint,
                    "l2": "inputs %.0f MB + accumulators %.0f MB per GPU exceed L2 (%.0f MB); no flush"
                          % (B * H * pitch / 1e6, peaks_bytes / 1e6, ld.ld_device_l2_bytes() / 1e6)},
         "gvotes_per_s": total_votes / (ms_per_step / 1e3) / 1e9,

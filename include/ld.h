@@ -180,6 +180,35 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
                       ld_peak *peaks, int32_t *n_peaks, void *workspace,
                       size_t workspace_bytes, void *stream);
 
+/* Peak hint: an optional by-product of voting that speeds up the peak search
+ * without changing its result (DESIGN R25).
+ *
+ * ld_hough_accumulate_hint votes exactly like ld_hough_accumulate and, while
+ * each theta band is still in shared memory, records for each of up to 32
+ * contiguous (row-major) ranges of the band the largest count and its cell
+ * (value << 32 | ~(t*n_rho + r), i.e. the lowest index among equal counts).
+ * ld_hough_peaks_hinted first verifies those cells, largest first, against
+ * the candidate definition above (a full window test on acc): verified cells
+ * are distinct candidates, so the value of the k-th verified one is a lower
+ * bound on the frame's k-th best candidate, and the search starts from it
+ * instead of min_votes.  peaks / n_peaks are bit-identical to
+ * ld_hough_peaks.  The hint must come from the ld_hough_accumulate_hint call
+ * that produced acc; a hint whose header (written by that call) does not
+ * match batch, n_theta and n_rho is ignored.
+ *  hint : device, >= ld_hough_hint_bytes(batch, width, height, n_theta),
+ *         16-B aligned; fully owned by the library between the two calls. */
+size_t ld_hough_hint_bytes(int32_t batch, int32_t width, int32_t height, int32_t n_theta);
+int ld_hough_accumulate_hint(const uint32_t *edge_xy, const uint32_t *edge_count,
+                             int64_t edge_stride, int32_t batch, int32_t width,
+                             int32_t height, int32_t n_theta, const int32_t *cos_q15,
+                             const int32_t *sin_q15, uint32_t *acc, void *hint,
+                             size_t hint_bytes, void *stream);
+int ld_hough_peaks_hinted(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                          int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                          int32_t k, const void *hint, size_t hint_bytes, ld_peak *peaks,
+                          int32_t *n_peaks, void *workspace, size_t workspace_bytes,
+                          void *stream);
+
 /* Steps 1-4 for a batch of whole frames (img->row_begin = 0, row_end = height):
  * ld_sobel_binarize (no binary map) -> ld_hough_accumulate -> ld_hough_peaks,
  * stream-ordered, no host synchronisation.

@@ -212,7 +212,7 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
 static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
                       int32_t batch, int32_t width, int32_t height, int32_t n_theta,
                       const int32_t *cos_q15, const int32_t *sin_q15, uint32_t *acc,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, void *hint = nullptr) {
   DevInfo dev;
   int rc = device_info(&dev);
   if (rc) return rc;
@@ -237,6 +237,9 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   p.n_bands = n_bands;
   p.koff = 16384 + (d << 15);
   p.acc = acc;
+  p.hint_hdr = static_cast<uint32_t *>(hint);
+  p.hint_keys = hint ? reinterpret_cast<unsigned long long *>(static_cast<char *>(hint) + HINT_HDR_BYTES)
+                     : nullptr;
   cudaError_t e = launch_hough(p, trig, ctas, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");
   return LD_OK;
@@ -246,7 +249,7 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
                       int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
                       ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t ws_bytes,
                       cudaStream_t stream, int32_t cand_t0 = 0, int32_t cand_t1 = -1,
-                      int32_t theta_offset = 0) {
+                      int32_t theta_offset = 0, const void *hint = nullptr) {
   PeaksParams p;
   p.acc = acc;
   p.batch = batch;
@@ -260,6 +263,10 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   p.cand_t0 = cand_t0;
   p.cand_t1 = cand_t1 < 0 ? n_theta : cand_t1;
   p.theta_offset = theta_offset;
+  p.hint_hdr = static_cast<const uint32_t *>(hint);
+  p.hint_keys = hint ? reinterpret_cast<const unsigned long long *>(static_cast<const char *>(hint) +
+                                                                    HINT_HDR_BYTES)
+                     : nullptr;
   // workspace: [batch] uint32 per-frame thresholds (256-B padded), then the keys
   p.gtau = static_cast<uint32_t *>(workspace);
   p.band_keys = reinterpret_cast<unsigned long long *>(
@@ -285,8 +292,13 @@ static int check_peaks_args(const uint32_t *acc, int32_t batch, int32_t n_theta,
   return LD_OK;
 }
 
+static size_t hint_bytes(int32_t batch, int32_t n_theta) {
+  // the band count never exceeds n_theta
+  return HINT_HDR_BYTES + sizeof(unsigned long long) * static_cast<size_t>(batch) * n_theta * HINT_MAX_RANGES;
+}
+
 struct DetectLayout {
-  size_t counts_off, edges_off, acc_off, peaks_off, total;
+  size_t counts_off, edges_off, acc_off, hint_off, peaks_off, total;
   int64_t edge_stride;
 };
 
@@ -303,6 +315,8 @@ static DetectLayout detect_layout(const ld_image *img, int32_t n_theta, int32_t 
   off = align_up(off + sizeof(uint32_t) * static_cast<size_t>(L.edge_stride) * img->batch, 256);
   L.acc_off = off;
   if (acc_ws) off = align_up(off + acc_bytes, 256);
+  L.hint_off = off;
+  off = align_up(off + hint_bytes(img->batch, n_theta), 256);
   L.peaks_off = off;
   off = align_up(off + peaks_workspace_bytes(img->batch, n_theta, 2 * d + 1, k), 256);
   L.total = off;
@@ -385,6 +399,30 @@ int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count, int
                     sin_q15, acc, static_cast<cudaStream_t>(stream));
 }
 
+size_t ld_hough_hint_bytes(int32_t batch, int32_t width, int32_t height, int32_t n_theta) {
+  if (batch < 1 || width < 1 || height < 1 || n_theta < 1) return 0;
+  return hint_bytes(batch, n_theta);
+}
+
+int ld_hough_accumulate_hint(const uint32_t *edge_xy, const uint32_t *edge_count,
+                             int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
+                             int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
+                             uint32_t *acc, void *hint, size_t hint_bytes_, void *stream) {
+  g_launches = 0;
+  if (!edge_xy || !edge_count || !acc || !hint) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
+  if (batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
+  if (width < 1 || height < 1 || width > LD_MAX_DIM || height > LD_MAX_DIM)
+    return fail(LD_ERR_INVALID_ARG, "width/height outside [1, %d]", LD_MAX_DIM);
+  if (!aligned(edge_xy, 16) || edge_stride < 0 || edge_stride % 4 != 0)
+    return fail(LD_ERR_INVALID_ARG, "edge_xy must be 16-byte aligned and edge_stride a multiple of 4");
+  if (n_theta < 1 || n_theta > LD_MAX_THETA)
+    return fail(LD_ERR_INVALID_ARG, "n_theta %d outside [1, %d]", n_theta, LD_MAX_THETA);
+  if (!aligned(hint, 16) || hint_bytes_ < hint_bytes(batch, n_theta))
+    return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned", hint_bytes(batch, n_theta));
+  return hough_impl(edge_xy, edge_count, edge_stride, batch, width, height, n_theta, cos_q15,
+                    sin_q15, acc, static_cast<cudaStream_t>(stream), hint);
+}
+
 size_t ld_hough_peaks_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_rho, int32_t k) {
   (void)n_rho;
   if (batch < 1 || n_theta < 1 || n_rho < 1 || k < 1) return 0;
@@ -415,6 +453,26 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   return peaks_impl(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
                     n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
                     cand_row_begin, cand_row_end, theta_offset);
+}
+
+int ld_hough_peaks_hinted(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                          int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                          const void *hint, size_t hint_bytes_, ld_peak *peaks, int32_t *n_peaks,
+                          void *workspace, size_t workspace_bytes, void *stream) {
+  g_launches = 0;
+  int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
+  if (rc) return rc;
+  if (!hint || !aligned(hint, 16) || hint_bytes_ < hint_bytes(batch, n_theta))
+    return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned", hint_bytes(batch, n_theta));
+  DevInfo dev;
+  if ((rc = device_info(&dev))) return rc;
+  if (!workspace || !aligned(workspace, 16) ||
+      workspace_bytes < peaks_workspace_bytes(batch, n_theta, n_rho, k))
+    return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 16-byte aligned",
+                peaks_workspace_bytes(batch, n_theta, n_rho, k));
+  return peaks_impl(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
+                    n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), 0, -1,
+                    0, hint);
 }
 
 int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
@@ -462,14 +520,15 @@ int ld_detect_batch_ex(const uint8_t *gray, const ld_image *img, int32_t thresho
   uint32_t *edges = reinterpret_cast<uint32_t *>(ws + L.edges_off);
   uint32_t *A = acc ? acc : reinterpret_cast<uint32_t *>(ws + L.acc_off);
   void *pws = ws + L.peaks_off;
+  void *hint = ws + L.hint_off;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if ((rc = sobel_impl(gray, img, threshold, flags, nullptr, edges, L.edge_stride, counts, s)))
     return rc;
   if ((rc = hough_impl(edges, counts, L.edge_stride, img->batch, img->width, img->height, n_theta,
-                       cos_q15, sin_q15, A, s)))
+                       cos_q15, sin_q15, A, s, hint)))
     return rc;
   if ((rc = peaks_impl(A, img->batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
-                       n_peaks, pws, workspace_bytes - L.peaks_off, s)))
+                       n_peaks, pws, workspace_bytes - L.peaks_off, s, 0, -1, 0, hint)))
     return rc;
   if (edge_count) {
     cudaError_t e = cudaMemcpyAsync(edge_count, counts, sizeof(uint32_t) * img->batch,

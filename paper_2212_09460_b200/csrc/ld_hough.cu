@@ -116,8 +116,65 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
                  "r"(smem_u32(slice + head)), "r"(static_cast<uint32_t>(mid) * 4u)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
+  if (p.hint_keys) {
+    // Peak hint (DESIGN R25), while the bulk copy reads the slice: the band's
+    // cells, row-major, split into one contiguous range per warp; for each
+    // the largest count and its first cell.  Lanes scan with 16-byte loads
+    // (the slice is 16-byte aligned at slice_raw); a lane keeps the first
+    // vector where its running maximum rose, and the warp reduction keeps the
+    // lowest cell index among equal counts.  No barrier: each warp writes its
+    // own key.
+    const int c0 = static_cast<int>((static_cast<int64_t>(ncell) * warp) / NWARPS);
+    const int c1 = static_cast<int>((static_cast<int64_t>(ncell) * (warp + 1)) / NWARPS);
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(slice_raw);
+    const int w0 = (mw + c0) >> 2, w1 = (mw + c1 + 3) >> 2;
+    auto vec = [&](int w) {  // the vector's words outside [c0, c1) read as 0
+      uint4 q = v4[w];
+      const int i0 = w * 4 - mw;
+      if (i0 < c0 || i0 + 4 > c1) {
+        q.x = (i0 >= c0 && i0 < c1) ? q.x : 0u;
+        q.y = (i0 + 1 >= c0 && i0 + 1 < c1) ? q.y : 0u;
+        q.z = (i0 + 2 >= c0 && i0 + 2 < c1) ? q.z : 0u;
+        q.w = (i0 + 3 >= c0 && i0 + 3 < c1) ? q.w : 0u;
+      }
+      return q;
+    };
+    uint32_t run = 0;
+    int pos = -1;
+    for (int w = w0 + lane; w < w1; w += 32) {
+      const uint4 q = vec(w);
+      const uint32_t m4 = max(max(q.x, q.y), max(q.z, q.w));
+      if (m4 > run) {
+        run = m4;
+        pos = w;
+      }
+    }
+    unsigned long long key = 0ull;
+    if (run) {
+      const uint4 q = vec(pos);
+      const int j = q.x == run ? 0 : q.y == run ? 1 : q.z == run ? 2 : 3;
+      const uint32_t idx = static_cast<uint32_t>(t0) * static_cast<uint32_t>(p.n_rho) +
+                           static_cast<uint32_t>(pos * 4 + j - mw);
+      key = (static_cast<unsigned long long>(run) << 32) | (0xFFFFFFFFu - idx);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other > key ? other : key;
+    }
+    if (lane == 0) p.hint_keys[(static_cast<int64_t>(f) * p.n_bands + band) * NWARPS + warp] = key;
+    if (f == 0 && band == 0 && tid == 0) {
+      uint32_t *h = p.hint_hdr;
+      h[0] = HINT_MAGIC;
+      h[1] = static_cast<uint32_t>(p.batch);
+      h[2] = static_cast<uint32_t>(p.n_theta);
+      h[3] = static_cast<uint32_t>(p.n_rho);
+      h[4] = static_cast<uint32_t>(p.n_bands);
+      h[5] = NWARPS;
+    }
+  }
+  if (tid == 0 && mid > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 static int rows_per_band(int n_theta, int n_rho, size_t limit, int *n_bands) {
@@ -154,9 +211,13 @@ cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, 
   cudaGetDevice(&dev);
   auto kern = ctas == 2 ? hough_vote_kernel<2> : hough_vote_kernel<1>;
   if (!g_hough_attr[dev & 63][ctas]) {
-    // the largest slice hough_plan can request for this CTA count (rowk is static)
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024 / ctas - static_cast<int>(sizeof(uint4)) * HV_MAX_ROWS);
+    // the largest slice hough_plan can request for this CTA count, next to the
+    // kernel's static shared memory (rowk, the hint reduction)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024 / ctas - static_cast<int>(fa.sharedSizeBytes));
     if (e != cudaSuccess) return e;
     g_hough_attr[dev & 63][ctas] = true;
   }

@@ -64,7 +64,17 @@ struct HoughParams {
   int32_t rows_per_band, n_bands;
   int32_t koff;  // 2^14 + (D << 15): rho_bin = (x*C + y*S + koff) >> 15
   uint32_t *acc;
+  uint32_t *hint_hdr;            // nullable: peak-hint header (written by CTA (0, 0))
+  unsigned long long *hint_keys;  // [batch][n_bands][warps per CTA] range maxima
 };
+
+// Peak-hint buffer layout (ld_hough_accumulate_hint / ld_hough_peaks_hinted):
+// a 64-byte header {magic, batch, n_theta, n_rho, n_bands, ranges per band,
+// 0...} then the range-maximum keys (one range per warp of the voting CTA).
+constexpr uint32_t HINT_MAGIC = 0x3148444Cu;  // "LDH1"
+constexpr int HINT_HDR_BYTES = 64;
+constexpr int HINT_MAX_KEYS = 4096;  // per frame, what the verifying kernel sorts
+constexpr int HINT_MAX_RANGES = 32;  // ranges per band (warps of a 1024-thread CTA)
 
 constexpr int HV_THREADS = 1024;  // threads per SM; a CTA has HV_THREADS / CTAS of them
 constexpr int HV_MAX_ROWS = 256;
@@ -99,6 +109,8 @@ struct PeaksParams {
   uint32_t *gtau;                 // [batch] per-frame running k-th candidate value (stream kernel)
   int32_t cand_t0, cand_t1;       // candidate rows [cand_t0, cand_t1) (windows read every row)
   int32_t theta_offset;           // added to the row index in keys and reported theta bins
+  const uint32_t *hint_hdr;       // nullable: peak hint (unrestricted searches only)
+  const unsigned long long *hint_keys;
   ld_peak *peaks;
   int32_t *n_peaks;
 };

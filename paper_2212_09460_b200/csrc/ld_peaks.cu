@@ -155,6 +155,112 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
   for (int i = threadIdx.x; i < p.k; i += PK_THREADS) out[i] = i < ntop ? top[i] : 0ull;
 }
 
+// ---------------------------------------------------------------------------
+// Peak hint (DESIGN R25): one CTA per frame turns the range maxima recorded by
+// the voting kernel into the per-frame starting threshold gtau[f].  The keys
+// are sorted (largest count first, lowest index among equals), then checked
+// eight at a time (one warp each) against the full candidate definition on
+// acc: every count in the clipped window is <= v, and an equal count has a
+// higher (theta, rho) index.  Verified cells are distinct candidates, so the
+// value of the k-th verified key in sorted order bounds the frame's k-th best
+// candidate from below; with fewer than k verified the bound is 0 (no hint).
+// ---------------------------------------------------------------------------
+constexpr int PH_THREADS = 512;
+constexpr int PH_UNROLL = 8;
+
+__global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParams p) {
+  __shared__ u64 keys[HINT_MAX_KEYS];
+  __shared__ int s_ok[PH_THREADS / 32];
+  __shared__ uint32_t s_bound;
+  __shared__ int s_done;
+  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t *h = p.hint_hdr;
+  const bool match = h[0] == HINT_MAGIC && h[1] == static_cast<uint32_t>(p.batch) &&
+                     h[2] == static_cast<uint32_t>(p.n_theta) &&
+                     h[3] == static_cast<uint32_t>(p.n_rho) && h[5] >= 1 &&
+                     h[5] <= HINT_MAX_RANGES && h[4] >= 1 && h[4] <= static_cast<uint32_t>(p.n_theta);
+  const int n_src = match ? static_cast<int>(h[4] * h[5]) : 0;
+  if (n_src <= 0) {
+    if (tid == 0) p.gtau[f] = 0u;
+    return;
+  }
+  // more keys than the sort holds: merge g consecutive ranges (the maximum of
+  // a union of ranges is again a range maximum)
+  const int g = (n_src + HINT_MAX_KEYS - 1) / HINT_MAX_KEYS;
+  const int n = (n_src + g - 1) / g;
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  const u64 *src = p.hint_keys + static_cast<int64_t>(f) * n_src;
+  for (int i = tid; i < np2; i += PH_THREADS) {
+    u64 m = 0ull;
+    for (int j = i * g; j < min(i * g + g, n_src) && i < n; ++j) m = src[j] > m ? src[j] : m;
+    keys[i] = m;
+  }
+  if (tid == 0) {
+    s_bound = 0u;
+    s_done = 0;
+  }
+  __syncthreads();
+  bitonic_desc(keys, np2);
+  const uint32_t *A = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
+  const int ht = p.half_theta, hr = p.half_rho;
+  int found = 0;  // thread 0's count of verified keys
+  for (int base = 0; base < n; base += PH_THREADS / 32) {
+    const int j = base + warp;
+    int ok = 0;
+    if (j < n) {
+      const u64 key = keys[j];
+      const uint32_t v = static_cast<uint32_t>(key >> 32);
+      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+      if (v >= p.floor_votes) {
+        const int t = static_cast<int>(idx / static_cast<uint32_t>(p.n_rho));
+        const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * p.n_rho);
+        const int ta = max(t - ht, 0), tb = min(t + ht, p.n_theta - 1);
+        const int ra = max(r - hr, 0), rb = min(r + hr, p.n_rho - 1);
+        // the clipped window as one flat range of cells, 32 x PH_UNROLL per
+        // warp step: the loads of a step are independent (no early exit
+        // between them), so a small window costs one or two round trips
+        const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
+        bool bad = false;
+        for (int c0 = 0; c0 < cells && !__any_sync(0xffffffffu, bad); c0 += 32 * PH_UNROLL) {
+          uint32_t w[PH_UNROLL], ci[PH_UNROLL];
+#pragma unroll
+          for (int u = 0; u < PH_UNROLL; ++u) {
+            const int c = c0 + 32 * u + lane;
+            const int tt = ta + c / wc, rr = ra + c % wc;
+            ci[u] = static_cast<uint32_t>(tt) * static_cast<uint32_t>(p.n_rho) + static_cast<uint32_t>(rr);
+            w[u] = c < cells ? __ldg(A + ci[u]) : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < PH_UNROLL; ++u)
+            bad = bad || w[u] > v || (w[u] == v && ci[u] < idx);
+        }
+        ok = !__any_sync(0xffffffffu, bad);
+      } else {
+        ok = -1;  // below the floor: this and every later key end the search
+      }
+    }
+    if (lane == 0) s_ok[warp] = ok;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 0; w < PH_THREADS / 32 && base + w < n; ++w) {
+        if (s_ok[w] < 0) {
+          s_done = 1;
+          break;
+        }
+        if (s_ok[w] && ++found == p.k) {
+          s_bound = static_cast<uint32_t>(keys[base + w] >> 32);
+          s_done = 1;
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  if (tid == 0) p.gtau[f] = s_bound;
+}
+
 __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksParams p) {
   __shared__ u64 buf[PK_BUF];
   __shared__ u64 top[LD_MAX_K];
@@ -1112,6 +1218,18 @@ static bool g_tile_attr[64][PT_MAX_HT + 1];
 static bool g_stream_attr[64][2][PT_MAX_HT + 1];
 static bool g_warp_attr[64][4];
 
+// Per-frame starting thresholds of the streaming kernels: the verified peak
+// hint when one is given for an unrestricted search, else 0.
+static cudaError_t init_gtau(const PeaksParams &p, bool restricted, cudaStream_t stream) {
+  if (getenv("LD_PEAKS_GTAU_KEEP")) return cudaSuccess;  // experiments (tools/exp_tau_oracle.py)
+  if (p.hint_hdr && !restricted) {
+    peaks_hint_kernel<<<p.batch, PH_THREADS, 0, stream>>>(p);
+    note_launch();
+    return cudaGetLastError();
+  }
+  return cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+}
+
 cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   PeaksParams p = p_in;
   size_t smem = 0;
@@ -1135,8 +1253,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   }
   if (!force_band && !force_tile &&
       peaks_warp_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem)) {
-    cudaError_t em = getenv("LD_PEAKS_GTAU_KEEP") ? cudaSuccess
-                     : cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+    cudaError_t em = init_gtau(p, restricted, stream);
     if (em != cudaSuccess) return em;
     WarpKernel kern = warp_kernel(p.half_theta);
     if (!g_warp_attr[dev & 63][p.half_theta]) {
@@ -1150,8 +1267,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   } else if (!force_band && !force_tile &&
       peaks_stream_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
                         &smem)) {
-    cudaError_t em = getenv("LD_PEAKS_GTAU_KEEP") ? cudaSuccess
-                     : cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+    cudaError_t em = init_gtau(p, restricted, stream);
     if (em != cudaSuccess) return em;
     StreamKernel kern = stream_kernel(p.half_theta, cpt);
     bool &attr = g_stream_attr[dev & 63][cpt == 4][p.half_theta];

@@ -53,6 +53,7 @@ PEAK_DTYPE = np.dtype([("theta_bin", "<i4"), ("rho_bin", "<i4"), ("votes", "<u4"
 LD_FLAG_ZERO_PAD, LD_FLAG_CLAMP_255 = 1, 2
 
 EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",
+           "ld_hough_hint_bytes", "ld_hough_accumulate_hint", "ld_hough_peaks_hinted",
            "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_hough_peaks_ex",
            "ld_detect_workspace_bytes",
            "ld_detect_batch", "ld_detect_batch_ex", "ld_detect_host_workspace_bytes", "ld_detect_batch_host",
@@ -78,6 +79,11 @@ def lib():
             "ld_sobel_binarize": ([P, IMG, i32, P, P, i64, P, P], ctypes.c_int),
             "ld_sobel_binarize_ex": ([P, IMG, i32, u32, P, P, i64, P, P], ctypes.c_int),
             "ld_hough_accumulate": ([P, P, i64, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
+            "ld_hough_hint_bytes": ([i32, i32, i32, i32], sz),
+            "ld_hough_accumulate_hint": ([P, P, i64, i32, i32, i32, i32, P, P, P, P, sz, P],
+                                         ctypes.c_int),
+            "ld_hough_peaks_hinted": ([P, i32, i32, i32, i32, i32, u32, i32, P, sz, P, P, P, sz,
+                                       P], ctypes.c_int),
             "ld_hough_peaks_workspace_bytes": ([i32, i32, i32, i32], sz),
             "ld_hough_peaks": ([P, i32, i32, i32, i32, i32, u32, i32, P, P, P, sz, P],
                                ctypes.c_int),
@@ -179,6 +185,28 @@ def ld_hough_accumulate(edge_xy, edge_count, edge_stride, batch, width, height, 
     _check(lib().ld_hough_accumulate(_addr(edge_xy), _addr(edge_count), int(edge_stride),
                                      int(batch), int(width), int(height), int(n_theta),
                                      _addr(c), _addr(s), _addr(acc), _stream(stream)))
+
+
+def ld_hough_hint_bytes(batch, width, height, n_theta) -> int:
+    return int(lib().ld_hough_hint_bytes(batch, width, height, n_theta))
+
+
+def ld_hough_accumulate_hint(edge_xy, edge_count, edge_stride, batch, width, height, n_theta,
+                             cos_q15, sin_q15, acc, hint, hint_bytes, stream=None):
+    c, s = _host_i32(cos_q15), _host_i32(sin_q15)
+    _check(lib().ld_hough_accumulate_hint(_addr(edge_xy), _addr(edge_count), int(edge_stride),
+                                          int(batch), int(width), int(height), int(n_theta),
+                                          _addr(c), _addr(s), _addr(acc), _addr(hint),
+                                          int(hint_bytes), _stream(stream)))
+
+
+def ld_hough_peaks_hinted(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, hint,
+                          hint_bytes, peaks, n_peaks, workspace, workspace_bytes, stream=None):
+    _check(lib().ld_hough_peaks_hinted(_addr(acc), int(batch), int(n_theta), int(n_rho),
+                                       int(half_theta), int(half_rho), int(min_votes), int(k),
+                                       _addr(hint), int(hint_bytes), _addr(peaks),
+                                       _addr(n_peaks), _addr(workspace), int(workspace_bytes),
+                                       _stream(stream)))
 
 
 def ld_hough_peaks_workspace_bytes(batch, n_theta, n_rho, k) -> int:
@@ -304,29 +332,41 @@ def sobel_binarize(gray, threshold: int, want_binary=True, want_edges=True, stre
     return binary, edges, counts, stride
 
 
-def hough_accumulate(edges, counts, edge_stride, width, height, cos_q15, sin_q15, stream=None):
+def hough_accumulate(edges, counts, edge_stride, width, height, cos_q15, sin_q15, stream=None,
+                     want_hint=False):
+    """Returns acc, or (acc, hint) with want_hint (ld_hough_accumulate_hint)."""
     import torch
     b = counts.shape[0]
     n_theta = len(cos_q15)
     n_rho = 2 * ld_rho_offset(width, height) + 1
     acc = torch.empty((b, n_theta, n_rho), dtype=torch.int32, device=counts.device)
-    ld_hough_accumulate(edges, counts, edge_stride, b, width, height, n_theta, cos_q15, sin_q15,
-                        acc, stream)
-    return acc
+    if not want_hint:
+        ld_hough_accumulate(edges, counts, edge_stride, b, width, height, n_theta, cos_q15,
+                            sin_q15, acc, stream)
+        return acc
+    hb = ld_hough_hint_bytes(b, width, height, n_theta)
+    hint = torch.empty((hb,), dtype=torch.uint8, device=counts.device)
+    ld_hough_accumulate_hint(edges, counts, edge_stride, b, width, height, n_theta, cos_q15,
+                             sin_q15, acc, hint, hb, stream)
+    return acc, hint
 
 
 def hough_peaks(acc, half_theta, half_rho, min_votes, k, stream=None, cand_rows=None,
-                theta_offset=0):
+                theta_offset=0, hint=None):
     """acc: int32 CUDA [B][n_theta][n_rho] (uint32 bits).  cand_rows=(begin, end)
     and theta_offset select ld_hough_peaks_ex (a theta slice of a larger
-    accumulator)."""
+    accumulator); hint (from hough_accumulate(want_hint=True)) selects
+    ld_hough_peaks_hinted."""
     import torch
     b, n_theta, n_rho = acc.shape
     ws_bytes = ld_hough_peaks_workspace_bytes(b, n_theta, n_rho, k)
     ws = torch.empty((max(ws_bytes, 16),), dtype=torch.uint8, device=acc.device)
     peaks = torch.empty((b, k, 3), dtype=torch.int32, device=acc.device)
     n_peaks = torch.empty((b,), dtype=torch.int32, device=acc.device)
-    if cand_rows is None and theta_offset == 0:
+    if hint is not None:
+        ld_hough_peaks_hinted(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, hint,
+                              hint.numel(), peaks, n_peaks, ws, ws_bytes, stream)
+    elif cand_rows is None and theta_offset == 0:
         ld_hough_peaks(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
                        n_peaks, ws, ws_bytes, stream)
     else:

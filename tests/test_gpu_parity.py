@@ -590,3 +590,84 @@ def test_theta_sharded_detector_emulated(ld, oracle):
         torch.cuda.synchronize()
         assert int(n[0]) == r["n_peaks"], world
         assert peak_tuples(p.cpu()) == oracle_peak_tuples(r["peaks"]), world
+
+
+# ----------------------------------------------------------------------------
+# Peak hint (DESIGN R25): ld_hough_accumulate_hint votes identically, and
+# ld_hough_peaks_hinted returns exactly ld_hough_peaks' result; the per-frame
+# threshold left in the workspace never exceeds the frame's k-th best
+# candidate value (the property that makes the hint safe).
+# ----------------------------------------------------------------------------
+def _hint_case(ld, oracle, frames, cfg, kernel=None, monkeypatch=None, check_oracle=True):
+    c, s = synth.q15_table(cfg.n_theta)
+    g = cuda(frames)
+    _, edges, counts, stride = ld.sobel_binarize(g, cfg.threshold, want_binary=False)
+    b, h, w = frames.shape
+    acc0 = ld.hough_accumulate(edges, counts, stride, w, h, c, s)
+    acc, hint = ld.hough_accumulate(edges, counts, stride, w, h, c, s, want_hint=True)
+    assert torch.equal(acc0, acc)
+    p0, n0 = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+    _, nt, nr = acc.shape
+    wsb = ld.ld_hough_peaks_workspace_bytes(b, nt, nr, cfg.k)
+    ws = torch.zeros((wsb,), dtype=torch.uint8, device="cuda")
+    p1 = torch.empty((b, cfg.k, 3), dtype=torch.int32, device="cuda")
+    n1 = torch.empty((b,), dtype=torch.int32, device="cuda")
+    ld.ld_hough_peaks_hinted(acc, b, nt, nr, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k,
+                             hint, hint.numel(), p1, n1, ws, wsb)
+    torch.cuda.synchronize()
+    assert torch.equal(n0, n1) and torch.equal(p0, p1)
+    gtau = ws[:4 * b].view(torch.int32).cpu().numpy().view(np.uint32)
+    n1c, p1c = n1.cpu().numpy(), p1.cpu().numpy()
+    for f in range(b):
+        if n1c[f] == cfg.k:
+            assert gtau[f] <= np.uint32(np.int32(p1c[f, cfg.k - 1, 2])), (f, gtau[f])
+    if check_oracle:
+        A = acc.cpu().numpy().view(np.uint32)
+        for f in range(b):
+            pk, npk = oracle.hough_peaks(A[f], cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+            assert int(n1c[f]) == npk
+            assert peak_tuples(p1c[f]) == oracle_peak_tuples(pk)  # sentinels included
+    return gtau, p1c, n1c
+
+
+@pytest.mark.parametrize("name,nf", [("cfg1", 1), ("cfg2", 1), ("cfg3", 6), ("cfg4", 2),
+                                     ("cfg5", 1)])
+def test_hinted_peaks_identical(ld, oracle, name, nf):
+    cfg = synth.CONFIGS[name]
+    frames = synth.gen_batch(name, 0, nf) if cfg.batch > 1 else synth.gen_frame(name, 0)[None]
+    gtau, p, n = _hint_case(ld, oracle, frames, cfg)
+    # the hint is not vacuous on the road configs: the start threshold reached
+    # a real candidate value for some frame
+    if name in ("cfg2", "cfg3"):
+        assert gtau.max() > 1
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("k", [1, 4, 64])
+def test_hinted_peaks_ties_and_sparse(ld, oracle, seed, k):
+    # low-contrast frames (many equal small counts: ties everywhere) and a few
+    # hard lines; several window sizes through the warp and stream kernels
+    rng = np.random.default_rng(100 + seed)
+    frames = rng.integers(0, 2, size=(3, 96, 160), dtype=np.uint8) * 255
+    frames[1] = 0
+    frames[1, 40:43, :] = 255
+    frames[2, :, 70:72] = 255
+    for (ht, hr) in [(0, 4), (2, 29), (3, 64), (7, 44), (10, 116)]:
+        cfg = synth.Config("t", 160, 96, 3, 200, 90, k, ht, hr)
+        _hint_case(ld, oracle, frames, cfg)
+
+
+def test_hint_header_mismatch_ignored(ld, oracle):
+    cfg = synth.CONFIGS["cfg2"]
+    frames = synth.gen_frame("cfg2", 0)[None]
+    c, s = synth.q15_table(cfg.n_theta)
+    _, edges, counts, stride = ld.sobel_binarize(cuda(frames), cfg.threshold, want_binary=False)
+    acc, hint = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s, want_hint=True)
+    p0, n0 = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, 1, cfg.k)
+    bad = hint.clone()
+    bad[:4] = 0  # wrong magic: ignored
+    p1, n1 = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=bad)
+    assert torch.equal(p0, p1) and torch.equal(n0, n1)
+    with pytest.raises(ld.LdError):  # too small a hint buffer
+        ld.ld_hough_accumulate_hint(edges, counts, stride, 1, 1280, 720, cfg.n_theta, c, s, acc,
+                                    hint, 64)
