@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 
+#include <cstdlib>
 #include "ld_internal.cuh"
 
 namespace ld {
@@ -144,6 +145,30 @@ static int check_trig(int32_t n_theta, const int32_t *c, const int32_t *s, int32
   return LD_OK;
 }
 
+// Half-angle pairing (NEXT 2) is exact iff the table is symmetric,
+// C[n-t] = -C[t] and S[n-t] = S[t] for 0 < t < n, t != n/2; the unpaired rows
+// (t = 0, t = n/2) also vote their mirror (-C[t], S[t]) into a scratch row,
+// whose bins must pass the same corner range proof.  LD_VOTE_PAIRED=0
+// disables the paired kernel.
+static bool pairable_trig(int32_t n_theta, const int32_t *c, const int32_t *s, int32_t w,
+                          int32_t h, int32_t d) {
+  const char *env = getenv("LD_VOTE_PAIRED");
+  if (env && env[0] == '0') return false;
+  for (int t = 1; t < n_theta; ++t)
+    if (2 * t != n_theta && (c[n_theta - t] != -c[t] || s[n_theta - t] != s[t])) return false;
+  const int64_t n_rho = 2 * static_cast<int64_t>(d) + 1;
+  const int64_t xs[2] = {0, w - 1}, ys[2] = {0, h - 1};
+  for (int t = 0; t < n_theta; t += (n_theta % 2 == 0 && n_theta > 1) ? n_theta / 2 : n_theta) {
+    if (-static_cast<int64_t>(c[t]) > 32768) return false;
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        const int64_t v = -xs[a] * c[t] + ys[b] * s[t] + 16384 + (static_cast<int64_t>(d) << 15);
+        if (v < 0 || (v >> 15) >= n_rho) return false;
+      }
+  }
+  return true;
+}
+
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // ---------------------------------------------------------------------------
@@ -221,7 +246,11 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   const int n_rho = 2 * d + 1;
   int ctas = 1, rpb = 0, n_bands = 0;
   size_t smem = 0;
-  if (!hough_plan(n_theta, n_rho, static_cast<size_t>(dev.smem_optin), &ctas, &rpb, &n_bands, &smem))
+  const bool paired = pairable_trig(n_theta, cos_q15, sin_q15, width, height, d) &&
+                      hough_plan_pairs(n_theta, n_rho, static_cast<size_t>(dev.smem_optin), &ctas,
+                                       &rpb, &n_bands, &smem);
+  if (!paired &&
+      !hough_plan(n_theta, n_rho, static_cast<size_t>(dev.smem_optin), &ctas, &rpb, &n_bands, &smem))
     return fail(LD_ERR_UNSUPPORTED, "one accumulator row (%d bins) exceeds shared memory", n_rho);
   static thread_local TrigTable trig;  // 16 KB: keep it off the stack
   memcpy(trig.c, cos_q15, sizeof(int32_t) * n_theta);
@@ -240,7 +269,10 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   p.hint_hdr = static_cast<uint32_t *>(hint);
   p.hint_keys = hint ? reinterpret_cast<unsigned long long *>(static_cast<char *>(hint) + HINT_HDR_BYTES)
                      : nullptr;
-  cudaError_t e = launch_hough(p, trig, ctas, smem, stream);
+  p.n_pairs = paired ? hough_pair_count(n_theta) : 0;
+  p.pair_delta = static_cast<uint32_t>(rpb) * static_cast<uint32_t>(n_rho) * 4u;
+  cudaError_t e = paired ? launch_hough_pairs(p, trig, ctas, smem, stream)
+                         : launch_hough(p, trig, ctas, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");
   return LD_OK;
 }

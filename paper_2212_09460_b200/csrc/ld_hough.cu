@@ -14,6 +14,8 @@
 // range proof done on the host (ld_api.cu) makes a per-vote bounds check
 // unnecessary.  The band is then written to HBM with plain coalesced stores:
 // no global atomics anywhere.
+#include <cstdlib>
+
 #include "ld_internal.cuh"
 
 #ifndef LD_HV_UNROLL
@@ -220,6 +222,239 @@ cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, 
                              227 * 1024 / ctas - static_cast<int>(fa.sharedSizeBytes));
     if (e != cudaSuccess) return e;
     g_hough_attr[dev & 63][ctas] = true;
+  }
+  dim3 grid(p.n_bands, p.batch);
+  kern<<<grid, HV_THREADS / ctas, smem_bytes, stream>>>(p, trig);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Half-angle paired voting (NEXT 2; the paper's Eq. 4-5): for a
+// table with C[n-t] = -C[t] and S[n-t] = S[t], the rows t and n - t share
+// Q = y*S[t] + K: V_t = Q + x*C[t], V_{n-t} = Q - x*C[t].  A CTA holds pairs
+// p0 .. p0+np-1: rows t = p0 + i in the first half of its slice (in order,
+// like the unpaired kernel), their partners n - t in the second half at the
+// same slot i, i.e. a CONSTANT distance delta = rows_per_band * 4 n_rho bytes
+// above, which the compiler folds into the ATOMS as a uniform-register offset
+// ([R+UR]):
+//   addr(t)   = ((x*C + Q) >> 13) & ~3          (Q = y*S + koff + (row t address << 13))
+//   addr(n-t) = ((x*(-C) + Q) >> 13) & ~3, + delta
+// 9 instructions per 2 votes instead of 10; consecutive bins stay in distinct
+// banks.  Folding is exact as in the unpaired kernel: V in [0, 2^31) for both
+// rows (host range proof, mirrored entries included), addresses < 2^18.
+// Pair p = 0 and p = n/2 (n even) have no partner: their mirror votes land in
+// a scratch row that is not written out.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int pair_partner(int t, int n_theta) {
+  return (t == 0 || 2 * t == n_theta) ? -1 : n_theta - t;
+}
+
+int hough_pair_count(int n_theta) { return n_theta / 2 + 1; }
+
+template <int EPL, bool FULL>
+__device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t blk, uint32_t end,
+                                                 int lane, int np, const uint4 *rowk,
+                                                 uint32_t delta) {
+  uint32_t xs[EPL], ys[EPL];
+  bool ok[EPL];
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    const uint32_t e = blk + 32u * j + lane;
+    ok[j] = FULL || e < end;
+    const uint32_t q = ok[j] ? __ldg(el + e) : 0u;
+    xs[j] = q & 0xFFFFu;
+    ys[j] = q >> 16;
+  }
+#pragma unroll 2
+  for (int r = 0; r < np; ++r) {
+    const uint4 k = rowk[r];  // C, S, K, -C
+#pragma unroll
+    for (int j = 0; j < EPL; ++j)
+      if (FULL || ok[j]) {
+        const uint32_t q = ys[j] * k.y + k.z;
+        red_shared_add(((xs[j] * k.x + q) >> 13) & ~3u, 1u);
+        red_shared_add((((xs[j] * k.w + q) >> 13) & ~3u) + delta, 1u);
+      }
+  }
+}
+
+template <int CTAS>
+__global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
+    hough_vote_pairs_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
+  constexpr int NT = HV_THREADS / CTAS;
+  constexpr int NWARPS = NT / 32;
+  extern __shared__ __align__(16) uint32_t slice_raw[];
+  __shared__ uint4 rowk[HV_MAX_ROWS];  // per pair: C, S, K = koff + (row t address << 13), -C
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int band = blockIdx.x;
+  const int f = blockIdx.y;
+  const int n_rho = p.n_rho, n_theta = p.n_theta;
+  const int p0 = band * p.rows_per_band;
+  const int np = min(p.rows_per_band, p.n_pairs - p0);
+  const int ncell = np * n_rho;                       // first half (rows p0 ..)
+  const int half = p.rows_per_band * n_rho;           // words to the partner half
+  uint32_t *frame = p.acc + static_cast<int64_t>(f) * n_theta * n_rho;
+  uint32_t *dst = frame + static_cast<int64_t>(p0) * n_rho;
+  // first half at the destination's address modulo 16 (bulk write-out)
+  const int mw = static_cast<int>((reinterpret_cast<uintptr_t>(dst) & 15u) >> 2);
+  uint32_t *slice = slice_raw + mw;
+  const uint32_t sbase = smem_u32(slice);
+  const uint32_t row_bytes = static_cast<uint32_t>(n_rho) * 4u;
+  const uint32_t delta = p.pair_delta;
+  {
+    uint4 *s4 = reinterpret_cast<uint4 *>(slice_raw);
+    const int n4 = (mw + half + ncell + 3) >> 2;
+    for (int i = tid; i < n4; i += NT) s4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < np; i += NT) {
+      const int t = p0 + i;
+      rowk[i] = make_uint4(static_cast<uint32_t>(trig.c[t]), static_cast<uint32_t>(trig.s[t]),
+                           static_cast<uint32_t>(p.koff) + ((sbase + i * row_bytes) << 13),
+                           static_cast<uint32_t>(-trig.c[t]));
+    }
+  }
+  __syncthreads();
+
+  const uint32_t n_edges = p.counts[f];
+  const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
+  uint32_t base = 0;
+  for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
+    vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, delta);
+  uint32_t blk = base + static_cast<uint32_t>(warp) * (32u * 8u);
+  for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
+    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, delta);
+  if (blk < n_edges) vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, delta);
+  __syncthreads();
+
+  // write-out, first half: rows p0 .. p0+np-1 are consecutive in acc -- one
+  // bulk copy of the aligned middle, head and tail words by threads
+  const int head = min((4 - mw) & 3, ncell);
+  const int mid = ((ncell - head) >> 2) << 2;
+  if (tid < head) dst[tid] = slice[tid];
+  for (int i = head + mid + tid; i < ncell; i += NT) dst[i] = slice[i];
+  if (tid == 0 && mid > 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
+                 "r"(smem_u32(slice + head)), "r"(static_cast<uint32_t>(mid) * 4u)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  // second half: partner rows n - t descend as t ascends; coalesced thread
+  // stores (the scratch partner of an unpaired row is dropped).  The peak
+  // hint (R25) rides along here and scans the first half.
+  const bool hint = p.hint_keys != nullptr;
+  uint32_t run = 0, ridx = 0xFFFFFFFFu;
+  for (int i = 0; i < np; ++i) {
+    const int tp = pair_partner(p0 + i, n_theta);
+    if (tp < 0) continue;  // uniform
+    uint32_t *rb = frame + static_cast<int64_t>(tp) * n_rho;
+    const uint32_t *src = slice + half + i * n_rho;
+    const uint32_t ib = static_cast<uint32_t>(tp) * static_cast<uint32_t>(n_rho);
+    for (int j = tid; j < n_rho; j += NT) {
+      const uint32_t v = src[j];
+      rb[j] = v;
+      if (hint && v > run) {
+        run = v;
+        ridx = ib + static_cast<uint32_t>(j);
+      }
+    }
+  }
+  if (hint) {
+    unsigned long long key = run ? (static_cast<unsigned long long>(run) << 32) | (0xFFFFFFFFu - ridx) : 0ull;
+    // first half: this warp's contiguous share, 16-byte loads
+    const int c0 = static_cast<int>((static_cast<int64_t>(ncell) * warp) / NWARPS);
+    const int c1 = static_cast<int>((static_cast<int64_t>(ncell) * (warp + 1)) / NWARPS);
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(slice_raw);
+    const int w0 = (mw + c0) >> 2, w1 = (mw + c1 + 3) >> 2;
+    auto vec = [&](int w) {
+      uint4 q = v4[w];
+      const int i0 = w * 4 - mw;
+      if (i0 < c0 || i0 + 4 > c1) {
+        q.x = (i0 >= c0 && i0 < c1) ? q.x : 0u;
+        q.y = (i0 + 1 >= c0 && i0 + 1 < c1) ? q.y : 0u;
+        q.z = (i0 + 2 >= c0 && i0 + 2 < c1) ? q.z : 0u;
+        q.w = (i0 + 3 >= c0 && i0 + 3 < c1) ? q.w : 0u;
+      }
+      return q;
+    };
+    uint32_t r2 = 0;
+    int pos = -1;
+    for (int w = w0 + lane; w < w1; w += 32) {
+      const uint4 q = vec(w);
+      const uint32_t m4 = max(max(q.x, q.y), max(q.z, q.w));
+      if (m4 > r2) {
+        r2 = m4;
+        pos = w;
+      }
+    }
+    if (r2) {
+      const uint4 q = vec(pos);
+      const int jj = q.x == r2 ? 0 : q.y == r2 ? 1 : q.z == r2 ? 2 : 3;
+      const uint32_t idx = static_cast<uint32_t>(p0) * static_cast<uint32_t>(n_rho) +
+                           static_cast<uint32_t>(pos * 4 + jj - mw);
+      const unsigned long long k2 = (static_cast<unsigned long long>(r2) << 32) | (0xFFFFFFFFu - idx);
+      key = k2 > key ? k2 : key;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other > key ? other : key;
+    }
+    if (lane == 0) p.hint_keys[(static_cast<int64_t>(f) * p.n_bands + band) * NWARPS + warp] = key;
+    if (f == 0 && band == 0 && tid == 0) {
+      uint32_t *h = p.hint_hdr;
+      h[0] = HINT_MAGIC;
+      h[1] = static_cast<uint32_t>(p.batch);
+      h[2] = static_cast<uint32_t>(p.n_theta);
+      h[3] = static_cast<uint32_t>(p.n_rho);
+      h[4] = static_cast<uint32_t>(p.n_bands);
+      h[5] = NWARPS;
+    }
+  }
+  if (tid == 0 && mid > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+int hough_plan_pairs(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *ppb, int *n_bands,
+                     size_t *smem_bytes) {
+  const size_t fixed = sizeof(uint4) * HV_MAX_ROWS + 1024 + 16;
+  const int np = hough_pair_count(n_theta);
+  const size_t pair = static_cast<size_t>(n_rho) * 8u;
+  auto plan = [&](size_t limit, int *nb) {
+    int pmax = static_cast<int>(limit / pair);
+    if (pmax > HV_MAX_ROWS) pmax = HV_MAX_ROWS;
+    if (pmax < 1) return 0;
+    *nb = (np + pmax - 1) / pmax;
+    return (np + *nb - 1) / *nb;
+  };
+  int nb1 = 0, nb2 = 0;
+  const int p1 = plan(smem_optin - fixed, &nb1);
+  if (p1 < 1) return 0;
+  const int p2 = plan(smem_optin / 2 - fixed, &nb2);
+  const char *env = getenv("LD_VOTE_CTAS");
+  const bool two = env ? (env[0] == '2' && p2 >= 1) : (p2 >= 4 && p1 >= 8);
+  *ctas = two ? 2 : 1;
+  *ppb = two ? p2 : p1;
+  *n_bands = two ? nb2 : nb1;
+  *smem_bytes = ((static_cast<size_t>(*ppb) * pair + 15) / 16) * 16 + 16;
+  return 1;
+}
+
+static bool g_pairs_attr[64][3];
+
+cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int ctas,
+                               size_t smem_bytes, cudaStream_t stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto kern = ctas == 2 ? hough_vote_pairs_kernel<2> : hough_vote_pairs_kernel<1>;
+  if (!g_pairs_attr[dev & 63][ctas]) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024 / ctas - static_cast<int>(fa.sharedSizeBytes));
+    if (e != cudaSuccess) return e;
+    g_pairs_attr[dev & 63][ctas] = true;
   }
   dim3 grid(p.n_bands, p.batch);
   kern<<<grid, HV_THREADS / ctas, smem_bytes, stream>>>(p, trig);

@@ -61,7 +61,11 @@ struct HoughParams {
   int64_t edge_stride;
   int32_t batch;
   int32_t n_theta, n_rho;
-  int32_t rows_per_band, n_bands;
+  int32_t rows_per_band, n_bands;  // paired kernel: pairs per band, bands
+  int32_t n_pairs;                 // paired kernel (NEXT 2): theta pairs (t, n_theta - t)
+  uint32_t pair_delta;             // paired kernel: bytes from row t to its partner's row
+                                   // (= rows_per_band * n_rho * 4, a parameter so that it
+                                   // stays a uniform-register ATOMS offset)
   int32_t koff;  // 2^14 + (D << 15): rho_bin = (x*C + y*S + koff) >> 15
   uint32_t *acc;
   uint32_t *hint_hdr;            // nullable: peak-hint header (written by CTA (0, 0))
@@ -86,6 +90,16 @@ int hough_plan(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *rows_p
                int *n_bands, size_t *smem_bytes);
 cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, size_t smem_bytes,
                          cudaStream_t stream);
+// Half-angle paired voting (NEXT 2, Eq. 4-5): valid when the table is
+// symmetric, C[n-t] = -C[t] and S[n-t] = S[t] for 0 < t < n (checked on the
+// host).  Pair p = (t = p, n - t); p = 0 and p = n/2 (n even) have no partner
+// and vote their mirror into a scratch row.  Same planning contract as
+// hough_plan, in pairs.
+int hough_pair_count(int n_theta);
+int hough_plan_pairs(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *pairs_per_band,
+                     int *n_bands, size_t *smem_bytes);
+cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int ctas,
+                               size_t smem_bytes, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // B4: peaks (ld_peaks.cu)
@@ -177,6 +191,11 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
 
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// the counter 4 bytes above addr (an immediate offset of the ATOMS)
+__device__ __forceinline__ void red_shared_add_next(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0+4], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {

@@ -144,8 +144,22 @@ def gpu_vote_list(ld, edge_lists, w, h, n_theta):
     return acc.cpu().numpy().view(np.uint32)
 
 
-@pytest.mark.parametrize("n_theta", [1, 2, 3, 180, 181, 720, 1024, 2048])
-def test_vote_random_lists(ld, oracle, n_theta):
+# LD_VOTE_PAIRED=0 forces the plain kernel; unset, a symmetric table (every
+# synth.q15_table) selects the half-angle paired kernel (NEXT 2)
+VOTE_MODES = ["paired", "plain"]
+
+
+@pytest.fixture(params=VOTE_MODES)
+def vote_mode(request, monkeypatch):
+    if request.param == "plain":
+        monkeypatch.setenv("LD_VOTE_PAIRED", "0")
+    else:
+        monkeypatch.delenv("LD_VOTE_PAIRED", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("n_theta", [1, 2, 3, 4, 5, 180, 181, 720, 1024, 2048])
+def test_vote_random_lists(ld, oracle, n_theta, vote_mode):
     c, s = synth.q15_table(n_theta)
     rng = np.random.default_rng(n_theta)
     w, h = 301, 203
@@ -158,7 +172,7 @@ def test_vote_random_lists(ld, oracle, n_theta):
         assert np.array_equal(got[i], oracle.hough_accumulate(e, w, h, c, s)), (n_theta, len(e))
 
 
-def test_vote_extreme_corners_and_tiny(ld, oracle):
+def test_vote_extreme_corners_and_tiny(ld, oracle, vote_mode):
     for w, h in [(1, 1), (2, 1), (16384, 1), (1, 16384), (16384, 16384)]:
         c, s = synth.q15_table(64)
         corners = sorted({(0, 0), (w - 1, 0), (0, h - 1), (w - 1, h - 1)})
@@ -167,13 +181,44 @@ def test_vote_extreme_corners_and_tiny(ld, oracle):
         assert np.array_equal(got[0], oracle.hough_accumulate(e, w, h, c, s)), (w, h)
 
 
-def test_vote_collinear_hotspot(ld, oracle):
+def test_vote_collinear_hotspot(ld, oracle, vote_mode):
     # thousands of votes into the same bin (same-address atomics)
     c, s = synth.q15_table(180)
     e = np.array([(100 << 16) | x for x in range(1000)] * 3, np.uint32)
     got = gpu_vote_list(ld, [e], 1000, 200, 180)
     want = oracle.hough_accumulate(e, 1000, 200, c, s)
     assert np.array_equal(got[0], want) and want.max() == 3000
+
+
+def test_vote_asymmetric_table_uses_plain_path(ld, oracle):
+    # one entry off the symmetry C[n-t] = -C[t]: the paired kernel would be
+    # wrong for that row, so the host must fall back (results stay exact)
+    c, s = synth.q15_table(180)
+    c = c.copy()
+    c[30] += 1
+    rng = np.random.default_rng(5)
+    w, h = 640, 360
+    xs, ys = rng.integers(0, w, 20000), rng.integers(0, h, 20000)
+    e = (ys.astype(np.uint32) << 16) | xs.astype(np.uint32)
+    counts = cuda(np.array([len(e)], np.int32))
+    acc = ld.hough_accumulate(cuda(e.view(np.int32)[None]), counts, len(e), w, h, c, s)
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy().view(np.uint32)[0],
+                          oracle.hough_accumulate(e, w, h, c, s))
+
+
+def test_vote_paired_equals_plain_on_frames(ld, monkeypatch):
+    cfg = synth.CONFIGS["cfg3"]
+    c, s = synth.q15_table(cfg.n_theta)
+    _, edges, counts, stride = ld.sobel_binarize(cuda(synth.gen_batch("cfg3", 0, 4)), cfg.threshold,
+                                                 want_binary=False)
+    a1, h1 = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s, want_hint=True)
+    monkeypatch.setenv("LD_VOTE_PAIRED", "0")
+    a0, h0 = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s, want_hint=True)
+    assert torch.equal(a0, a1)
+    p0, n0 = ld.hough_peaks(a0, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=h0)
+    p1, n1 = ld.hough_peaks(a1, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=h1)
+    assert torch.equal(p0, p1) and torch.equal(n0, n1)
 
 
 def test_vote_range_error(ld):
