@@ -36,8 +36,10 @@ def build(force: bool = False) -> str:
              max(os.path.getmtime(SRC), os.path.getmtime(HDR)) > os.path.getmtime(LIB))
     if force or stale:
         tmp = LIB + ".tmp%d" % os.getpid()
+        # -ffp-contract=off: every double product and quotient of the lanes
+        # module (R27, R28) is rounded on its own, as the header states
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-Wextra", "-Werror",
-                               "-fPIC", "-shared", "-o", tmp, SRC])
+                               "-ffp-contract=off", "-fPIC", "-shared", "-o", tmp, SRC, "-lm"])
         os.replace(tmp, LIB)
     return LIB
 
@@ -61,6 +63,10 @@ def lib():
         L.ldo_compact.argtypes = [P, i32, i32, P, i64, P]
         L.ldo_hough_accumulate.argtypes = [P, i64, i32, i32, i32, P, P, P]
         L.ldo_hough_peaks.argtypes = [P, i32, i32, i32, i32, u32, i32, P, P]
+        L.ldo_hough_peaks_nms.argtypes = [P, i32, i32, i32, i32, u32, u32, u32, i32, P, P]
+        L.ldo_peak_to_line.argtypes = [Peak, i32, i32, i32, P, P, P, P]
+        L.ldo_extract_segments.argtypes = [P, i32, i32, i64, Peak, i32, P, P, i32, i32, P, i32,
+                                           P]
         L.ldo_detect.argtypes = [P, i32, i32, i64, i32, i32, P, P, i32, i32, u32, i32,
                                  P, P, P, P, P, P]
         for f in ("ldo_sobel_magnitude", "ldo_sobel_binarize", "ldo_sobel_magnitude_ex",
@@ -191,3 +197,52 @@ def detect(gray: np.ndarray, threshold: int, cos_q15: np.ndarray, sin_q15: np.nd
                             _ptr(peaks), ctypes.byref(npk)), "detect")
     return {"binary": binary, "edges": edges[: ne.value].copy(), "n_edges": int(ne.value),
             "acc": acc, "peaks": peaks, "n_peaks": int(npk.value)}
+
+
+# ----------------------------------------------------------------------------
+# NEXT 3: lanes module (ld_oracle.h R26-R28)
+# ----------------------------------------------------------------------------
+SEG_DTYPE = np.dtype([("x0", "<i4"), ("y0", "<i4"), ("x1", "<i4"), ("y1", "<i4")])
+
+
+def hough_peaks_nms(acc: np.ndarray, half_theta: int, half_rho: int, min_votes: int,
+                    ratio_num: int, ratio_den: int, k: int) -> tuple[np.ndarray, int]:
+    a = np.ascontiguousarray(acc, dtype=np.uint32)
+    n_theta, n_rho = a.shape
+    peaks = np.empty(k, PEAK_DTYPE)
+    n = ctypes.c_int32(0)
+    _check(lib().ldo_hough_peaks_nms(_ptr(a), n_theta, n_rho, half_theta, half_rho,
+                                     int(min_votes), int(ratio_num), int(ratio_den), k,
+                                     _ptr(peaks), ctypes.byref(n)), "hough_peaks_nms")
+    return peaks, int(n.value)
+
+
+def _peak(p) -> Peak:
+    return Peak(int(p[0]), int(p[1]), int(p[2]))
+
+
+def peak_to_line(peak, width: int, height: int, cos_q15: np.ndarray,
+                 sin_q15: np.ndarray):
+    """peak = (theta_bin, rho_bin, votes).  Returns (x0, y0, x1, y1) or None."""
+    c = np.ascontiguousarray(cos_q15, dtype=np.int32)
+    s = np.ascontiguousarray(sin_q15, dtype=np.int32)
+    seg = np.zeros(1, SEG_DTYPE)
+    hit = ctypes.c_int32(0)
+    _check(lib().ldo_peak_to_line(_peak(peak), width, height, c.shape[0], _ptr(c), _ptr(s),
+                                  _ptr(seg), ctypes.byref(hit)), "peak_to_line")
+    return tuple(int(v) for v in seg[0]) if hit.value else None
+
+
+def extract_segments(binary: np.ndarray, peak, cos_q15: np.ndarray, sin_q15: np.ndarray,
+                     fill_gap: int = 20, min_len: int = 40, cap: int = 1024):
+    """Returns the list of (x0, y0, x1, y1) segments in walk order."""
+    b = np.ascontiguousarray(binary, dtype=np.uint8)
+    h, w = b.shape
+    c = np.ascontiguousarray(cos_q15, dtype=np.int32)
+    s = np.ascontiguousarray(sin_q15, dtype=np.int32)
+    segs = np.zeros(max(cap, 1), SEG_DTYPE)
+    n = ctypes.c_int32(0)
+    _check(lib().ldo_extract_segments(_ptr(b), w, h, w, _peak(peak), c.shape[0], _ptr(c),
+                                      _ptr(s), fill_gap, min_len, _ptr(segs), cap,
+                                      ctypes.byref(n)), "extract_segments")
+    return [tuple(int(v) for v in segs[i]) for i in range(min(n.value, cap))], int(n.value)

@@ -7,6 +7,7 @@
  */
 #include "ld_oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -269,4 +270,155 @@ int ldo_detect(const uint8_t *gray, int32_t width, int32_t height, int64_t pitch
   if (!edges) free(edg);
   if (!acc) free(ac);
   return rc;
+}
+
+/* ---------------------------------------------------------------------------
+ * NEXT 3: lanes module (R26-R28)
+ * ------------------------------------------------------------------------- */
+int ldo_hough_peaks_nms(const uint32_t *acc, int32_t n_theta, int32_t n_rho,
+                        int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                        uint32_t ratio_num, uint32_t ratio_den, int32_t k,
+                        ldo_peak *peaks, int32_t *n_peaks) {
+  if (!acc || !peaks || !n_peaks || n_theta < 1 || n_rho < 1 || half_theta < 0 ||
+      half_rho < 0 || k < 1 || ratio_den < 1)
+    return LDO_EARG;
+  const int64_t cells = (int64_t)n_theta * n_rho;
+  uint32_t gmax = 0;
+  for (int64_t i = 0; i < cells; i++)
+    if (acc[i] > gmax) gmax = acc[i];
+  uint32_t floor_votes = min_votes > 1 ? min_votes : 1;
+  unsigned char *suppressed = (unsigned char *)calloc((size_t)cells, 1);
+  if (!suppressed) return LDO_ENOMEM;
+  int32_t m = 0;
+  while (m < k) {
+    /* the eligible, unsuppressed cell with the largest key */
+    int64_t best = -1;
+    for (int32_t t = 0; t < n_theta; t++) {
+      for (int32_t r = 0; r < n_rho; r++) {
+        int64_t i = (int64_t)t * n_rho + r;
+        uint32_t v = acc[i];
+        if (suppressed[i] || v < floor_votes) continue;
+        if ((uint64_t)v * ratio_den < (uint64_t)ratio_num * gmax) continue;
+        if (best < 0 || key_greater(v, t, r, acc[best], (int32_t)(best / n_rho),
+                                    (int32_t)(best % n_rho)))
+          best = i;
+      }
+    }
+    if (best < 0) break;
+    int32_t bt = (int32_t)(best / n_rho), br = (int32_t)(best % n_rho);
+    peaks[m].theta_bin = bt;
+    peaks[m].rho_bin = br;
+    peaks[m].votes = acc[best];
+    m++;
+    for (int32_t t = bt - half_theta; t <= bt + half_theta; t++) {
+      if (t < 0 || t >= n_theta) continue;
+      for (int32_t r = br - half_rho; r <= br + half_rho; r++) {
+        if (r < 0 || r >= n_rho) continue;
+        suppressed[(int64_t)t * n_rho + r] = 1;
+      }
+    }
+  }
+  for (int32_t i = m; i < k; i++) {
+    peaks[i].theta_bin = -1;
+    peaks[i].rho_bin = -1;
+    peaks[i].votes = 0;
+  }
+  *n_peaks = m;
+  free(suppressed);
+  return LDO_OK;
+}
+
+static int32_t round_half_up(double v) { return (int32_t)floor(v + 0.5); }
+
+int ldo_peak_to_line(ldo_peak peak, int32_t width, int32_t height, int32_t n_theta,
+                     const int32_t *cos_q15, const int32_t *sin_q15, ldo_segment *seg,
+                     int32_t *hit) {
+  if (!cos_q15 || !sin_q15 || !seg || !hit || width < 1 || height < 1 ||
+      peak.theta_bin < 0 || peak.theta_bin >= n_theta)
+    return LDO_EARG;
+  int32_t d = ldo_rho_offset(width, height);
+  double c = (double)cos_q15[peak.theta_bin] / 32768.0;
+  double s = (double)sin_q15[peak.theta_bin] / 32768.0;
+  double rho = (double)(peak.rho_bin - d);
+  double px[4], py[4];
+  int n = 0;
+  double xs[2] = {0.0, (double)(width - 1)}, ys[2] = {0.0, (double)(height - 1)};
+  if (s != 0.0) {
+    for (int i = 0; i < 2; i++) {
+      double y = (rho - xs[i] * c) / s;
+      if (y >= 0.0 && y <= (double)(height - 1)) { px[n] = xs[i]; py[n] = y; n++; }
+    }
+  }
+  if (c != 0.0) {
+    for (int i = 0; i < 2; i++) {
+      double x = (rho - ys[i] * s) / c;
+      if (x >= 0.0 && x <= (double)(width - 1)) { px[n] = x; py[n] = ys[i]; n++; }
+    }
+  }
+  if (n == 0) { *hit = 0; return LDO_OK; }
+  int lo = 0, hi = 0;
+  double plo = -px[0] * s + py[0] * c, phi = plo;
+  for (int i = 1; i < n; i++) {
+    double p = -px[i] * s + py[i] * c;
+    if (p < plo) { plo = p; lo = i; }
+    if (p > phi) { phi = p; hi = i; }
+  }
+  int32_t ax = round_half_up(px[lo]), ay = round_half_up(py[lo]);
+  int32_t bx = round_half_up(px[hi]), by = round_half_up(py[hi]);
+  if (bx < ax || (bx == ax && by < ay)) {
+    int32_t tx = ax, ty = ay;
+    ax = bx; ay = by; bx = tx; by = ty;
+  }
+  seg->x0 = ax; seg->y0 = ay; seg->x1 = bx; seg->y1 = by;
+  *hit = 1;
+  return LDO_OK;
+}
+
+int ldo_extract_segments(const uint8_t *binary, int32_t width, int32_t height,
+                         int64_t pitch, ldo_peak peak, int32_t n_theta,
+                         const int32_t *cos_q15, const int32_t *sin_q15,
+                         int32_t fill_gap, int32_t min_len, ldo_segment *segs,
+                         int32_t cap, int32_t *n_segs) {
+  if (!binary || !cos_q15 || !sin_q15 || !n_segs || width < 1 || height < 1 ||
+      pitch < width || peak.theta_bin < 0 || peak.theta_bin >= n_theta ||
+      fill_gap < 0 || min_len < 0 || cap < 0 || (cap > 0 && !segs))
+    return LDO_EARG;
+  int32_t d = ldo_rho_offset(width, height);
+  int32_t ci = cos_q15[peak.theta_bin], si = sin_q15[peak.theta_bin];
+  *n_segs = 0;
+  if (ci == 0 && si == 0) return LDO_OK;
+  double c = (double)ci / 32768.0, s = (double)si / 32768.0;
+  double rho = (double)(peak.rho_bin - d);
+  int along_x = (si < 0 ? -si : si) >= (ci < 0 ? -ci : ci);
+  int32_t n = along_x ? width : height;
+  int32_t count = 0;
+  int32_t run_a = -1, run_b = -1; /* walk indices of the current run's ends */
+  int32_t ax = 0, ay = 0, bx = 0, by = 0;
+  for (int32_t i = 0; i <= n; i++) {
+    int white = 0;
+    int32_t x = 0, y = 0;
+    if (i < n) {
+      if (along_x) { x = i; y = round_half_up((rho - (double)i * c) / s); }
+      else { y = i; x = round_half_up((rho - (double)i * s) / c); }
+      white = x >= 0 && x < width && y >= 0 && y < height &&
+              binary[(int64_t)y * pitch + x] == 255;
+    }
+    /* close the run when the walk ends or this white sample is too far */
+    if (run_a >= 0 && (i == n || (white && i - run_b - 1 > fill_gap))) {
+      int64_t dx = bx - ax, dy = by - ay;
+      if (dx * dx + dy * dy >= (int64_t)min_len * min_len) {
+        if (count < cap) {
+          segs[count].x0 = ax; segs[count].y0 = ay;
+          segs[count].x1 = bx; segs[count].y1 = by;
+        }
+        count++;
+      }
+      run_a = -1;
+    }
+    if (!white) continue;
+    if (run_a < 0) { run_a = i; ax = x; ay = y; }
+    run_b = i; bx = x; by = y;
+  }
+  *n_segs = count;
+  return LDO_OK;
 }

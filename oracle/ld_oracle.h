@@ -122,6 +122,60 @@ int ldo_detect(const uint8_t *gray, int32_t width, int32_t height, int64_t pitch
                int64_t *n_edges, uint32_t *acc, ldo_peak *peaks,
                int32_t *n_peaks);
 
+/* ---------------------------------------------------------------------------
+ * NEXT 3: SPEC's lanes module, completing Fig. 1 step 4 (P:42,
+ * "draw the lane lines"; P:185 MATLAB houghpeaks / Fig. 12 houghlines).
+ * DESIGN R26-R28.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t x0, y0, x1, y1; /* pixel endpoints */
+} ldo_segment;
+
+/* R26, SPEC find_peaks: greedy non-maximum suppression.
+ *   gmax = the largest count of acc; a cell is eligible iff
+ *     acc >= max(1, min_votes)  and  acc * ratio_den >= ratio_num * gmax
+ *   (the "threshold_ratio x global max" rule as an exact integer test);
+ *   repeat up to k times: select the eligible, not yet suppressed cell with
+ *   the largest key(t, r) = (acc, -t, -r); stop if there is none; suppress
+ *   every cell with |t'-t| <= half_theta and |r'-r| <= half_rho (clipped, no
+ *   theta wrap-around), the selected cell included.
+ * peaks[0..k) and *n_peaks as ldo_hough_peaks (sentinel {-1,-1,0} fill).
+ * ratio_den >= 1. */
+int ldo_hough_peaks_nms(const uint32_t *acc, int32_t n_theta, int32_t n_rho,
+                        int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                        uint32_t ratio_num, uint32_t ratio_den, int32_t k,
+                        ldo_peak *peaks, int32_t *n_peaks);
+
+/* R27, SPEC peak_to_line: the line x*c + y*s = rho of a peak,
+ * c = C[t] / 32768, s = S[t] / 32768 (the caller's Q15 table, exact binary
+ * fractions), rho = rho_bin - D, clipped to the rectangle of pixel centres
+ * [0, W-1] x [0, H-1].  In double precision, each product and quotient
+ * rounded once (no fused multiply-add):
+ *   for X in {0, W-1}, if s != 0: Y = (rho - X*c) / s, kept if 0 <= Y <= H-1;
+ *   for Y in {0, H-1}, if c != 0: X = (rho - Y*s) / c, kept if 0 <= X <= W-1;
+ *   the kept points with the smallest and the largest projection -X*s + Y*c
+ *   (first one found on ties) are the ends; each coordinate is rounded to
+ *   floor(v + 0.5); seg = the two ends, the lexicographically smaller (x, y)
+ *   first.  *hit = 0 (seg untouched) when no point is kept. */
+int ldo_peak_to_line(ldo_peak peak, int32_t width, int32_t height, int32_t n_theta,
+                     const int32_t *cos_q15, const int32_t *sin_q15, ldo_segment *seg,
+                     int32_t *hit);
+
+/* R28, SPEC extract_segments: walk the rasterised peak line
+ * (c, s, rho as in R27).  If |S[t]| >= |C[t]| the walk steps x = 0 .. W-1
+ * with y = floor((rho - x*c) / s + 0.5), else y = 0 .. H-1 with
+ * x = floor((rho - y*s) / c + 0.5); a sample is white iff it lies in the
+ * image and binary == 255.  White samples whose walk indices differ by at
+ * most fill_gap + 1 belong to one run; a run from sample a to sample b is a
+ * segment (a, b) iff (xb-xa)^2 + (yb-ya)^2 >= min_len^2.  Segments in walk
+ * order; the first cap are written, *n_segs = how many there are.  A table
+ * entry with C[t] = S[t] = 0 has no line: *n_segs = 0. */
+int ldo_extract_segments(const uint8_t *binary, int32_t width, int32_t height,
+                         int64_t pitch, ldo_peak peak, int32_t n_theta,
+                         const int32_t *cos_q15, const int32_t *sin_q15,
+                         int32_t fill_gap, int32_t min_len, ldo_segment *segs,
+                         int32_t cap, int32_t *n_segs);
+
 #ifdef __cplusplus
 }
 #endif

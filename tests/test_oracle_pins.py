@@ -403,3 +403,141 @@ def test_detect_composes_stages(oracle):
     pk, n = oracle.hough_peaks(acc, 2, 8, 1, 5)
     assert np.array_equal(r["edges"], e) and np.array_equal(r["acc"], acc)
     assert _as_tuples(r["peaks"]) == _as_tuples(pk) and r["n_peaks"] == n
+
+
+# ----------------------------------------------------------------------------
+# NEXT 3: lanes module (DESIGN R26-R28)
+# ----------------------------------------------------------------------------
+def test_lanes_golden_spec_examples(oracle):
+    g = load_golden("lanes_pins.json")
+    c, s = synth.q15_table(180)
+    for case in g["peak_to_line"]:
+        d = oracle.rho_offset(case["w"], case["h"])
+        got = oracle.peak_to_line((case["theta_bin"], d + case["rho"], 1), case["w"], case["h"],
+                                  c, s)
+        assert got == tuple(case["segment"]), case["cite"]
+    for case in g["extract_segments"]:
+        b = np.zeros((case["h"], case["w"]), np.uint8)
+        for a, e in case["white"]:
+            b[case["row"], a:e] = 255
+        d = oracle.rho_offset(case["w"], case["h"])
+        segs, n = oracle.extract_segments(b, (90, d + case["row"], 1), c, s, case["fill_gap"],
+                                          case["min_len"])
+        assert segs == [tuple(x) for x in case["segments"]] and n == len(segs), case["cite"]
+    for case in g["find_peaks"]:
+        acc = np.zeros((case["n_theta"], case["n_rho"]), np.uint32)
+        for t, r, v in case["cells"]:
+            acc[t, r] = v
+        pk, n = oracle.hough_peaks_nms(acc, case["nhood"][0], case["nhood"][1], 1, 0, 1, case["k"])
+        assert [tuple(int(v) for v in p) for p in pk[:n]] == [tuple(x) for x in case["peaks"]]
+
+
+def test_nms_greedy_differs_from_window_maxima(oracle):
+    # hand chain along rho (half_rho = 2): 5 @ r0, 6 @ r2, 7 @ r4.  The window
+    # maxima are {r4}; greedy picks r4, suppresses r2..r6, and r0 (5) is then
+    # the largest unsuppressed cell -- a pick that is not a window maximum.
+    acc = np.zeros((1, 12), np.uint32)
+    acc[0, [0, 2, 4]] = [5, 6, 7]
+    pk, n = oracle.hough_peaks_nms(acc, 0, 2, 1, 0, 1, 4)
+    assert n == 2 and [tuple(int(v) for v in p) for p in pk[:2]] == [(0, 4, 7), (0, 0, 5)]
+    wp, wn = oracle.hough_peaks(acc, 0, 2, 1, 4)
+    assert wn == 1 and tuple(int(v) for v in wp[0]) == (0, 4, 7)
+
+
+def test_nms_ratio_threshold_is_inclusive(oracle):
+    acc = np.zeros((5, 40), np.uint32)
+    acc[0, 0], acc[2, 20], acc[4, 39] = 10, 5, 4
+    pk, n = oracle.hough_peaks_nms(acc, 0, 0, 1, 1, 2, 8)  # votes >= 0.5 * 10
+    assert n == 2 and [int(p["votes"]) for p in pk[:2]] == [10, 5]
+    pk, n = oracle.hough_peaks_nms(acc, 0, 0, 6, 0, 1, 8)  # min_votes floor
+    assert n == 1
+    pk, n = oracle.hough_peaks_nms(np.zeros((3, 3), np.uint32), 1, 1, 1, 0, 1, 2)
+    assert n == 0 and all(tuple(int(v) for v in p) == (-1, -1, 0) for p in pk)
+
+
+def test_nms_sparse_far_cells_is_a_sort(oracle):
+    # cells pairwise farther apart than the window: greedy = all cells by key
+    rng = np.random.default_rng(3)
+    for trial in range(20):
+        acc = np.zeros((60, 200), np.uint32)
+        cells = []
+        for t in range(0, 60, 7):
+            for r in range(0, 200, 19):
+                if rng.random() < 0.5:
+                    v = int(rng.integers(1, 6))
+                    acc[t, r] = v
+                    cells.append((v, -t, -r))
+        cells.sort(reverse=True)
+        want = [(-t, -r, v) for v, t, r in cells][:12]
+        pk, n = oracle.hough_peaks_nms(acc, 3, 9, 1, 0, 1, 12)
+        assert [tuple(int(v) for v in p) for p in pk[:n]] == want
+
+
+def test_nms_first_pick_is_global_max_and_picks_are_separated(oracle):
+    rng = np.random.default_rng(4)
+    for trial in range(30):
+        acc = rng.integers(0, 9, size=(int(rng.integers(1, 30)), int(rng.integers(1, 60)))).astype(np.uint32)
+        ht, hr, k = int(rng.integers(0, 4)), int(rng.integers(0, 8)), int(rng.integers(1, 10))
+        pk, n = oracle.hough_peaks_nms(acc, ht, hr, 1, 0, 1, k)
+        wp, wn = oracle.hough_peaks(acc, ht, hr, 1, 1)
+        if acc.max() == 0:
+            assert n == 0
+            continue
+        assert tuple(int(v) for v in pk[0]) == tuple(int(v) for v in wp[0])  # the key maximum
+        picks = [tuple(int(v) for v in p) for p in pk[:n]]
+        for i in range(n):
+            for j in range(i):  # a later pick is outside every earlier window
+                assert abs(picks[i][0] - picks[j][0]) > ht or abs(picks[i][1] - picks[j][1]) > hr
+            assert picks[i][2] == acc[picks[i][0], picks[i][1]]
+        assert [p[2] for p in picks] == sorted((p[2] for p in picks), reverse=True)
+        # maximality: every unpicked positive cell is inside some pick's window
+        if n < k:
+            for t, r in zip(*np.nonzero(acc)):
+                assert any(abs(t - p[0]) <= ht and abs(r - p[1]) <= hr for p in picks)
+
+
+def test_peak_to_line_endpoints_on_line_and_border(oracle):
+    # every returned end is the rounding of a point of the rectangle's border
+    # that lies on x cos + y sin = rho, so it is within 0.5*sqrt(2) px of the
+    # line (in the table's own cos/sin) and at the border (up to rounding)
+    rng = np.random.default_rng(5)
+    for n_theta in (180, 720):
+        c, s = synth.q15_table(n_theta)
+        for trial in range(200):
+            w, h = int(rng.integers(2, 700)), int(rng.integers(2, 500))
+            d = oracle.rho_offset(w, h)
+            t = int(rng.integers(0, n_theta))
+            r = int(rng.integers(-d, d + 1))
+            seg = oracle.peak_to_line((t, d + r, 1), w, h, c, s)
+            cc, ss = c[t] / 32768.0, s[t] / 32768.0
+            if seg is None:
+                # a miss: every corner is strictly on one side of the line
+                vals = [x * cc + y * ss - r for x in (0, w - 1) for y in (0, h - 1)]
+                assert all(v > 0 for v in vals) or all(v < 0 for v in vals)
+                continue
+            for x, y in ((seg[0], seg[1]), (seg[2], seg[3])):
+                assert 0 <= x <= w - 1 and 0 <= y <= h - 1
+                assert abs(x * cc + y * ss - r) <= 0.5 * (abs(cc) + abs(ss)) + 1e-9
+                assert min(x, y, w - 1 - x, h - 1 - y) <= 0  # on the border
+            assert (seg[0], seg[1]) <= (seg[2], seg[3])
+
+
+def test_extract_segments_gap_rule_and_vertical_walk(oracle):
+    c, s = synth.q15_table(180)
+    d = oracle.rho_offset(120, 90)
+    b = np.zeros((90, 120), np.uint8)
+    # column x = 30 (theta bin 0 walks along y): runs 0..29 and 56..89 (gap 26)
+    b[0:30, 30] = 255
+    b[56:90, 30] = 255
+    segs, n = oracle.extract_segments(b, (0, d + 30, 1), c, s, 25, 20)
+    assert segs == [(30, 0, 30, 29), (30, 56, 30, 89)]
+    segs, n = oracle.extract_segments(b, (0, d + 30, 1), c, s, 26, 20)  # gap 26 <= 26
+    assert segs == [(30, 0, 30, 89)]
+    segs, n = oracle.extract_segments(b, (0, d + 30, 1), c, s, 25, 33)  # second run is 33 long
+    assert segs == [(30, 56, 30, 89)]
+    # capacity: count reported, list truncated
+    b2 = np.zeros((10, 200), np.uint8)
+    b2[4, ::3] = 255
+    segs, n = oracle.extract_segments(b2, (90, oracle.rho_offset(200, 10) + 4, 1), c, s, 0, 0,
+                                      cap=5)
+    assert n == 67 and len(segs) == 5 and segs[0] == (0, 4, 0, 4)
