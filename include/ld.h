@@ -209,6 +209,55 @@ int ld_hough_peaks_hinted(const uint32_t *acc, int32_t batch, int32_t n_theta, i
                           int32_t *n_peaks, void *workspace, size_t workspace_bytes,
                           void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Lanes module: Fig. 1 step 4, "draw the
+ * lane lines", i.e. MATLAB houghpeaks + houghlines (Fig. 12)
+ * made deterministic.  DESIGN R26-R28.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t x0, y0, x1, y1; /* pixel endpoints, (x0, y0) <= (x1, y1) lexicographically for lines */
+} ld_segment;
+
+/* Greedy non-maximum suppression (SPEC find_peaks S:329-337; DESIGN R26):
+ * a cell is eligible iff acc >= max(1, min_votes) and
+ * acc * ratio_den >= ratio_num * (largest count of the frame); up to k times
+ * the eligible, unsuppressed cell with the largest key (acc, -t, -r) is taken
+ * and every cell with |t'-t| <= half_theta, |r'-r| <= half_rho (clipped)
+ * becomes suppressed.  peaks / n_peaks as ld_hough_peaks (sentinel fill).
+ * ratio_den >= 1 (ratio 1/2 = MATLAB's default 0.5 * max).
+ *  workspace : device, >= ld_hough_peaks_nms_workspace_bytes(...), 16-B aligned.
+ * Cost: k passes over the accumulators (exact for every input). */
+size_t ld_hough_peaks_nms_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_rho);
+int ld_hough_peaks_nms(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                       int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                       uint32_t ratio_num, uint32_t ratio_den, int32_t k, ld_peak *peaks,
+                       int32_t *n_peaks, void *workspace, size_t workspace_bytes,
+                       void *stream);
+
+/* peak_to_line (DESIGN R27): for peaks[f][i], i < n_peaks[f],
+ * the line x*c + y*s = rho_bin - D with c = C[t]/32768, s = S[t]/32768 (the
+ * caller's HOST Q15 table), clipped to the pixel-centre rectangle
+ * [0, W-1] x [0, H-1], ends rounded half up; hit[f][i] = 1 and lines[f][i]
+ * set, else hit[f][i] = 0 (no intersection, or i >= n_peaks[f]).
+ *  peaks [batch][k], n_peaks [batch], lines [batch][k], hit [batch][k]: device. */
+int ld_peak_lines(const ld_peak *peaks, const int32_t *n_peaks, int32_t batch, int32_t k,
+                  int32_t width, int32_t height, int32_t n_theta, const int32_t *cos_q15,
+                  const int32_t *sin_q15, ld_segment *lines, int32_t *hit, void *stream);
+
+/* extract_segments (DESIGN R28): walk the rasterised line of
+ * each peak over the binary map (255 = edge): along x when |S[t]| >= |C[t]|,
+ * else along y, rounding half up; white samples at most fill_gap + 1 walk
+ * steps apart form one run; a run is a segment iff its Euclidean length is
+ * >= min_len.  segments[f][i][0..max_segments) in walk order,
+ * n_segments[f][i] = how many exist (may exceed max_segments).
+ *  binary: device, frames described by img (width, height, pitch,
+ *  frame_stride, batch; whole frames), as written by ld_sobel_binarize. */
+int ld_extract_segments(const uint8_t *binary, const ld_image *img, const ld_peak *peaks,
+                        const int32_t *n_peaks, int32_t k, int32_t n_theta,
+                        const int32_t *cos_q15, const int32_t *sin_q15, int32_t fill_gap,
+                        int32_t min_len, int32_t max_segments, ld_segment *segments,
+                        int32_t *n_segments, void *stream);
+
 /* Steps 1-4 for a batch of whole frames (img->row_begin = 0, row_end = height):
  * ld_sobel_binarize (no binary map) -> ld_hough_accumulate -> ld_hough_peaks,
  * stream-ordered, no host synchronisation.

@@ -524,6 +524,137 @@ size_t ld_detect_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k
   return detect_layout(&whole, n_theta, k, acc_in_workspace != 0).total;
 }
 
+// ---------------------------------------------------------------------------
+// Lanes module (NEXT 3)
+// ---------------------------------------------------------------------------
+static size_t nms_layout(int32_t batch, int32_t n_theta, int32_t n_rho, int64_t *words,
+                         size_t *bitmap_off) {
+  *words = (static_cast<int64_t>(n_theta) * n_rho + 31) / 32;
+  *bitmap_off = align_up(sizeof(NmsState) * static_cast<size_t>(batch), 256);
+  return *bitmap_off + sizeof(uint32_t) * static_cast<size_t>(*words) * batch;
+}
+
+size_t ld_hough_peaks_nms_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_rho) {
+  if (batch < 1 || n_theta < 1 || n_rho < 1) return 0;
+  int64_t w;
+  size_t off;
+  return nms_layout(batch, n_theta, n_rho, &w, &off);
+}
+
+int ld_hough_peaks_nms(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                       int32_t half_theta, int32_t half_rho, uint32_t min_votes,
+                       uint32_t ratio_num, uint32_t ratio_den, int32_t k, ld_peak *peaks,
+                       int32_t *n_peaks, void *workspace, size_t workspace_bytes,
+                       void *stream) {
+  g_launches = 0;
+  int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
+  if (rc) return rc;
+  if (ratio_den < 1) return fail(LD_ERR_INVALID_ARG, "ratio_den must be >= 1");
+  int64_t words;
+  size_t off;
+  const size_t need = nms_layout(batch, n_theta, n_rho, &words, &off);
+  if (!workspace || !aligned(workspace, 16) || workspace_bytes < need)
+    return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 16-byte aligned", need);
+  DevInfo dev;
+  if ((rc = device_info(&dev))) return rc;
+  NmsParams p;
+  p.acc = acc;
+  p.batch = batch;
+  p.n_theta = n_theta;
+  p.n_rho = n_rho;
+  p.half_theta = half_theta;
+  p.half_rho = half_rho;
+  p.k = k;
+  p.floor_votes = min_votes > 1 ? min_votes : 1u;
+  p.ratio_num = ratio_num;
+  p.ratio_den = ratio_den;
+  p.state = static_cast<NmsState *>(workspace);
+  p.bitmap = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + off);
+  p.bitmap_words = words;
+  p.peaks = peaks;
+  p.n_peaks = n_peaks;
+  cudaError_t e = launch_nms(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "NMS kernels launch");
+  return LD_OK;
+}
+
+static int lanes_common(const ld_peak *peaks, const int32_t *n_peaks, int32_t batch, int32_t k,
+                        int32_t width, int32_t height, int32_t n_theta, const int32_t *c,
+                        const int32_t *s, LanesParams *p, TrigTable *trig) {
+  if (!peaks || !n_peaks) return fail(LD_ERR_INVALID_ARG, "NULL peaks/n_peaks");
+  if (batch < 1 || k < 1 || k > LD_MAX_K) return fail(LD_ERR_INVALID_ARG, "bad batch/k");
+  if (width < 1 || height < 1 || width > LD_MAX_DIM || height > LD_MAX_DIM)
+    return fail(LD_ERR_INVALID_ARG, "width/height outside [1, %d]", LD_MAX_DIM);
+  if (n_theta < 1 || n_theta > LD_MAX_THETA || !c || !s)
+    return fail(LD_ERR_INVALID_ARG, "bad trig table");
+  for (int t = 0; t < n_theta; ++t)
+    if (c[t] < -32768 || c[t] > 32768 || s[t] < -32768 || s[t] > 32768)
+      return fail(LD_ERR_RANGE, "trig entry %d (%d, %d) exceeds |32768|", t, c[t], s[t]);
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  memset(p, 0, sizeof(*p));
+  p->peaks = peaks;
+  p->n_peaks = n_peaks;
+  p->batch = batch;
+  p->k = k;
+  p->width = width;
+  p->height = height;
+  p->n_theta = n_theta;
+  p->rho_offset = rho_offset(width, height);
+  memcpy(trig->c, c, sizeof(int32_t) * n_theta);
+  memcpy(trig->s, s, sizeof(int32_t) * n_theta);
+  return LD_OK;
+}
+
+int ld_peak_lines(const ld_peak *peaks, const int32_t *n_peaks, int32_t batch, int32_t k,
+                  int32_t width, int32_t height, int32_t n_theta, const int32_t *cos_q15,
+                  const int32_t *sin_q15, ld_segment *lines, int32_t *hit, void *stream) {
+  g_launches = 0;
+  static thread_local TrigTable trig;
+  LanesParams p;
+  int rc = lanes_common(peaks, n_peaks, batch, k, width, height, n_theta, cos_q15, sin_q15, &p,
+                        &trig);
+  if (rc) return rc;
+  if (!lines || !hit) return fail(LD_ERR_INVALID_ARG, "NULL lines/hit");
+  p.lines = lines;
+  p.hit = hit;
+  cudaError_t e = launch_peak_lines(p, trig, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "peak_lines_kernel launch");
+  return LD_OK;
+}
+
+int ld_extract_segments(const uint8_t *binary, const ld_image *img, const ld_peak *peaks,
+                        const int32_t *n_peaks, int32_t k, int32_t n_theta,
+                        const int32_t *cos_q15, const int32_t *sin_q15, int32_t fill_gap,
+                        int32_t min_len, int32_t max_segments, ld_segment *segments,
+                        int32_t *n_segments, void *stream) {
+  g_launches = 0;
+  if (!img || !binary) return fail(LD_ERR_INVALID_ARG, "NULL binary/img");
+  if (img->pitch < img->width || img->batch < 1 ||
+      (img->batch > 1 && img->frame_stride < static_cast<int64_t>(img->height) * img->pitch))
+    return fail(LD_ERR_INVALID_ARG, "binary geometry: pitch >= width, frame_stride >= height*pitch");
+  if (fill_gap < 0 || min_len < 0 || max_segments < 1)
+    return fail(LD_ERR_INVALID_ARG, "fill_gap, min_len >= 0 and max_segments >= 1");
+  if (!segments || !n_segments) return fail(LD_ERR_INVALID_ARG, "NULL segments/n_segments");
+  static thread_local TrigTable trig;
+  LanesParams p;
+  int rc = lanes_common(peaks, n_peaks, img->batch, k, img->width, img->height, n_theta, cos_q15,
+                        sin_q15, &p, &trig);
+  if (rc) return rc;
+  p.binary = binary;
+  p.bin_pitch = img->pitch;
+  p.bin_frame_stride = img->batch > 1 ? img->frame_stride : static_cast<int64_t>(img->height) * img->pitch;
+  p.fill_gap = fill_gap;
+  p.min_len = min_len;
+  p.max_segs = max_segments;
+  p.segs = segments;
+  p.n_segs = n_segments;
+  cudaError_t e = launch_extract_segments(p, trig, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "extract_segments_kernel launch");
+  return LD_OK;
+}
+
 int ld_detect_batch_ex(const uint8_t *gray, const ld_image *img, int32_t threshold,
                        uint32_t flags, int32_t n_theta, const int32_t *cos_q15,
                        const int32_t *sin_q15, int32_t half_theta, int32_t half_rho,

@@ -133,6 +133,45 @@ size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k);
 cudaError_t launch_peaks(const PeaksParams &p, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
+// NEXT 3: lanes module (ld_lanes.cu)
+// ---------------------------------------------------------------------------
+struct NmsState {
+  unsigned long long best;  // arg-max key of the current round
+  uint32_t npicks;
+  uint32_t thr;             // eligibility threshold (0 until the first pick)
+  uint32_t done;
+  uint32_t pad;
+};
+
+struct NmsParams {
+  const uint32_t *acc;
+  int32_t batch, n_theta, n_rho, half_theta, half_rho, k;
+  uint32_t floor_votes, ratio_num, ratio_den;
+  NmsState *state;       // [batch]
+  uint32_t *bitmap;      // [batch][bitmap_words] suppression bits
+  int64_t bitmap_words;
+  ld_peak *peaks;
+  int32_t *n_peaks;
+};
+cudaError_t launch_nms(const NmsParams &p, cudaStream_t stream);
+
+struct LanesParams {
+  const ld_peak *peaks;   // [batch][k]
+  const int32_t *n_peaks;  // [batch]
+  int32_t batch, k, width, height, n_theta, rho_offset;
+  ld_segment *lines;       // peak_to_line: [batch][k]
+  int32_t *hit;            // [batch][k]
+  const uint8_t *binary;   // extract_segments: [batch] frames of [height][bin_pitch]
+  int64_t bin_pitch, bin_frame_stride;
+  int32_t fill_gap, min_len, max_segs;
+  ld_segment *segs;        // [batch][k][max_segs]
+  int32_t *n_segs;         // [batch][k]
+};
+cudaError_t launch_peak_lines(const LanesParams &p, const TrigTable &trig, cudaStream_t stream);
+cudaError_t launch_extract_segments(const LanesParams &p, const TrigTable &trig,
+                                    cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
 // B5: shared-memory atomic microbenchmark (ld_hough.cu)
 // ---------------------------------------------------------------------------
 cudaError_t launch_smem_atomic_bench(int mode, int iters, int grid, uint32_t *scratch,

@@ -55,6 +55,8 @@ LD_FLAG_ZERO_PAD, LD_FLAG_CLAMP_255 = 1, 2
 EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",
            "ld_hough_hint_bytes", "ld_hough_accumulate_hint", "ld_hough_peaks_hinted",
            "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_hough_peaks_ex",
+           "ld_hough_peaks_nms_workspace_bytes", "ld_hough_peaks_nms", "ld_peak_lines",
+           "ld_extract_segments",
            "ld_detect_workspace_bytes",
            "ld_detect_batch", "ld_detect_batch_ex", "ld_detect_host_workspace_bytes", "ld_detect_batch_host",
            "ld_bench_smem_atomics", "ld_device_sm_count", "ld_device_l2_bytes",
@@ -89,6 +91,12 @@ def lib():
                                ctypes.c_int),
             "ld_hough_peaks_ex": ([P, i32, i32, i32, i32, i32, u32, i32, i32, i32, i32, P, P, P,
                                    sz, P], ctypes.c_int),
+            "ld_hough_peaks_nms_workspace_bytes": ([i32, i32, i32], sz),
+            "ld_hough_peaks_nms": ([P, i32, i32, i32, i32, i32, u32, u32, u32, i32, P, P, P, sz,
+                                    P], ctypes.c_int),
+            "ld_peak_lines": ([P, P, i32, i32, i32, i32, i32, P, P, P, P, P], ctypes.c_int),
+            "ld_extract_segments": ([P, IMG, P, P, i32, i32, P, P, i32, i32, i32, P, P, P],
+                                    ctypes.c_int),
             "ld_detect_workspace_bytes": ([IMG, i32, i32, i32], sz),
             "ld_detect_batch": ([P, IMG, i32, i32, P, P, i32, i32, u32, i32, P, P, P, P, P, sz, P],
                                 ctypes.c_int),
@@ -229,6 +237,36 @@ def ld_hough_peaks_ex(acc, batch, n_theta, n_rho, half_theta, half_rho, min_vote
                                    int(cand_row_begin), int(cand_row_end), int(theta_offset),
                                    _addr(peaks), _addr(n_peaks), _addr(workspace),
                                    int(workspace_bytes), _stream(stream)))
+
+
+def ld_hough_peaks_nms_workspace_bytes(batch, n_theta, n_rho) -> int:
+    return int(lib().ld_hough_peaks_nms_workspace_bytes(batch, n_theta, n_rho))
+
+
+def ld_hough_peaks_nms(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, ratio_num,
+                       ratio_den, k, peaks, n_peaks, workspace, workspace_bytes, stream=None):
+    _check(lib().ld_hough_peaks_nms(_addr(acc), int(batch), int(n_theta), int(n_rho),
+                                    int(half_theta), int(half_rho), int(min_votes),
+                                    int(ratio_num), int(ratio_den), int(k), _addr(peaks),
+                                    _addr(n_peaks), _addr(workspace), int(workspace_bytes),
+                                    _stream(stream)))
+
+
+def ld_peak_lines(peaks, n_peaks, batch, k, width, height, n_theta, cos_q15, sin_q15, lines,
+                  hit, stream=None):
+    c, s = _host_i32(cos_q15), _host_i32(sin_q15)
+    _check(lib().ld_peak_lines(_addr(peaks), _addr(n_peaks), int(batch), int(k), int(width),
+                               int(height), int(n_theta), _addr(c), _addr(s), _addr(lines),
+                               _addr(hit), _stream(stream)))
+
+
+def ld_extract_segments(binary, img: ld_image, peaks, n_peaks, k, n_theta, cos_q15, sin_q15,
+                        fill_gap, min_len, max_segments, segments, n_segments, stream=None):
+    c, s = _host_i32(cos_q15), _host_i32(sin_q15)
+    _check(lib().ld_extract_segments(_addr(binary), ctypes.byref(img), _addr(peaks),
+                                     _addr(n_peaks), int(k), int(n_theta), _addr(c), _addr(s),
+                                     int(fill_gap), int(min_len), int(max_segments),
+                                     _addr(segments), _addr(n_segments), _stream(stream)))
 
 
 def ld_detect_workspace_bytes(img: ld_image, n_theta, k, acc_in_workspace) -> int:
@@ -443,3 +481,47 @@ class HostDetector:
                              self.peaks, self.n_peaks, self.counts, self.chunk, self.ws,
                              self.ws_bytes, stream)
         return self.peaks, self.n_peaks, self.counts
+
+
+# ----------------------------------------------------------------------------
+# lanes module (NEXT 3) convenience wrappers
+# ----------------------------------------------------------------------------
+def hough_peaks_nms(acc, half_theta, half_rho, min_votes, k, ratio=(0, 1), stream=None):
+    """Greedy NMS (ld_hough_peaks_nms); ratio = (num, den): votes >= num/den * max."""
+    import torch
+    b, n_theta, n_rho = acc.shape
+    wsb = ld_hough_peaks_nms_workspace_bytes(b, n_theta, n_rho)
+    ws = torch.empty((wsb,), dtype=torch.uint8, device=acc.device)
+    peaks = torch.empty((b, k, 3), dtype=torch.int32, device=acc.device)
+    n_peaks = torch.empty((b,), dtype=torch.int32, device=acc.device)
+    ld_hough_peaks_nms(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, ratio[0],
+                       ratio[1], k, peaks, n_peaks, ws, wsb, stream)
+    return peaks, n_peaks
+
+
+def peak_lines(peaks, n_peaks, width, height, cos_q15, sin_q15, stream=None):
+    """Returns (lines int32 [B][k][4], hit int32 [B][k])."""
+    import torch
+    b, k, _ = peaks.shape
+    lines = torch.zeros((b, k, 4), dtype=torch.int32, device=peaks.device)
+    hit = torch.empty((b, k), dtype=torch.int32, device=peaks.device)
+    ld_peak_lines(peaks, n_peaks, b, k, width, height, len(cos_q15), cos_q15, sin_q15, lines, hit,
+                  stream)
+    return lines, hit
+
+
+def extract_segments(binary, peaks, n_peaks, cos_q15, sin_q15, fill_gap=20, min_len=40,
+                     max_segments=64, width=None, stream=None):
+    """binary: contiguous uint8 CUDA [B][H][pitch] (pitch >= width; width
+    defaults to pitch).  Returns (segments int32 [B][k][max_segments][4],
+    n_segments int32 [B][k])."""
+    import torch
+    b, h, pitch = binary.shape
+    k = peaks.shape[1]
+    width = pitch if width is None else width
+    img = make_image(width, h, pitch, h * pitch, b)
+    segs = torch.zeros((b, k, max_segments, 4), dtype=torch.int32, device=binary.device)
+    nseg = torch.empty((b, k), dtype=torch.int32, device=binary.device)
+    ld_extract_segments(binary, img, peaks, n_peaks, k, len(cos_q15), cos_q15, sin_q15, fill_gap,
+                        min_len, max_segments, segs, nseg, stream)
+    return segs, nseg

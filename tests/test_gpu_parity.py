@@ -716,3 +716,114 @@ def test_hint_header_mismatch_ignored(ld, oracle):
     with pytest.raises(ld.LdError):  # too small a hint buffer
         ld.ld_hough_accumulate_hint(edges, counts, stride, 1, 1280, 720, cfg.n_theta, c, s, acc,
                                     hint, 64)
+
+
+# ----------------------------------------------------------------------------
+# Lanes module (NEXT 3, DESIGN R26-R28): greedy NMS, peak_to_line,
+# extract_segments against the oracle
+# ----------------------------------------------------------------------------
+def _np_peaks(p, n):
+    return [tuple(int(v) for v in q) for q in np.asarray(p)[:n]]
+
+
+@pytest.mark.parametrize("ratio", [(0, 1), (1, 2), (3, 4), (5, 4)])
+def test_nms_random_accumulators(ld, oracle, ratio):
+    rng = np.random.default_rng(31)
+    for trial in range(12):
+        b = int(rng.integers(1, 4))
+        nt, nr = int(rng.integers(1, 50)), int(rng.integers(1, 400))
+        acc = rng.integers(0, int(rng.integers(1, 12)), size=(b, nt, nr)).astype(np.uint32)
+        ht, hr = int(rng.integers(0, 4)), int(rng.integers(0, 20))
+        mv, k = int(rng.integers(0, 4)), int(rng.choice([1, 2, 4, 9]))
+        pk, npk = ld.hough_peaks_nms(cuda(acc.view(np.int32)), ht, hr, mv, k, ratio=ratio)
+        torch.cuda.synchronize()
+        pk, npk = pk.cpu().numpy(), npk.cpu().numpy()
+        for f in range(b):
+            want, wn = oracle.hough_peaks_nms(acc[f], ht, hr, mv, ratio[0], ratio[1], k)
+            assert npk[f] == wn, (trial, f)
+            assert peak_tuples(pk[f]) == oracle_peak_tuples(want), (trial, f)
+
+
+def test_nms_on_detected_frames(ld, oracle):
+    cfg = synth.CONFIGS["cfg3"]
+    c, s = synth.q15_table(cfg.n_theta)
+    frames = synth.gen_batch("cfg3", 0, 3)
+    _, edges, counts, stride = ld.sobel_binarize(cuda(frames), cfg.threshold, want_binary=False)
+    acc = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s)
+    pk, npk = ld.hough_peaks_nms(acc, 5, 40, 1, 8, ratio=(1, 2))
+    torch.cuda.synchronize()
+    A = acc.cpu().numpy().view(np.uint32)
+    for f in range(3):
+        want, wn = oracle.hough_peaks_nms(A[f], 5, 40, 1, 1, 2, 8)
+        assert int(npk[f]) == wn and peak_tuples(pk[f].cpu()) == oracle_peak_tuples(want)
+
+
+def test_peak_lines_match_oracle(ld, oracle):
+    rng = np.random.default_rng(32)
+    for n_theta in (180, 720, 1024):
+        c, s = synth.q15_table(n_theta)
+        for (w, h) in [(512, 512), (1280, 720), (37, 900), (2, 2)]:
+            d = oracle.rho_offset(w, h)
+            k = 64
+            pk = np.zeros((1, k, 3), np.int32)
+            pk[0, :, 0] = rng.integers(0, n_theta, k)
+            pk[0, :, 1] = rng.integers(0, 2 * d + 1, k)
+            pk[0, :, 2] = 1
+            pk[0, :4, 0] = [0, n_theta // 2, n_theta // 4, 0]  # the axis-aligned and 45-degree cases
+            pk[0, :4, 1] = [d + 100 % max(w, 1), d + 3, d, d]
+            npk = np.array([k - 3], np.int32)  # the last 3 slots are not peaks
+            lines, hit = ld.peak_lines(cuda(pk), cuda(npk), w, h, c, s)
+            torch.cuda.synchronize()
+            lines, hit = lines.cpu().numpy(), hit.cpu().numpy()
+            for i in range(k):
+                want = oracle.peak_to_line(tuple(pk[0, i]), w, h, c, s) if i < k - 3 else None
+                assert (hit[0, i] == 1) == (want is not None), (n_theta, w, h, i)
+                if want is not None:
+                    assert tuple(int(v) for v in lines[0, i]) == want, (n_theta, w, h, i)
+
+
+def test_extract_segments_match_oracle(ld, oracle):
+    cfg = synth.CONFIGS["cfg3"]
+    c, s = synth.q15_table(cfg.n_theta)
+    frames = synth.gen_batch("cfg3", 0, 2)
+    binary, edges, counts, stride = ld.sobel_binarize(cuda(frames), cfg.threshold)
+    acc = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s)
+    pk, npk = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, 1, 16)
+    bpitch = binary.contiguous()
+    for fill_gap, min_len in [(20, 40), (0, 0), (5, 100)]:
+        segs, nseg = ld.extract_segments(bpitch, pk, npk, c, s, fill_gap, min_len,
+                                         max_segments=32)
+        torch.cuda.synchronize()
+        segs, nseg = segs.cpu().numpy(), nseg.cpu().numpy()
+        B = bpitch.cpu().numpy()
+        P, N = pk.cpu().numpy(), npk.cpu().numpy()
+        for f in range(2):
+            for i in range(16):
+                if i >= N[f]:
+                    assert nseg[f, i] == 0
+                    continue
+                want, wn = oracle.extract_segments(B[f], tuple(P[f, i]), c, s, fill_gap, min_len,
+                                                   cap=32)
+                assert nseg[f, i] == wn, (fill_gap, min_len, f, i)
+                got = [tuple(int(v) for v in segs[f, i, j]) for j in range(min(wn, 32))]
+                assert got == want, (fill_gap, min_len, f, i)
+
+
+def test_extract_segments_vertical_and_synthetic(ld, oracle):
+    c, s = synth.q15_table(180)
+    b = np.zeros((1, 90, 128), np.uint8)
+    b[0, 0:30, 30] = 255
+    b[0, 56:90, 30] = 255
+    b[0, 45, :] = 255
+    b[0, 45, 60:75] = 0
+    d = oracle.rho_offset(128, 90)
+    pk = np.array([[[0, d + 30, 1], [90, d + 45, 1], [45, d + 50, 1]]], np.int32)
+    npk = np.array([3], np.int32)
+    for fg, ml in [(25, 20), (26, 20), (14, 10), (15, 0)]:
+        segs, nseg = ld.extract_segments(cuda(b), cuda(pk), cuda(npk), c, s, fg, ml, 8)
+        torch.cuda.synchronize()
+        segs, nseg = segs.cpu().numpy(), nseg.cpu().numpy()
+        for i in range(3):
+            want, wn = oracle.extract_segments(b[0], tuple(pk[0, i]), c, s, fg, ml, cap=8)
+            assert nseg[0, i] == wn
+            assert [tuple(int(v) for v in segs[0, i, j]) for j in range(min(wn, 8))] == want
