@@ -438,14 +438,26 @@ def run_banded(args, rank, world, local):
         else:
             det.count.zero_()
         mark(1)
-        ld.ld_hough_accumulate(det.edges, det.count, det.edge_stride, 1, W, H, cfg.n_theta, c, s,
-                               det.acc, stream)
+        if det.hint is not None:  # one rank: the whole accumulator, the hint is valid
+            ld.ld_hough_accumulate_hint(det.edges, det.count, det.edge_stride, 1, W, H,
+                                        cfg.n_theta, c, s, det.acc, det.hint, det.hint_bytes,
+                                        stream)
+        else:
+            ld.ld_hough_accumulate(det.edges, det.count, det.edge_stride, 1, W, H, cfg.n_theta,
+                                   c, s, det.acc, stream)
         launches[0] += ld.ld_last_launch_count()
         mark(2)
         pdist.allreduce_accumulator(det.acc)
         mark(3)
-        ld.ld_hough_peaks(det.acc, 1, cfg.n_theta, det.n_rho, cfg.half_theta, cfg.half_rho,
-                          cfg.min_votes, cfg.k, det.peaks, det.n_peaks, det.ws, det.ws_bytes, stream)
+        if det.hint is not None:
+            ld.ld_hough_peaks_hinted(det.acc, 1, cfg.n_theta, det.n_rho, cfg.half_theta,
+                                     cfg.half_rho, cfg.min_votes, cfg.k, det.hint,
+                                     det.hint_bytes, det.peaks, det.n_peaks, det.ws, det.ws_bytes,
+                                     stream)
+        else:
+            ld.ld_hough_peaks(det.acc, 1, cfg.n_theta, det.n_rho, cfg.half_theta, cfg.half_rho,
+                              cfg.min_votes, cfg.k, det.peaks, det.n_peaks, det.ws, det.ws_bytes,
+                              stream)
         launches[0] += ld.ld_last_launch_count()
         mark(4)
 

@@ -77,7 +77,7 @@ struct HoughParams {
 // 0...} then the range-maximum keys (one range per warp of the voting CTA).
 constexpr uint32_t HINT_MAGIC = 0x3148444Cu;  // "LDH1"
 constexpr int HINT_HDR_BYTES = 64;
-constexpr int HINT_MAX_KEYS = 4096;  // per frame, what the verifying kernel sorts
+constexpr int HINT_MAX_KEYS = 1024;  // per frame, what the verifying kernel sorts (more are merged)
 constexpr int HINT_MAX_RANGES = 32;  // ranges per band (warps of a 1024-thread CTA)
 
 constexpr int HV_THREADS = 1024;  // threads per SM; a CTA has HV_THREADS / CTAS of them

@@ -158,19 +158,39 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
 // ---------------------------------------------------------------------------
 // Peak hint (DESIGN R25): one CTA per frame turns the range maxima recorded by
 // the voting kernel into the per-frame starting threshold gtau[f].  The keys
-// are sorted (largest count first, lowest index among equals), then checked
-// eight at a time (one warp each) against the full candidate definition on
-// acc: every count in the clipped window is <= v, and an equal count has a
-// higher (theta, rho) index.  Verified cells are distinct candidates, so the
-// value of the k-th verified key in sorted order bounds the frame's k-th best
-// candidate from below; with fewer than k verified the bound is 0 (no hint).
+// (count << 32 | ~cell) are taken largest first -- each warp sorts 32-key
+// chunks with shuffles, then warp 0 merges the chunk heads PH_M keys at a
+// time -- and each batch of PH_M is checked (one warp per key) against the
+// full candidate definition on acc: every count in the clipped window is
+// <= v, and an equal count has a higher (theta, rho) index.  Verified cells
+// are distinct candidates, so the value of the k-th verified key in this
+// order bounds the frame's k-th best candidate from below; with fewer than k
+// verified the bound is 0 (no hint).
 // ---------------------------------------------------------------------------
 constexpr int PH_THREADS = 512;
-constexpr int PH_UNROLL = 8;
+constexpr int PH_WARPS = PH_THREADS / 32;
+constexpr int PH_UNROLL = 16;
+constexpr int PH_M = 32;  // keys per merge/verify round
+static_assert(HINT_MAX_KEYS <= 32 * 32, "warp 0 merges at most 32 chunks of 32");
+
+__device__ __forceinline__ u64 warp_sort32_desc(u64 key, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const u64 other = __shfl_xor_sync(0xffffffffu, key, j);
+      const bool desc = (lane & k) == 0, lower = (lane & j) == 0;
+      const u64 hi = other > key ? other : key, lo = other > key ? key : other;
+      key = (desc == lower) ? hi : lo;
+    }
+  }
+  return key;
+}
 
 __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParams p) {
   __shared__ u64 keys[HINT_MAX_KEYS];
-  __shared__ int s_ok[PH_THREADS / 32];
+  __shared__ u64 top[PH_M];
+  __shared__ int s_ok[PH_M];
   __shared__ uint32_t s_bound;
   __shared__ int s_done;
   const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -184,42 +204,59 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
     if (tid == 0) p.gtau[f] = 0u;
     return;
   }
-  // more keys than the sort holds: merge g consecutive ranges (the maximum of
-  // a union of ranges is again a range maximum)
+  // more keys than the merge holds: combine g consecutive ranges (the
+  // maximum of a union of ranges is again a range maximum)
   const int g = (n_src + HINT_MAX_KEYS - 1) / HINT_MAX_KEYS;
   const int n = (n_src + g - 1) / g;
-  int np2 = 1;
-  while (np2 < n) np2 <<= 1;
+  const int chunks = (n + 31) >> 5;
   const u64 *src = p.hint_keys + static_cast<int64_t>(f) * n_src;
-  for (int i = tid; i < np2; i += PH_THREADS) {
+  for (int c = warp; c < chunks; c += PH_WARPS) {
+    const int i = c * 32 + lane;
     u64 m = 0ull;
-    for (int j = i * g; j < min(i * g + g, n_src) && i < n; ++j) m = src[j] > m ? src[j] : m;
-    keys[i] = m;
+    if (i < n)
+      for (int j = i * g; j < min(i * g + g, n_src); ++j) m = src[j] > m ? src[j] : m;
+    keys[i] = warp_sort32_desc(m, lane);
   }
   if (tid == 0) {
     s_bound = 0u;
     s_done = 0;
   }
   __syncthreads();
-  bitonic_desc(keys, np2);
   const uint32_t *A = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
   const int ht = p.half_theta, hr = p.half_rho;
-  int found = 0;  // thread 0's count of verified keys
-  for (int base = 0; base < n; base += PH_THREADS / 32) {
-    const int j = base + warp;
-    int ok = 0;
-    if (j < n) {
-      const u64 key = keys[j];
+  int ptr = 0;    // warp 0, lane l: position of chunk l's head
+  u64 head = (warp == 0 && lane < chunks) ? keys[lane * 32] : 0ull;
+  int found = 0;  // thread 0: verified keys so far
+  for (;;) {
+    if (warp == 0) {  // the next PH_M keys, largest first
+      for (int m = 0; m < PH_M; ++m) {
+        u64 best = head;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
+          best = other > best ? other : best;
+        }
+        if (lane == 0) top[m] = best;
+        if (best != 0ull && head == best) {  // keys are distinct: one winner
+          ++ptr;
+          head = ptr < 32 ? keys[lane * 32 + ptr] : 0ull;
+        }
+      }
+    }
+    __syncthreads();
+    for (int j = warp; j < PH_M; j += PH_WARPS) {
+      const u64 key = top[j];
       const uint32_t v = static_cast<uint32_t>(key >> 32);
       const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
-      if (v >= p.floor_votes) {
+      int ok = -1;  // below the floor (or exhausted): this and every later key end the search
+      if (key != 0ull && v >= p.floor_votes) {
         const int t = static_cast<int>(idx / static_cast<uint32_t>(p.n_rho));
         const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * p.n_rho);
         const int ta = max(t - ht, 0), tb = min(t + ht, p.n_theta - 1);
         const int ra = max(r - hr, 0), rb = min(r + hr, p.n_rho - 1);
         // the clipped window as one flat range of cells, 32 x PH_UNROLL per
         // warp step: the loads of a step are independent (no early exit
-        // between them), so a small window costs one or two round trips
+        // between them), so a small window costs one round trip
         const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
         bool bad = false;
         for (int c0 = 0; c0 < cells && !__any_sync(0xffffffffu, bad); c0 += 32 * PH_UNROLL) {
@@ -236,20 +273,18 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
             bad = bad || w[u] > v || (w[u] == v && ci[u] < idx);
         }
         ok = !__any_sync(0xffffffffu, bad);
-      } else {
-        ok = -1;  // below the floor: this and every later key end the search
       }
+      if (lane == 0) s_ok[j] = ok;
     }
-    if (lane == 0) s_ok[warp] = ok;
     __syncthreads();
     if (tid == 0) {
-      for (int w = 0; w < PH_THREADS / 32 && base + w < n; ++w) {
-        if (s_ok[w] < 0) {
+      for (int j = 0; j < PH_M; ++j) {
+        if (s_ok[j] < 0) {
           s_done = 1;
           break;
         }
-        if (s_ok[w] && ++found == p.k) {
-          s_bound = static_cast<uint32_t>(keys[base + w] >> 32);
+        if (s_ok[j] && ++found == p.k) {
+          s_bound = static_cast<uint32_t>(top[j] >> 32);
           s_done = 1;
           break;
         }
@@ -862,9 +897,6 @@ static bool peaks_stream_plan(int batch, int n_theta, int n_rho, int half_theta,
 // resolved exactly from the frame.
 // ---------------------------------------------------------------------------
 constexpr int PW_CPT = 8, PW_G = 2, PW_W = 8, PW_COLS = 32 * PW_CPT, PW_KMAX = 64, PW_CBUF = 128;
-#ifndef LD_PW_POLL_EVERY_GROUP
-#define LD_PW_POLL_EVERY_GROUP 1
-#endif
 
 struct PwSmem {
   uint32_t CM[PW_G][PW_COLS];  // column maxima of the group's rows (when a survivor exists)
@@ -1016,6 +1048,8 @@ __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksPar
   int ntop = 0;                  // warp-uniform
   uint32_t tau = p.floor_votes;  // warp-uniform
   uint32_t gt_next = 0;          // lane 0: per-frame threshold read last group
+  const bool hinted = p.hint_hdr != nullptr && p.cand_t0 == 0 && p.cand_t1 == n_theta &&
+                      p.theta_offset == 0;
   if (lane == 0) gt_next = ld_relaxed_u32(p.gtau + f);  // first poll, before the row loads
   uint32_t ring[R][PW_CPT];
 #pragma unroll
@@ -1031,7 +1065,11 @@ __global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksPar
 #pragma unroll
         for (int k = 0; k < PW_G; ++k) load_row(RG(NV + k));
       }
-      if (LD_PW_POLL_EVERY_GROUP || u == 0) {
+      // poll every group when the threshold must be learned, once per ring
+      // period when the peak hint already started it near the k-th best
+      // (measured: tools/exp_tau_oracle.py, 0.30 vs 0.36 ms unhinted, 0.16 vs
+      // 0.15 ms from the true k-th value)
+      if (!hinted || u == 0) {
         // the threshold read one poll ago has arrived; read the next one
         const uint32_t gt = gt_next;
         if (lane == 0) gt_next = ld_relaxed_u32(p.gtau + f);
@@ -1220,13 +1258,19 @@ static bool g_warp_attr[64][4];
 
 // Per-frame starting thresholds of the streaming kernels: the verified peak
 // hint when one is given for an unrestricted search, else 0.
-static cudaError_t init_gtau(const PeaksParams &p, bool restricted, cudaStream_t stream) {
+// (p.hint_hdr is cleared when the hint is not used, which the warp kernel reads)
+static cudaError_t init_gtau(PeaksParams &p, bool restricted, cudaStream_t stream) {
   if (getenv("LD_PEAKS_GTAU_KEEP")) return cudaSuccess;  // experiments (tools/exp_tau_oracle.py)
-  if (p.hint_hdr && !restricted) {
+  // the hint pays when its verification is cheap next to the search it
+  // shortens: a window of at most 64 K cells in total over k keys
+  const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
+  if (p.hint_hdr && !restricted && wcells * p.k <= 65536) {
     peaks_hint_kernel<<<p.batch, PH_THREADS, 0, stream>>>(p);
     note_launch();
     return cudaGetLastError();
   }
+  p.hint_hdr = nullptr;
+  p.hint_keys = nullptr;
   return cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
 }
 

@@ -116,6 +116,11 @@ class BandedDetector:
         self.ws = torch.empty((max(self.ws_bytes, 16),), dtype=torch.uint8, device=self.device)
         self.peaks = torch.empty((1, k, 3), dtype=torch.int32, device=self.device)
         self.n_peaks = torch.empty((1,), dtype=torch.int32, device=self.device)
+        # one rank holds the whole accumulator: the peak hint (DESIGN R25) is
+        # valid; with several ranks the band partials are summed afterwards
+        self.hint_bytes = ld.ld_hough_hint_bytes(1, width, height, n_theta) if world == 1 else 0
+        self.hint = (torch.empty((self.hint_bytes,), dtype=torch.uint8, device=self.device)
+                     if self.hint_bytes else None)
         self.launches = 0
 
     def load(self, gray_full):
@@ -145,13 +150,24 @@ class BandedDetector:
             self.launches += ld.ld_last_launch_count()
         else:
             self.count.zero_()
-        ld.ld_hough_accumulate(self.edges, self.count, self.edge_stride, 1, self.w, self.h,
-                               self.n_theta, self.cos, self.sin, self.acc, stream)
+        if self.hint is not None:
+            ld.ld_hough_accumulate_hint(self.edges, self.count, self.edge_stride, 1, self.w,
+                                        self.h, self.n_theta, self.cos, self.sin, self.acc,
+                                        self.hint, self.hint_bytes, stream)
+        else:
+            ld.ld_hough_accumulate(self.edges, self.count, self.edge_stride, 1, self.w, self.h,
+                                   self.n_theta, self.cos, self.sin, self.acc, stream)
         self.launches += ld.ld_last_launch_count()
         allreduce_accumulator(self.acc, self.group)
-        ld.ld_hough_peaks(self.acc, 1, self.n_theta, self.n_rho, self.half_theta, self.half_rho,
-                          self.min_votes, self.k, self.peaks, self.n_peaks, self.ws, self.ws_bytes,
-                          stream)
+        if self.hint is not None:
+            ld.ld_hough_peaks_hinted(self.acc, 1, self.n_theta, self.n_rho, self.half_theta,
+                                     self.half_rho, self.min_votes, self.k, self.hint,
+                                     self.hint_bytes, self.peaks, self.n_peaks, self.ws,
+                                     self.ws_bytes, stream)
+        else:
+            ld.ld_hough_peaks(self.acc, 1, self.n_theta, self.n_rho, self.half_theta,
+                              self.half_rho, self.min_votes, self.k, self.peaks, self.n_peaks,
+                              self.ws, self.ws_bytes, stream)
         self.launches += ld.ld_last_launch_count()
         return self.peaks, self.n_peaks, self.acc, self.count
 
