@@ -27,8 +27,11 @@ namespace ld {
 // One block of 32 x EPL consecutive list entries of a warp (entry
 // blk + 32j + lane in lane `lane`), voted into every row of the band.
 template <int EPL, bool FULL>
+// Entries past `end` (FULL = false) vote into the scratch word instead of
+// being branched around: no divergent control flow in the tail.
 __device__ __forceinline__ void vote_block(const uint32_t *el, uint32_t blk, uint32_t end,
-                                           int lane, int nr, const uint4 *rowk) {
+                                           int lane, int nr, const uint4 *rowk,
+                                           uint32_t scratch) {
   uint32_t xs[EPL], ys[EPL];
   bool ok[EPL];
 #pragma unroll
@@ -45,7 +48,10 @@ __device__ __forceinline__ void vote_block(const uint32_t *el, uint32_t blk, uin
     const uint4 k = rowk[r];
 #pragma unroll
     for (int j = 0; j < EPL; ++j)
-      if (FULL || ok[j]) red_shared_add(((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u, 1u);
+    {
+      const uint32_t a = ((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u;
+      red_shared_add(FULL || ok[j] ? a : scratch, 1u);
+    }
   }
 }
 
@@ -98,12 +104,13 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = NT / 32;
   uint32_t base = 0;
+  const uint32_t scratch = smem_u32(slice + ncell);  // inside the allocation, never written out
   for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
-    vote_block<16, true>(el, base + warp * 32u * 16u, n_edges, lane, nr, rowk);
+    vote_block<16, true>(el, base + warp * 32u * 16u, n_edges, lane, nr, rowk, scratch);
   uint32_t blk = base + static_cast<uint32_t>(warp) * (32u * 8u);
   for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
-    vote_block<8, true>(el, blk, n_edges, lane, nr, rowk);
-  if (blk < n_edges) vote_block<8, false>(el, blk, n_edges, lane, nr, rowk);
+    vote_block<8, true>(el, blk, n_edges, lane, nr, rowk, scratch);
+  if (blk < n_edges) vote_block<8, false>(el, blk, n_edges, lane, nr, rowk, scratch);
   __syncthreads();
 
   // write-out: unaligned head and tail words by threads, the aligned middle
@@ -255,7 +262,7 @@ int hough_pair_count(int n_theta) { return n_theta / 2 + 1; }
 template <int EPL, bool FULL>
 __device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t blk, uint32_t end,
                                                  int lane, int np, const uint4 *rowk,
-                                                 uint32_t delta) {
+                                                 uint32_t delta, uint32_t scratch) {
   uint32_t xs[EPL], ys[EPL];
   bool ok[EPL];
 #pragma unroll
@@ -271,11 +278,13 @@ __device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t bl
     const uint4 k = rowk[r];  // C, S, K, -C
 #pragma unroll
     for (int j = 0; j < EPL; ++j)
-      if (FULL || ok[j]) {
-        const uint32_t q = ys[j] * k.y + k.z;
-        red_shared_add(((xs[j] * k.x + q) >> 13) & ~3u, 1u);
-        red_shared_add((((xs[j] * k.w + q) >> 13) & ~3u) + delta, 1u);
-      }
+    {
+      const uint32_t q = ys[j] * k.y + k.z;
+      const uint32_t a1 = ((xs[j] * k.x + q) >> 13) & ~3u;
+      const uint32_t a2 = ((xs[j] * k.w + q) >> 13) & ~3u;
+      red_shared_add(FULL || ok[j] ? a1 : scratch, 1u);
+      red_shared_add((FULL || ok[j] ? a2 : scratch - delta) + delta, 1u);
+    }
   }
 }
 
@@ -318,13 +327,17 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
 
   const uint32_t n_edges = p.counts[f];
   const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
+  // scratch word past the partner half (>= the partner offset): inside the
+  // allocation, never written out
+  const uint32_t scratch = smem_u32(slice + half + ncell);
   uint32_t base = 0;
   for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
-    vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, delta);
+    vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, delta,
+                               scratch);
   uint32_t blk = base + static_cast<uint32_t>(warp) * (32u * 8u);
   for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
-    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, delta);
-  if (blk < n_edges) vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, delta);
+    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, delta, scratch);
+  if (blk < n_edges) vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, delta, scratch);
   __syncthreads();
 
   // write-out, first half: rows p0 .. p0+np-1 are consecutive in acc -- one
