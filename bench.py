@@ -177,6 +177,16 @@ def run_reference(args, rank, world):
 # ----------------------------------------------------------------------------
 # roofline denominators
 # ----------------------------------------------------------------------------
+def vote_kernel_name(c, s):
+    """Which voting kernel libld.so picks for this table (label only): the
+    half-angle paired kernel for a symmetric table (C[n-t] = -C[t],
+    S[n-t] = S[t]) unless LD_VOTE_PAIRED=0."""
+    n = len(c)
+    sym = all(c[n - t] == -c[t] and s[n - t] == s[t] for t in range(1, n) if 2 * t != n)
+    return ("hough_vote_pairs_kernel" if sym and os.environ.get("LD_VOTE_PAIRED") != "0"
+            else "hough_vote_kernel")
+
+
 def smem_atomic_peaks():
     """B5 microbenchmark (conflict-free / random / same-address red.shared.add.u32
     on all SMs), measured in this run: Gatomic/s."""
@@ -364,7 +374,7 @@ def run_ours(args, rank, world, local):
     sobel_bytes = B * (W * H + 4) + 4 * int(cnt.sum())
     vote_rate = votes / (vote_ms / 1e3) / 1e9
     peaks_bytes = B * cfg.n_theta * n_rho * 4
-    roofline = {"kernel": "hough_vote_kernel", "bound": "smem_atomic",
+    roofline = {"kernel": vote_kernel_name(c, s), "bound": "smem_atomic",
                 "achieved": vote_rate, "peak": atom["conflict_free"], "unit": "Gatomic/s",
                 "frac": vote_rate / atom["conflict_free"], "traffic": None,
                 "peak_source": "B5 microbenchmark (conflict-free red.shared.add.u32, all SMs), "
@@ -547,7 +557,7 @@ def run_banded(args, rank, world, local):
         "edges_total": edges_total,
         "stages_ms": {"sobel_binarize_compact": sob_ms, "hough_vote": vote_ms,
                       "allreduce": ar_ms, "hough_peaks": peak_ms},
-        "roofline": {"kernel": "hough_vote_kernel", "bound": "smem_atomic", "achieved": vote_rate,
+        "roofline": {"kernel": vote_kernel_name(c, s), "bound": "smem_atomic", "achieved": vote_rate,
                      "peak": atom["conflict_free"], "unit": "Gatomic/s",
                      "frac": vote_rate / atom["conflict_free"], "traffic": None,
                      "peak_source": "B5 microbenchmark measured in this run"},
@@ -668,7 +678,7 @@ def run_theta(args, rank, world, local):
         "edges_total": edges_total,
         "stages_ms": {"sobel_binarize_compact": sob_ms, "edge_allgather": xch_ms,
                       "hough_vote": vote_ms, "hough_peaks": peak_ms, "topk_merge": merge_ms},
-        "roofline": {"kernel": "hough_vote_kernel", "bound": "smem_atomic", "achieved": vote_rate,
+        "roofline": {"kernel": vote_kernel_name(det.cos_s, det.sin_s), "bound": "smem_atomic", "achieved": vote_rate,
                      "peak": atom["conflict_free"], "unit": "Gatomic/s",
                      "frac": vote_rate / atom["conflict_free"], "traffic": None,
                      "peak_source": "B5 microbenchmark measured in this run"},
