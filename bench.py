@@ -10,6 +10,13 @@ ld_sobel_binarize (fused Sobel + binarize + compaction) -> ld_hough_accumulate
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+Steps go round-robin to ``--streams`` streams (default 2), each with its own
+output buffers, as a serving pipeline double-buffers batches: one step's peak
+search (memory-latency-bound) overlaps the next step's Sobel (issue-bound).
+The headline is K such steps from a common start event to the join;
+per-kernel times (and the roofline) come from the same K steps serialised on
+one stream, reported next to it (``config.ms_per_step_one_stream``).
+
 N > 1 is launched by torchrun (one process per GPU, NCCL): frames shard across
 ranks with no data-path collective (weak scaling: 256 frames per rank); timing
 is the max over ranks.  ``--impl reference`` times the CPU oracle (the only
@@ -49,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="streams (each with its own buffers) the steps go to round-robin")
     ap.add_argument("--no-hint", action="store_true",
                     help="plain ld_hough_accumulate + ld_hough_peaks (no peak hint)")
     ap.add_argument("--shard", default="band", choices=["band", "theta"],
@@ -253,78 +262,110 @@ def run_ours(args, rank, world, local):
     n_rho = 2 * ld.ld_rho_offset(W, H) + 1
     img = ld.make_image(W, H, pitch, H * pitch, B)
     stride = ld._round_up(H * max(W - 2, 0), 4)
-    edges = torch.empty((B, stride), dtype=torch.int32, device="cuda")
-    counts = torch.empty((B,), dtype=torch.int32, device="cuda")
-    acc = torch.empty((B, cfg.n_theta, n_rho), dtype=torch.int32, device="cuda")
-    pws_bytes = ld.ld_hough_peaks_workspace_bytes(B, cfg.n_theta, n_rho, cfg.k)
-    pws = torch.empty((pws_bytes,), dtype=torch.uint8, device="cuda")
     use_hint = not args.no_hint
+    pws_bytes = ld.ld_hough_peaks_workspace_bytes(B, cfg.n_theta, n_rho, cfg.k)
     hint_bytes = ld.ld_hough_hint_bytes(B, W, H, cfg.n_theta)
-    hint = torch.empty((hint_bytes,), dtype=torch.uint8, device="cuda")
-    peaks = torch.empty((B, cfg.k, 3), dtype=torch.int32, device="cuda")
-    npk = torch.empty((B,), dtype=torch.int32, device="cuda")
 
+    class Buffers:
+        """One step's outputs and workspaces, and the stream its steps run on."""
+
+        def __init__(self, st):
+            self.stream = st
+            self.edges = torch.empty((B, stride), dtype=torch.int32, device="cuda")
+            self.counts = torch.empty((B,), dtype=torch.int32, device="cuda")
+            self.acc = torch.empty((B, cfg.n_theta, n_rho), dtype=torch.int32, device="cuda")
+            self.pws = torch.empty((pws_bytes,), dtype=torch.uint8, device="cuda")
+            self.hint = torch.empty((hint_bytes,), dtype=torch.uint8, device="cuda")
+            self.peaks = torch.empty((B, cfg.k, 3), dtype=torch.int32, device="cuda")
+            self.npk = torch.empty((B,), dtype=torch.int32, device="cuda")
+
+    # steps go round-robin to `--streams` streams with a buffer set each (a
+    # serving pipeline's double buffering): step i+1's Sobel can run while
+    # step i's peak search still streams its accumulators
+    bufs = [Buffers(stream if i == 0 else torch.cuda.Stream()) for i in range(args.streams)]
     launches = [0]
 
-    def step(ev=None):
+    def step(bf, ev=None):
+        st = bf.stream
         if ev is not None:
-            ev[0].record(stream)
-        ld.ld_sobel_binarize(gray, img, cfg.threshold, None, edges, stride, counts, stream)
+            ev[0].record(st)
+        ld.ld_sobel_binarize(gray, img, cfg.threshold, None, bf.edges, stride, bf.counts, st)
         launches[0] += ld.ld_last_launch_count()
         if ev is not None:
-            ev[1].record(stream)
+            ev[1].record(st)
         if use_hint:
-            ld.ld_hough_accumulate_hint(edges, counts, stride, B, W, H, cfg.n_theta, c, s, acc,
-                                        hint, hint_bytes, stream)
+            ld.ld_hough_accumulate_hint(bf.edges, bf.counts, stride, B, W, H, cfg.n_theta, c, s,
+                                        bf.acc, bf.hint, hint_bytes, st)
         else:
-            ld.ld_hough_accumulate(edges, counts, stride, B, W, H, cfg.n_theta, c, s, acc, stream)
+            ld.ld_hough_accumulate(bf.edges, bf.counts, stride, B, W, H, cfg.n_theta, c, s,
+                                   bf.acc, st)
         launches[0] += ld.ld_last_launch_count()
         if ev is not None:
-            ev[2].record(stream)
+            ev[2].record(st)
         if use_hint:
-            ld.ld_hough_peaks_hinted(acc, B, cfg.n_theta, n_rho, cfg.half_theta, cfg.half_rho,
-                                     cfg.min_votes, cfg.k, hint, hint_bytes, peaks, npk, pws,
-                                     pws_bytes, stream)
+            ld.ld_hough_peaks_hinted(bf.acc, B, cfg.n_theta, n_rho, cfg.half_theta, cfg.half_rho,
+                                     cfg.min_votes, cfg.k, bf.hint, hint_bytes, bf.peaks, bf.npk,
+                                     bf.pws, pws_bytes, st)
         else:
-            ld.ld_hough_peaks(acc, B, cfg.n_theta, n_rho, cfg.half_theta, cfg.half_rho,
-                              cfg.min_votes, cfg.k, peaks, npk, pws, pws_bytes, stream)
+            ld.ld_hough_peaks(bf.acc, B, cfg.n_theta, n_rho, cfg.half_theta, cfg.half_rho,
+                              cfg.min_votes, cfg.k, bf.peaks, bf.npk, bf.pws, pws_bytes, st)
         launches[0] += ld.ld_last_launch_count()
         if ev is not None:
-            ev[3].record(stream)
+            ev[3].record(st)
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(max(args.warmup, len(bufs))):
+        step(bufs[i % len(bufs)])
     torch.cuda.synchronize()
+    counts, acc, peaks = bufs[0].counts, bufs[0].acc, bufs[0].peaks
     cnt = counts.cpu().numpy().astype(np.int64)
     votes = int(cnt.sum()) * cfg.n_theta
     if args.profile:
-        for _ in range(args.steps):
-            step()
+        for i in range(args.steps):
+            step(bufs[0])
         torch.cuda.synchronize()
         if rank == 0:
             print(json.dumps({"profile_run": True, "votes": votes}), flush=True)
         return
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if sampler:
         sampler.start()
         time.sleep(0.3)
+    # (1) the headline: K steps back to back, round-robin over the streams,
+    # device-timed on the launching stream from a common start to the join
     launches[0] = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for bf in bufs[1:]:
+        bf.stream.wait_event(e_start)
     for i in range(args.steps):
-        step(evs[i])
+        step(bufs[i % len(bufs)])
+    for bf in bufs[1:]:
+        j = torch.cuda.Event()
+        j.record(bf.stream)
+        stream.wait_event(j)
+    e_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = sampler.stop() if sampler else None
     gpu_launches = launches[0]
-
+    elapsed_ms = float(e_start.elapsed_time(e_end))
+    # (2) per-kernel times: the same K steps serialised on one stream with
+    # CUDA events between the kernels (the roofline's launch durations)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        step(bufs[0], evs[i])
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
     stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(3)]
                       for i in range(args.steps)])  # ms
-    elapsed_ms = float(evs[0][0].elapsed_time(evs[-1][3]))
+    serial_ms = float(evs[0][0].elapsed_time(evs[-1][3])) / args.steps
+    for bf in bufs[1:]:  # every buffer set computed the same result
+        assert torch.equal(bf.peaks, peaks) and torch.equal(bf.npk, bufs[0].npk)
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -397,6 +438,8 @@ def run_ours(args, rank, world, local):
                    "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
                    "parallelism": "frame-shard dp%d" % world,
                    "peak_hint": use_hint,
+                   "streams": args.streams,
+                   "ms_per_step_one_stream": serial_ms,
                    "l2": "inputs %.0f MB + accumulators %.0f MB per GPU exceed L2 (%.0f MB); no flush"
                          % (B * H * pitch / 1e6, peaks_bytes / 1e6, ld.ld_device_l2_bytes() / 1e6)},
         "gvotes_per_s": total_votes / (ms_per_step / 1e3) / 1e9,
