@@ -1000,7 +1000,10 @@ __device__ __noinline__ PwState pw_survivors(PwSmem &S, uint32_t surv, int lane,
 }
 
 template <int HT>
-__global__ void __launch_bounds__(32 * PW_W, 2) peaks_warp_kernel(const PeaksParams p) {
+#ifndef LD_PW_MINB
+#define LD_PW_MINB 2
+#endif
+__global__ void __launch_bounds__(32 * PW_W, LD_PW_MINB) peaks_warp_kernel(const PeaksParams p) {
   extern __shared__ __align__(16) unsigned char psm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x * PW_W + warp, f = blockIdx.y;

@@ -384,15 +384,18 @@ static cudaError_t launch_cfg(const CUtensorMap &tmap, const SobelParams &p, int
 // (profiles/) against 3 stages (smaller staging), 3 CTAs per SM
 // (register-capped), 64- and 96-row tiles and direct (unstaged) edge stores:
 // all slower on cfg3 and cfg4.
-SobelCfg sobel_cfg() { return SobelCfg{8, 2, 2, SB_STAGE_CAP}; }
+#ifndef LD_SOBEL_SR
+#define LD_SOBEL_SR 8  // output rows per thread strip (tile height 16 * SR)
+#endif
+SobelCfg sobel_cfg() { return SobelCfg{LD_SOBEL_SR, 2, 2, SB_STAGE_CAP}; }
 
 cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_count,
                          cudaStream_t stream) {
   const SobelCfg c = sobel_cfg();
   const int64_t max_ctas = static_cast<int64_t>(sm_count) * c.ctas_per_sm;
   const int n_ctas = static_cast<int>(p.n_tiles < max_ctas ? p.n_tiles : max_ctas);
-  return p.binary != nullptr ? launch_cfg<8, 2, 2, true>(tmap, p, n_ctas, stream)
-                             : launch_cfg<8, 2, 2, false>(tmap, p, n_ctas, stream);
+  return p.binary != nullptr ? launch_cfg<LD_SOBEL_SR, 2, 2, true>(tmap, p, n_ctas, stream)
+                             : launch_cfg<LD_SOBEL_SR, 2, 2, false>(tmap, p, n_ctas, stream);
 }
 
 }  // namespace ld
