@@ -63,6 +63,7 @@ def lib():
         L.ldo_compact.argtypes = [P, i32, i32, P, i64, P]
         L.ldo_hough_accumulate.argtypes = [P, i64, i32, i32, i32, P, P, P]
         L.ldo_hough_peaks.argtypes = [P, i32, i32, i32, i32, u32, i32, P, P]
+        L.ldo_hough_accumulate_f64.argtypes = [P, i64, i32, i32, i32, P, P, P]
         L.ldo_hough_peaks_nms.argtypes = [P, i32, i32, i32, i32, u32, u32, u32, i32, P, P]
         L.ldo_peak_to_line.argtypes = [Peak, i32, i32, i32, P, P, P, P]
         L.ldo_extract_segments.argtypes = [P, i32, i32, i64, Peak, i32, P, P, i32, i32, P, i32,
@@ -246,3 +247,18 @@ def extract_segments(binary: np.ndarray, peak, cos_q15: np.ndarray, sin_q15: np.
                                       _ptr(s), fill_gap, min_len, _ptr(segs), cap,
                                       ctypes.byref(n)), "extract_segments")
     return [tuple(int(v) for v in segs[i]) for i in range(min(n.value, cap))], int(n.value)
+
+
+def hough_accumulate_f64(edges: np.ndarray, width: int, height: int, cos_f64: np.ndarray,
+                         sin_f64: np.ndarray) -> np.ndarray:
+    """SPEC float64 trig mode (ld_oracle.h, DESIGN R29)."""
+    e = np.ascontiguousarray(edges, dtype=np.uint32)
+    c = np.ascontiguousarray(cos_f64, dtype=np.float64)
+    s = np.ascontiguousarray(sin_f64, dtype=np.float64)
+    n_theta = c.shape[0]
+    n_rho = 2 * rho_offset(width, height) + 1
+    acc = np.empty((n_theta, n_rho), np.uint32)
+    _check(lib().ldo_hough_accumulate_f64(_ptr(e) if e.size else None, e.size, width, height,
+                                          n_theta, _ptr(c), _ptr(s), _ptr(acc)),
+           "hough_accumulate_f64")
+    return acc

@@ -422,3 +422,26 @@ int ldo_extract_segments(const uint8_t *binary, int32_t width, int32_t height,
   *n_segs = count;
   return LDO_OK;
 }
+
+int ldo_hough_accumulate_f64(const uint32_t *edges, int64_t n_edges, int32_t width,
+                             int32_t height, int32_t n_theta, const double *cos_f64,
+                             const double *sin_f64, uint32_t *acc) {
+  if ((!edges && n_edges > 0) || !cos_f64 || !sin_f64 || !acc || n_edges < 0 || width < 1 ||
+      height < 1 || n_theta < 1)
+    return LDO_EARG;
+  int32_t d = ldo_rho_offset(width, height);
+  int64_t n_rho = 2 * (int64_t)d + 1;
+  memset(acc, 0, sizeof(uint32_t) * (size_t)n_theta * (size_t)n_rho);
+  for (int64_t i = 0; i < n_edges; i++) {
+    double x = (double)(edges[i] & 0xFFFFu), y = (double)(edges[i] >> 16);
+    for (int32_t t = 0; t < n_theta; t++) {
+      double px = x * cos_f64[t];
+      double py = y * sin_f64[t];
+      double r = px + py;
+      int64_t rho = (int64_t)floor(r + 0.5) + d;
+      if (rho < 0 || rho >= n_rho) return LDO_ERANGE;
+      acc[(int64_t)t * n_rho + rho] += 1;
+    }
+  }
+  return LDO_OK;
+}

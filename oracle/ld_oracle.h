@@ -98,6 +98,17 @@ int ldo_hough_accumulate(const uint32_t *edges, int64_t n_edges, int32_t width,
                          int32_t height, int32_t n_theta, const int32_t *cos_q15,
                          const int32_t *sin_q15, uint32_t *acc);
 
+/* SPEC's float64 trig mode ("a second, non-bit-exact-
+ * vs-Q15 workload"; DESIGN R29): the same voting with the caller's
+ * double-precision table,
+ *   r   = x*cos[t] + y*sin[t]   (each product and the sum rounded once)
+ *   rho = floor(r + 0.5) + D    (S:224 quantize = round half up)
+ *   acc[t][rho] += 1.
+ * Returns LDO_ERANGE (acc undefined) if any rho leaves [0, n_rho). */
+int ldo_hough_accumulate_f64(const uint32_t *edges, int64_t n_edges, int32_t width,
+                             int32_t height, int32_t n_theta, const double *cos_f64,
+                             const double *sin_f64, uint32_t *acc);
+
 /* Hough peaks ("picking the line with the most pixel value"; P:185;
  * DESIGN R13, R14).  key(t, r) = (acc[t][r], -t, -r), compared
  * lexicographically.  (t, r) is a candidate iff

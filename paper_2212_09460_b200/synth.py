@@ -37,6 +37,25 @@ def q15_table(n_theta: int) -> tuple[np.ndarray, np.ndarray]:
     return c.astype(np.int32), s.astype(np.int32)
 
 
+def f64_table(n_theta: int) -> tuple[np.ndarray, np.ndarray]:
+    """SPEC's float64 trig table (build_trig_table mode float64):
+    cos/sin(pi t / n_theta) for t <= n_theta/2 with the exact values at 0 and
+    90 degrees (cos[n/2] = 0, sin[n/2] = 1), and for t > n_theta/2 the
+    Eq. 4-5 completion cos[t] = -cos[n-t], sin[t] = sin[n-t], exactly."""
+    if n_theta < 1:
+        raise ValueError("n_theta must be >= 1")
+    t = np.arange(n_theta, dtype=np.float64)
+    th = np.pi * t / n_theta
+    c, s = np.cos(th), np.sin(th)
+    c[0], s[0] = 1.0, 0.0
+    if n_theta % 2 == 0:
+        c[n_theta // 2], s[n_theta // 2] = 0.0, 1.0
+    for i in range(n_theta // 2 + 1, n_theta):
+        c[i] = -c[n_theta - i]
+        s[i] = s[n_theta - i]
+    return c, s
+
+
 # ----------------------------------------------------------------------------
 # Workload configurations (BASELINE.json configs[0..4]).
 # ----------------------------------------------------------------------------

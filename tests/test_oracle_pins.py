@@ -541,3 +541,70 @@ def test_extract_segments_gap_rule_and_vertical_walk(oracle):
     segs, n = oracle.extract_segments(b2, (90, oracle.rho_offset(200, 10) + 4, 1), c, s, 0, 0,
                                       cap=5)
     assert n == 67 and len(segs) == 5 and segs[0] == (0, 4, 0, 4)
+
+
+# ----------------------------------------------------------------------------
+# NEXT 4: SPEC float64 trig mode (DESIGN R29)
+# ----------------------------------------------------------------------------
+def test_f64_table_spec_pins():
+    c, s = synth.f64_table(180)
+    assert c[0] == 1.0 and s[0] == 0.0 and c[90] == 0.0 and s[90] == 1.0
+    assert s[179] == s[1] and c[179] == -c[1]                            # S:200, Eq. 4
+    assert np.all(np.abs(c * c + s * s - 1.0) <= 1e-12)
+    for n in (2, 8, 720, 1024):
+        c, s = synth.f64_table(n)
+        for k in range(1, n // 2):
+            assert s[n - k] == s[k] and c[n - k] == -c[k]
+
+
+def test_f64_rho_of_and_accumulate_spec_examples(oracle):
+    c, s = synth.f64_table(180)
+    w, h = 64, 48
+    d = oracle.rho_offset(w, h)
+
+    def rho_bins(x, y):
+        acc = oracle.hough_accumulate_f64(np.array([(y << 16) | x], np.uint32), w, h, c, s)
+        return [int(np.nonzero(acc[t])[0][0]) for t in range(180)]
+
+    assert all(r == d for r in rho_bins(0, 0))                 # S:229 origin
+    assert rho_bins(10, 33)[0] == d + 10                       # S:230 r = x at theta 0
+    assert rho_bins(21, 7)[90] == d + 7                        # S:231 r = y at 90 degrees
+    row = np.array([(5 << 16) | x for x in (3, 4, 5)], np.uint32)
+    acc = oracle.hough_accumulate_f64(row, w, h, c, s)
+    assert acc[90, d + 5] == 3 and acc.sum() == 3 * 180
+    assert oracle.hough_accumulate_f64(np.zeros(0, np.uint32), w, h, c, s).sum() == 0
+
+
+def test_f64_matches_exact_rational_away_from_ties(oracle):
+    # exact r = x*c + y*s over the rationals of the double table entries; the
+    # double evaluation may only differ where r + 1/2 is within 1e-9 of an integer
+    c, s = synth.f64_table(180)
+    rng = np.random.default_rng(41)
+    w, h = 1280, 720
+    d = oracle.rho_offset(w, h)
+    xs, ys = rng.integers(0, w, 300), rng.integers(0, h, 300)
+    e = ((ys.astype(np.uint32) << 16) | xs.astype(np.uint32))
+    for i in range(len(e)):
+        acc = oracle.hough_accumulate_f64(e[i:i + 1], w, h, c, s)
+        got = acc.argmax(axis=1) - d
+        for t in range(0, 180, 7):
+            r = Fraction(int(xs[i])) * Fraction(float(c[t])) + Fraction(int(ys[i])) * Fraction(float(s[t]))
+            want = math.floor(r + Fraction(1, 2))
+            near = abs((r + Fraction(1, 2)) - round(r + Fraction(1, 2))) < Fraction(1, 10 ** 9)
+            assert got[t] == want or near, (i, t)
+
+
+def test_f64_within_one_bin_of_q15_and_conservation(oracle):
+    cf, sf = synth.f64_table(180)
+    cq, sq = synth.q15_table(180)
+    rng = np.random.default_rng(42)
+    w, h = 320, 240
+    e = ((rng.integers(0, h, 2000).astype(np.uint32) << 16) |
+         rng.integers(0, w, 2000).astype(np.uint32))
+    af = oracle.hough_accumulate_f64(e, w, h, cf, sf)
+    aq = oracle.hough_accumulate(e, w, h, cq, sq)
+    assert af.sum() == aq.sum() == len(e) * 180
+    for i in range(0, 2000, 97):
+        bf = oracle.hough_accumulate_f64(e[i:i + 1], w, h, cf, sf).argmax(axis=1)
+        bq = oracle.hough_accumulate(e[i:i + 1], w, h, cq, sq).argmax(axis=1)
+        assert np.abs(bf.astype(int) - bq.astype(int)).max() <= 1
