@@ -147,6 +147,20 @@ int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count,
                         int32_t height, int32_t n_theta, const int32_t *cos_q15,
                         const int32_t *sin_q15, uint32_t *acc, void *stream);
 
+/* SPEC's float64 trig mode ("a second, non-bit-exact-vs-Q15
+ * workload"; DESIGN R29): ld_hough_accumulate with a HOST
+ * double-precision table,
+ *   acc[f][t][floor(x*cos[t] + y*sin[t] + 0.5) + D] += 1
+ * with each product and each sum rounded to nearest once (no fused
+ * multiply-add), so the result is exactly reproducible on any IEEE machine.
+ * n_theta <= 1024; entries finite with |value| <= 1; the corner range proof
+ * uses the same arithmetic (LD_ERR_RANGE otherwise).  Other arguments as
+ * ld_hough_accumulate. */
+int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
+                            int64_t edge_stride, int32_t batch, int32_t width,
+                            int32_t height, int32_t n_theta, const double *cos_f64,
+                            const double *sin_f64, uint32_t *acc, void *stream);
+
 /* Step 4 ("picking the line with the most pixel value"), made
  * deterministic (DESIGN R13, R14): key(t, r) = (acc[t][r], -t, -r),
  * lexicographic.  (t, r) is a peak candidate iff acc[t][r] >= max(1, min_votes)

@@ -431,6 +431,67 @@ int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count, int
                     sin_q15, acc, static_cast<cudaStream_t>(stream));
 }
 
+int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
+                            int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
+                            int32_t n_theta, const double *cos_f64, const double *sin_f64,
+                            uint32_t *acc, void *stream) {
+  g_launches = 0;
+  if (!edge_xy || !edge_count || !acc) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
+  if (batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
+  if (width < 1 || height < 1 || width > LD_MAX_DIM || height > LD_MAX_DIM)
+    return fail(LD_ERR_INVALID_ARG, "width/height outside [1, %d]", LD_MAX_DIM);
+  if (!aligned(edge_xy, 16) || edge_stride < 0 || edge_stride % 4 != 0)
+    return fail(LD_ERR_INVALID_ARG, "edge_xy must be 16-byte aligned and edge_stride a multiple of 4");
+  if (n_theta < 1 || n_theta > LD_MAX_THETA_F64)
+    return fail(LD_ERR_INVALID_ARG, "n_theta %d outside [1, %d]", n_theta, LD_MAX_THETA_F64);
+  if (!cos_f64 || !sin_f64) return fail(LD_ERR_INVALID_ARG, "trig table pointer is NULL");
+  const int32_t d = rho_offset(width, height);
+  const int64_t n_rho = 2 * static_cast<int64_t>(d) + 1;
+  const double xs[2] = {0.0, static_cast<double>(width - 1)};
+  const double ys[2] = {0.0, static_cast<double>(height - 1)};
+  for (int t = 0; t < n_theta; ++t) {
+    const double c = cos_f64[t], s = sin_f64[t];
+    if (!(c >= -1.0 && c <= 1.0 && s >= -1.0 && s <= 1.0))
+      return fail(LD_ERR_RANGE, "trig entry %d (%g, %g) is not finite in [-1, 1]", t, c, s);
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        volatile double px = xs[a] * c;  // rounded on its own (no contraction)
+        volatile double py = ys[b] * s;
+        const double r = px + py;
+        const int64_t rho = static_cast<int64_t>(floor(r + 0.5)) + d;
+        if (rho < 0 || rho >= n_rho)
+          return fail(LD_ERR_RANGE, "theta bin %d sends a corner to rho bin %lld", t,
+                      static_cast<long long>(rho));
+      }
+  }
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  int ctas = 1, rpb = 0, n_bands = 0;
+  size_t smem = 0;
+  if (!hough_plan(n_theta, static_cast<int>(n_rho), static_cast<size_t>(dev.smem_optin), &ctas,
+                  &rpb, &n_bands, &smem))
+    return fail(LD_ERR_UNSUPPORTED, "one accumulator row (%lld bins) exceeds shared memory",
+                static_cast<long long>(n_rho));
+  static thread_local TrigTableF64 trig;
+  memcpy(trig.c, cos_f64, sizeof(double) * n_theta);
+  memcpy(trig.s, sin_f64, sizeof(double) * n_theta);
+  HoughParams p;
+  memset(&p, 0, sizeof(p));
+  p.edges = edge_xy;
+  p.counts = edge_count;
+  p.edge_stride = edge_stride;
+  p.batch = batch;
+  p.n_theta = n_theta;
+  p.n_rho = static_cast<int32_t>(n_rho);
+  p.rows_per_band = rpb;
+  p.n_bands = n_bands;
+  p.acc = acc;
+  cudaError_t e = launch_hough_f64(p, trig, ctas, smem, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "hough_vote_f64_kernel launch");
+  return LD_OK;
+}
+
 size_t ld_hough_hint_bytes(int32_t batch, int32_t width, int32_t height, int32_t n_theta) {
   if (batch < 1 || width < 1 || height < 1 || n_theta < 1) return 0;
   return hint_bytes(batch, n_theta);

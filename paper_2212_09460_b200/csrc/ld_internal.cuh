@@ -55,6 +55,12 @@ struct TrigTable {
   int32_t s[LD_MAX_THETA];
 };
 
+constexpr int LD_MAX_THETA_F64 = 1024;  // double tables are passed by value (2 x 8 KB)
+struct TrigTableF64 {
+  double c[LD_MAX_THETA_F64];
+  double s[LD_MAX_THETA_F64];
+};
+
 struct HoughParams {
   const uint32_t *edges;
   const uint32_t *counts;
@@ -90,6 +96,9 @@ int hough_plan(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *rows_p
                int *n_bands, size_t *smem_bytes);
 cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, size_t smem_bytes,
                          cudaStream_t stream);
+// SPEC float64 trig mode (NEXT 4, ld_hough_f64.cu): same planning as hough_plan.
+cudaError_t launch_hough_f64(const HoughParams &p, const TrigTableF64 &trig, int ctas,
+                             size_t smem_bytes, cudaStream_t stream);
 // Half-angle paired voting (NEXT 2, Eq. 4-5): valid when the table is
 // symmetric, C[n-t] = -C[t] and S[n-t] = S[t] for 0 < t < n (checked on the
 // host).  Pair p = (t = p, n - t); p = 0 and p = n/2 (n even) have no partner

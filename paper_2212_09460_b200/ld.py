@@ -54,6 +54,7 @@ LD_FLAG_ZERO_PAD, LD_FLAG_CLAMP_255 = 1, 2
 
 EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",
            "ld_hough_hint_bytes", "ld_hough_accumulate_hint", "ld_hough_peaks_hinted",
+           "ld_hough_accumulate_f64",
            "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_hough_peaks_ex",
            "ld_hough_peaks_nms_workspace_bytes", "ld_hough_peaks_nms", "ld_peak_lines",
            "ld_extract_segments",
@@ -82,6 +83,7 @@ def lib():
             "ld_sobel_binarize_ex": ([P, IMG, i32, u32, P, P, i64, P, P], ctypes.c_int),
             "ld_hough_accumulate": ([P, P, i64, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
             "ld_hough_hint_bytes": ([i32, i32, i32, i32], sz),
+            "ld_hough_accumulate_f64": ([P, P, i64, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
             "ld_hough_accumulate_hint": ([P, P, i64, i32, i32, i32, i32, P, P, P, P, sz, P],
                                          ctypes.c_int),
             "ld_hough_peaks_hinted": ([P, i32, i32, i32, i32, i32, u32, i32, P, sz, P, P, P, sz,
@@ -193,6 +195,28 @@ def ld_hough_accumulate(edge_xy, edge_count, edge_stride, batch, width, height, 
     _check(lib().ld_hough_accumulate(_addr(edge_xy), _addr(edge_count), int(edge_stride),
                                      int(batch), int(width), int(height), int(n_theta),
                                      _addr(c), _addr(s), _addr(acc), _stream(stream)))
+
+
+def ld_hough_accumulate_f64(edge_xy, edge_count, edge_stride, batch, width, height, n_theta,
+                            cos_f64, sin_f64, acc, stream=None):
+    c = np.ascontiguousarray(np.asarray(cos_f64, dtype=np.float64))
+    s = np.ascontiguousarray(np.asarray(sin_f64, dtype=np.float64))
+    _check(lib().ld_hough_accumulate_f64(_addr(edge_xy), _addr(edge_count), int(edge_stride),
+                                         int(batch), int(width), int(height), int(n_theta),
+                                         _addr(c), _addr(s), _addr(acc), _stream(stream)))
+
+
+def hough_accumulate_f64(edges, counts, edge_stride, width, height, cos_f64, sin_f64,
+                         stream=None):
+    """SPEC float64 trig mode (ld_hough_accumulate_f64)."""
+    import torch
+    b = counts.shape[0]
+    n_theta = len(cos_f64)
+    n_rho = 2 * ld_rho_offset(width, height) + 1
+    acc = torch.empty((b, n_theta, n_rho), dtype=torch.int32, device=counts.device)
+    ld_hough_accumulate_f64(edges, counts, edge_stride, b, width, height, n_theta, cos_f64,
+                            sin_f64, acc, stream)
+    return acc
 
 
 def ld_hough_hint_bytes(batch, width, height, n_theta) -> int:

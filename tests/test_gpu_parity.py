@@ -827,3 +827,61 @@ def test_extract_segments_vertical_and_synthetic(ld, oracle):
             want, wn = oracle.extract_segments(b[0], tuple(pk[0, i]), c, s, fg, ml, cap=8)
             assert nseg[0, i] == wn
             assert [tuple(int(v) for v in segs[0, i, j]) for j in range(min(wn, 8))] == want
+
+
+# ----------------------------------------------------------------------------
+# SPEC float64 trig mode (NEXT 4, DESIGN R29) against the oracle, bit-exact
+# ----------------------------------------------------------------------------
+def _gpu_vote_f64(ld, lists, w, h, c, s):
+    b = len(lists)
+    stride = ld._round_up(max(max(len(e) for e in lists), 1), 4)
+    el = np.zeros((b, stride), np.uint32)
+    for i, e in enumerate(lists):
+        el[i, :len(e)] = e
+    counts = cuda(np.array([len(e) for e in lists], np.int32))
+    acc = ld.hough_accumulate_f64(cuda(el.view(np.int32)), counts, stride, w, h, c, s)
+    torch.cuda.synchronize()
+    return acc.cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("n_theta", [1, 2, 3, 180, 181, 720, 1024])
+def test_vote_f64_random_lists(ld, oracle, n_theta):
+    c, s = synth.f64_table(n_theta)
+    rng = np.random.default_rng(500 + n_theta)
+    w, h = 301, 203
+    lists = []
+    for n in (0, 1, 7, 5003):
+        xs, ys = rng.integers(0, w, n), rng.integers(0, h, n)
+        lists.append(((ys.astype(np.uint32) << 16) | xs.astype(np.uint32)))
+    got = _gpu_vote_f64(ld, lists, w, h, c, s)
+    for i, e in enumerate(lists):
+        assert np.array_equal(got[i], oracle.hough_accumulate_f64(e, w, h, c, s)), (n_theta, i)
+
+
+def test_vote_f64_frames_and_corners(ld, oracle):
+    c, s = synth.f64_table(180)
+    img = synth.gen_frame("cfg2", 0)
+    _, edges, counts, stride = ld.sobel_binarize(cuda(img[None]), 200, want_binary=False)
+    acc = ld.hough_accumulate_f64(edges, counts, stride, 1280, 720, c, s)
+    torch.cuda.synchronize()
+    e = oracle.compact(oracle.sobel_binarize(img, 200))
+    assert np.array_equal(acc.cpu().numpy().view(np.uint32)[0],
+                          oracle.hough_accumulate_f64(e, 1280, 720, c, s))
+    for w, h in [(1, 1), (16384, 1), (1, 16384), (16384, 16384)]:
+        c2, s2 = synth.f64_table(64)
+        corners = sorted({(0, 0), (w - 1, 0), (0, h - 1), (w - 1, h - 1)})
+        ee = np.array([(y << 16) | x for x, y in corners], np.uint32)
+        got = _gpu_vote_f64(ld, [ee], w, h, c2, s2)
+        assert np.array_equal(got[0], oracle.hough_accumulate_f64(ee, w, h, c2, s2)), (w, h)
+
+
+def test_vote_f64_rejects_bad_tables(ld):
+    el = torch.zeros((4,), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    acc = torch.zeros((1, 2, 2 * ld.ld_rho_offset(10, 10) + 1), dtype=torch.int32, device="cuda")
+    for c, s in [([1.5, 0.0], [0.0, 1.0]), ([float("nan"), 0.0], [0.0, 1.0])]:
+        with pytest.raises(ld.LdError) as ei:
+            ld.ld_hough_accumulate_f64(el, cnt, 4, 1, 10, 10, 2, c, s, acc)
+        assert ei.value.status == ld.LD_ERR_RANGE
+    with pytest.raises(ld.LdError):
+        ld.ld_hough_accumulate_f64(el, cnt, 4, 1, 10, 10, 1025, [0.0] * 1025, [0.0] * 1025, acc)
