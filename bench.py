@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--trig", default="q15", choices=["q15", "f64"],
+                    help="voting table: the caller's Q15 table (the metric's) or SPEC's "
+                         "float64 mode (a second workload, no peak hint)")
     ap.add_argument("--streams", type=int, default=2,
                     help="streams (each with its own buffers) the steps go to round-robin")
     ap.add_argument("--no-hint", action="store_true",
@@ -262,7 +265,10 @@ def run_ours(args, rank, world, local):
     n_rho = 2 * ld.ld_rho_offset(W, H) + 1
     img = ld.make_image(W, H, pitch, H * pitch, B)
     stride = ld._round_up(H * max(W - 2, 0), 4)
-    use_hint = not args.no_hint
+    f64 = args.trig == "f64"
+    if f64:
+        cf, sf = synth.f64_table(cfg.n_theta)
+    use_hint = not args.no_hint and not f64
     pws_bytes = ld.ld_hough_peaks_workspace_bytes(B, cfg.n_theta, n_rho, cfg.k)
     hint_bytes = ld.ld_hough_hint_bytes(B, W, H, cfg.n_theta)
 
@@ -293,7 +299,10 @@ def run_ours(args, rank, world, local):
         launches[0] += ld.ld_last_launch_count()
         if ev is not None:
             ev[1].record(st)
-        if use_hint:
+        if f64:
+            ld.ld_hough_accumulate_f64(bf.edges, bf.counts, stride, B, W, H, cfg.n_theta, cf, sf,
+                                       bf.acc, st)
+        elif use_hint:
             ld.ld_hough_accumulate_hint(bf.edges, bf.counts, stride, B, W, H, cfg.n_theta, c, s,
                                         bf.acc, bf.hint, hint_bytes, st)
         else:
@@ -415,7 +424,8 @@ def run_ours(args, rank, world, local):
     sobel_bytes = B * (W * H + 4) + 4 * int(cnt.sum())
     vote_rate = votes / (vote_ms / 1e3) / 1e9
     peaks_bytes = B * cfg.n_theta * n_rho * 4
-    roofline = {"kernel": vote_kernel_name(c, s), "bound": "smem_atomic",
+    roofline = {"kernel": "hough_vote_f64_kernel" if f64 else vote_kernel_name(c, s),
+                "bound": "smem_atomic",
                 "achieved": vote_rate, "peak": atom["conflict_free"], "unit": "Gatomic/s",
                 "frac": vote_rate / atom["conflict_free"], "traffic": None,
                 "peak_source": "B5 microbenchmark (conflict-free red.shared.add.u32, all SMs), "
@@ -423,7 +433,7 @@ def run_ours(args, rank, world, local):
     hbm_peak = hbm_peak_gbs()
     sobel_gbs = sobel_bytes / (sob_ms / 1e3) / 1e9
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and not f64:
         n, tcpu = oracle_frames(args.workload, 0, args.cpu_seconds, B)
         cpu = {"value": n / tcpu, "unit": "frames/s", "cores": 1, "kind": "oracle",
                "sample": "first %d frames of %s (same seeds as the GPU batch), single thread, "
@@ -438,6 +448,7 @@ def run_ours(args, rank, world, local):
                    "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
                    "parallelism": "frame-shard dp%d" % world,
                    "peak_hint": use_hint,
+                   "trig": args.trig,
                    "streams": args.streams,
                    "ms_per_step_one_stream": serial_ms,
                    "l2": "inputs %.0f MB + accumulators %.0f MB per GPU exceed L2 (%.0f MB); no flush"
