@@ -536,8 +536,7 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
   const int nt = p.st_nt;
   const int width = nt * CPT;                          // loaded columns
   uint32_t *CM = reinterpret_cast<uint32_t *>(psm);     // [PS_G][width] column maxima
-  uint32_t *RAW = CM + PS_G * width;                    // [PS_G + HT][width] rows g0-HT ..
-  u64 *top = reinterpret_cast<u64 *>(RAW + (PS_G + HT) * width);  // [k] (8-aligned: width even)
+  u64 *top = reinterpret_cast<u64 *>(CM + PS_G * width);  // [k] (8-aligned: width even)
   u64 *buf = top + p.k;                                 // [pow2(candidate bound + k)]
   uint32_t *SL = reinterpret_cast<uint32_t *>(buf + p.st_buf);  // [PS_G * sw] survivors
   __shared__ int s_nbuf, s_ntop, s_nsurv;
@@ -646,13 +645,20 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
     uint32_t surv = 0;
 #pragma unroll
     for (int i = 0; i < PS_G; ++i) {
-      uint32_t m[CPT];
+      // per column: mu = max of the HT rows above, md = of the HT rows below;
+      // the cell beats its own column of the window with the tie rule iff
+      // v > mu and v >= md (an equal value above has a lower index)
+      uint32_t m[CPT], strict = 0;
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
-        uint32_t mm = V[i][q];
+        uint32_t mu = 0, md = 0;
 #pragma unroll
-        for (int k = 1; k <= 2 * HT; ++k) mm = max(mm, V[i + k][q]);
-        m[q] = mm;
+        for (int k = 0; k < HT; ++k) mu = max(mu, V[i + k][q]);
+#pragma unroll
+        for (int k = 1; k <= HT; ++k) md = max(md, V[i + HT + k][q]);
+        const uint32_t v = V[i + HT][q];
+        m[q] = max(max(mu, md), v);
+        strict |= static_cast<uint32_t>(v > mu) << q;
       }
       // prefilter: a window maximum is >= the column maxima of every column
       // within +-hr -- here the thread's own CPT columns and the nearest
@@ -667,13 +673,12 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
           const uint32_t need = hr_wide ? hm : m[q];
-          surv |= static_cast<uint32_t>(V[i + HT][q] >= max(need, tq[q])) << (i * CPT + q);
+          surv |= static_cast<uint32_t>(V[i + HT][q] >= max(need, tq[q]) && ((strict >> q) & 1u))
+                  << (i * CPT + q);
         }
       }
       stream_store(CM + i * width + j0, m);
     }
-#pragma unroll
-    for (int k = 0; k < PS_G + HT; ++k) stream_store(RAW + k * width + j0, V[k]);
     if (nrows < PS_G) surv &= (1u << (nrows * CPT)) - 1u;
     while (surv) {  // survivor list of the group: (row << 16) | loaded column
       const int b = __ffs(surv) - 1;
@@ -683,7 +688,7 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
       if (LD_CHK(slot < PS_G * p.st_sw))
         SL[slot] = (static_cast<uint32_t>(i) << 16) | static_cast<uint32_t>(j0 + q);
     }
-    __syncthreads();  // (1) CM, RAW and the survivor list of the group complete
+    __syncthreads();  // (1) CM and the survivor list of the group complete
     {
       // one warp per survivor: the lanes scan the +-hr column maxima and the
       // tie rows in parallel (ballots), instead of one divergent lane each
@@ -694,8 +699,7 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
         const int i = static_cast<int>(e >> 16), j = static_cast<int>(e & 0xFFFFu);
         const uint32_t *cmr = CM + i * width + j;
         const uint32_t v = *cmr;  // == the cell's own value
-        bool bad = lane < HT && RAW[(i + lane) * width + j] == v;  // own column, earlier rows
-        bool tie = false;
+        bool bad = false, tie = false;
         for (int d = 1 + lane; d <= hr; d += 32) {
           const uint32_t l = cmr[-d], r = cmr[d];
           bad = bad || l > v || r > v;
@@ -704,11 +708,15 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
         if (!__any_sync(0xffffffffu, bad) && __any_sync(0xffffffffu, tie)) {
           // equal column maxima: an equal value at a lower (theta, rho) index
           // -- to the left rows up to the cell's own, to the right rows above
+          // (re-read from the accumulator: ties are rare)
+          const int t = g0 + i;
           for (int d = 1 + lane; d <= hr && !bad; d += 32) {
             if (cmr[-d] == v)
-              for (int k = i; k <= i + HT && !bad; ++k) bad = RAW[k * width + j - d] == v;
+              for (int row = max(t - HT, 0); row <= t && !bad; ++row)
+                bad = __ldg(frame0 + static_cast<int64_t>(row) * n_rho + cbase + j - d) == v;
             if (!bad && cmr[d] == v)
-              for (int k = i; k < i + HT && !bad; ++k) bad = RAW[k * width + j + d] == v;
+              for (int row = max(t - HT, 0); row < t && !bad; ++row)
+                bad = __ldg(frame0 + static_cast<int64_t>(row) * n_rho + cbase + j + d) == v;
           }
         }
         if (!__any_sync(0xffffffffu, bad) && lane == 0) {
@@ -718,7 +726,7 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
         }
       }
     }
-    __syncthreads();  // (2) candidates buffered; CM / RAW / SL free
+    __syncthreads();  // (2) candidates buffered; CM / SL free
     const int nbuf = s_nbuf;
     if (nbuf > 0) merge_topk(buf, nbuf, top, &s_ntop, p.k);
     if (tid == 0) {
@@ -796,7 +804,8 @@ static int stream_buf_entries(int sw, int ht, int hr, int k) {
   return pow2_ceil(bound + k);
 }
 static size_t stream_smem_bytes(int width, int sw, int ht, int hr, int k) {
-  return sizeof(uint32_t) * static_cast<size_t>(2 * PS_G + ht) * width +
+  (void)ht;
+  return sizeof(uint32_t) * static_cast<size_t>(PS_G) * width +
          sizeof(u64) * (static_cast<size_t>(k) + stream_buf_entries(sw, ht, hr, k)) +
          sizeof(uint32_t) * static_cast<size_t>(PS_G) * sw;
 }
