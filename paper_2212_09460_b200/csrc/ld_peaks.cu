@@ -8,13 +8,17 @@
 // candidate iff acc >= max(1, min_votes) and its key is the maximum of its
 // (2ht+1) x (2hr+1) window clipped to the accumulator.  DESIGN.md 6.3.
 //
-// Kernel 1, fast path (peaks_tile_kernel): separable window maximum over
-// 16 x tc tiles, see below.  Kernel 1, generic fallback for very large windows
-// (peaks_band_kernel: frames x theta bands of PK_ROWS rows): each thread tests
-// cells of the band by a window scan with early exit; a cell whose key is not
-// above the band's running K-th best key is skipped first.  Candidates are
-// buffered in shared memory and merged into the band's top-K with a bitonic
-// sort.  Kernel 2 (one CTA per frame): merges the per-unit top-K lists.
+// Kernel 1, chosen per window (launch_peaks, in this order):
+//   peaks_warp_kernel    -- half_theta <= 3, 4 <= half_rho <= 64, k <= 64:
+//                           every warp an independent strip x row chunk;
+//   peaks_stream_kernel  -- half_theta <= 12: a CTA per strip x row chunk;
+//   peaks_tile_kernel    -- separable window maximum over 16-row tiles
+//                           (unrestricted searches);
+//   peaks_band_kernel    -- generic fallback: a window scan per cell.
+// All keep a per-unit top-k; kernel 2 (peaks_merge_kernel, one CTA per frame)
+// merges the per-unit lists.  The warp and stream kernels share a per-frame
+// running threshold (the k-th best found so far, gtau), optionally started
+// by peaks_hint_kernel from the voting kernel's range maxima (DESIGN R25).
 #include <cstdlib>
 
 #include "ld_internal.cuh"
