@@ -89,3 +89,42 @@ def test_workspace_sizes_are_consistent(libld):
     assert a - b >= acc and a - b < acc + 512
     assert libld.ld_hough_peaks_workspace_bytes(256, 180, 2939, 4) > 0
     assert libld.ld_detect_host_workspace_bytes(img, 180, 4, 32) > 0
+
+
+def test_validation_of_the_extension_entry_points(libld):
+    # every check below happens on the host before any device query
+    E = libld.LdError
+    with pytest.raises(E) as e:  # hinted voting needs a hint buffer
+        libld.ld_hough_accumulate_hint(16, 16, 4, 1, 10, 10, 2, [32768, 0], [0, 32768], 16,
+                                       None, 0, stream=0)
+    assert e.value.status == libld.LD_ERR_INVALID_ARG
+    with pytest.raises(E) as e:  # k = 0
+        libld.ld_hough_peaks_hinted(16, 1, 180, 801, 2, 8, 1, 0, 16, 1 << 20, 16, 16, 16, 1 << 20,
+                                    stream=0)
+    assert e.value.status == libld.LD_ERR_INVALID_ARG
+    with pytest.raises(E) as e:  # ratio denominator 0
+        libld.ld_hough_peaks_nms(16, 1, 180, 801, 2, 8, 1, 1, 0, 4, 16, 16, 16, 1 << 20, stream=0)
+    assert e.value.status == libld.LD_ERR_INVALID_ARG
+    with pytest.raises(E) as e:  # NULL peaks
+        libld.ld_peak_lines(None, 16, 1, 4, 512, 512, 180, [0] * 180, [0] * 180, 16, 16, stream=0)
+    assert e.value.status == libld.LD_ERR_INVALID_ARG
+    img = libld.make_image(128, 64, pitch=128)
+    with pytest.raises(E) as e:  # max_segments 0
+        libld.ld_extract_segments(16, img, 16, 16, 4, 180, [0] * 180, [0] * 180, 20, 40, 0, 16,
+                                  16, stream=0)
+    assert e.value.status == libld.LD_ERR_INVALID_ARG
+    with pytest.raises(E) as e:  # f64 table entry outside [-1, 1] (checked before the device)
+        libld.ld_hough_accumulate_f64(16, 16, 4, 1, 10, 10, 2, [2.0, 0.0], [0.0, 1.0], 16,
+                                      stream=0)
+    assert e.value.status == libld.LD_ERR_RANGE
+    with pytest.raises(E) as e:  # f64 mode is limited to 1024 theta bins
+        libld.ld_hough_accumulate_f64(16, 16, 4, 1, 10, 10, 1025, [0.0] * 1025, [0.0] * 1025, 16,
+                                      stream=0)
+    assert e.value.status == libld.LD_ERR_INVALID_ARG
+
+
+def test_workspace_size_queries_are_host_only(libld):
+    assert libld.ld_hough_hint_bytes(256, 1280, 720, 180) >= 64 + 256 * 180 * 8
+    assert libld.ld_hough_hint_bytes(0, 1280, 720, 180) == 0
+    assert libld.ld_hough_peaks_nms_workspace_bytes(2, 180, 2939) >= 2 * ((180 * 2939 + 31) // 32) * 4
+    assert libld.ld_hough_peaks_nms_workspace_bytes(0, 180, 2939) == 0
