@@ -885,3 +885,24 @@ def test_vote_f64_rejects_bad_tables(ld):
         assert ei.value.status == ld.LD_ERR_RANGE
     with pytest.raises(ld.LdError):
         ld.ld_hough_accumulate_f64(el, cnt, 4, 1, 10, 10, 1025, [0.0] * 1025, [0.0] * 1025, acc)
+
+
+def test_hinted_peaks_randomized_stress(ld, oracle):
+    # random images x windows (warp, stream, tile and band kernels) x k, the
+    # hinted path against the oracle and against the unhinted path
+    rng = np.random.default_rng(777)
+    for trial in range(10):
+        b = int(rng.integers(1, 5))
+        w, h = int(rng.integers(40, 300)), int(rng.integers(20, 200))
+        frames = np.zeros((b, h, w), np.uint8)
+        for f in range(b):
+            frames[f] = (rng.random((h, w)) < rng.uniform(0.02, 0.3)) * 255
+            for _ in range(int(rng.integers(0, 4))):
+                y = int(rng.integers(0, h))
+                frames[f, y, :] = 255
+        n_theta = int(rng.choice([90, 180, 181]))
+        ht = int(rng.choice([0, 1, 2, 3, 5, 8, 13]))
+        hr = int(rng.choice([4, 9, 29, 64, 70]))
+        k = int(rng.choice([1, 3, 4, 16, 64, 100]))
+        cfg = synth.Config("t", w, h, b, 200, n_theta, k, ht, hr)
+        _hint_case(ld, oracle, frames, cfg)
