@@ -1213,7 +1213,7 @@ static TileKernel tile_kernel(int ht) {
 }
 
 // Tile geometry for a window; returns false when the generic band kernel must be used.
-bool peaks_tile_plan(int n_theta, int n_rho, int half_theta, int half_rho, int k, PeaksParams *p,
+static bool peaks_tile_plan(int n_theta, int n_rho, int half_theta, int half_rho, int k, PeaksParams *p,
                      size_t *smem) {
   if (half_theta > PT_MAX_HT) return false;
   int best_tch = 0, best_tc = 0;

@@ -906,3 +906,30 @@ def test_hinted_peaks_randomized_stress(ld, oracle):
         k = int(rng.choice([1, 3, 4, 16, 64, 100]))
         cfg = synth.Config("t", w, h, b, 200, n_theta, k, ht, hr)
         _hint_case(ld, oracle, frames, cfg)
+
+
+def test_detect_randomized_soak(ld, oracle):
+    # end to end through ld_detect_batch (paired voting + peak hint inside)
+    # on random images, thresholds, theta counts, windows and k
+    rng = np.random.default_rng(4242)
+    for trial in range(12):
+        b = int(rng.integers(1, 4))
+        w, h = int(rng.integers(3, 400)), int(rng.integers(3, 300))
+        frames = rng.integers(0, 256, size=(b, h, w)).astype(np.uint8)
+        if trial % 3 == 0:
+            frames = (frames > 200).astype(np.uint8) * 255
+        thr = int(rng.choice([1, 100, 200, 700, 1531]))
+        n_theta = int(rng.choice([1, 2, 7, 90, 180, 181, 360]))
+        c, s = synth.q15_table(n_theta)
+        ht, hr = int(rng.integers(0, 8)), int(rng.integers(0, 70))
+        mv, k = int(rng.integers(0, 6)), int(rng.choice([1, 2, 4, 16, 64]))
+        peaks, npk, counts, acc = ld.detect_batch(cuda(frames), thr, c, s, ht, hr, mv, k)
+        torch.cuda.synchronize()
+        P, N, C, A = (peaks.cpu().numpy(), npk.cpu().numpy(), counts.cpu().numpy(),
+                      acc.cpu().numpy().view(np.uint32))
+        for f in range(b):
+            r = oracle.detect(frames[f], thr, c, s, ht, hr, mv, k)
+            assert int(C[f]) == r["n_edges"], (trial, f)
+            assert np.array_equal(A[f], r["acc"]), (trial, f)
+            assert int(N[f]) == r["n_peaks"], (trial, f)
+            assert peak_tuples(P[f]) == oracle_peak_tuples(r["peaks"]), (trial, f)
