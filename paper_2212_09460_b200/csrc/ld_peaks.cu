@@ -512,7 +512,10 @@ constexpr int PS_NPF = 2;  // groups of L2 prefetch beyond the register prefetch
 constexpr int PS_NT_MAX = 512;   // threads per CTA, one CTA per SM
 constexpr int PS_NT_MAX2 = 384;  // threads per CTA when two CTAs share an SM
 // register window (2 groups + 2HT rows) x CPT small enough for two CTAs per SM
-constexpr int ps_minb(int ht, int cpt) { return (2 * PS_G + 2 * ht) * cpt <= 48 ? 2 : 1; }
+#ifndef LD_PS_MINB_LIMIT
+#define LD_PS_MINB_LIMIT 48
+#endif
+constexpr int ps_minb(int ht, int cpt) { return (2 * PS_G + 2 * ht) * cpt <= LD_PS_MINB_LIMIT ? 2 : 1; }
 
 template <int CPT>
 __device__ __forceinline__ void stream_store(uint32_t *dst, const uint32_t (&v)[CPT]) {
