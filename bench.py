@@ -10,7 +10,7 @@ ld_sobel_binarize (fused Sobel + binarize + compaction) -> ld_hough_accumulate
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Steps go round-robin to ``--streams`` streams (default 2), each with its own
+Steps go round-robin to ``--streams`` streams (default 4), each with its own
 output buffers, as a serving pipeline double-buffers batches: one step's peak
 search (memory-latency-bound) overlaps the next step's Sobel (issue-bound).
 The headline is K such steps from a common start event to the join;
@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--trig", default="q15", choices=["q15", "f64"],
                     help="voting table: the caller's Q15 table (the metric's) or SPEC's "
                          "float64 mode (a second workload, no peak hint)")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=4,
                     help="streams (each with its own buffers) the steps go to round-robin")
     ap.add_argument("--no-hint", action="store_true",
                     help="plain ld_hough_accumulate + ld_hough_peaks (no peak hint)")
