@@ -471,6 +471,40 @@ class Detector:
         return self.peaks, self.n_peaks, self.counts, self.acc
 
 
+class PipelinedDetector:
+    """Batches in flight on several streams (the benchmark's serving mode).
+
+    Each of `streams` slots owns a Detector (its own workspace and outputs)
+    and a CUDA stream; submit() enqueues ld_detect_batch for one batch on the
+    next slot, after the caller's current stream (so the input is ready), and
+    returns that slot's (peaks, n_peaks, counts) tensors and a CUDA event that
+    completes with them.  A slot is reused `streams` submissions later, which
+    first waits for its previous batch (the stream order does it).  Step i's
+    peak search then overlaps step i+1's Sobel on the GPU."""
+
+    def __init__(self, width, height, batch, n_theta, cos_q15, sin_q15, threshold, k,
+                 half_theta, half_rho, min_votes=1, streams=4, device=None, flags=0):
+        import torch
+        self.slots = []
+        for _ in range(streams):
+            det = Detector(width, height, batch, n_theta, cos_q15, sin_q15, threshold, k,
+                           half_theta, half_rho, min_votes, False, device, flags)
+            self.slots.append((det, torch.cuda.Stream(device=det.device)))
+        self.next = 0
+
+    def submit(self, gray):
+        """gray: uint8 CUDA [B][H][pitch] (pitch = round_up(W, 16)); must stay
+        unmodified until the returned event completes."""
+        import torch
+        det, st = self.slots[self.next]
+        self.next = (self.next + 1) % len(self.slots)
+        st.wait_stream(torch.cuda.current_stream(det.device))
+        det(gray, st)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        return det.peaks, det.n_peaks, det.counts, ev
+
+
 def detect_batch(gray, threshold, cos_q15, sin_q15, half_theta, half_rho, min_votes, k,
                  export_acc=True, stream=None):
     b, h, w = gray.shape

@@ -933,3 +933,26 @@ def test_detect_randomized_soak(ld, oracle):
             assert np.array_equal(A[f], r["acc"]), (trial, f)
             assert int(N[f]) == r["n_peaks"], (trial, f)
             assert peak_tuples(P[f]) == oracle_peak_tuples(r["peaks"]), (trial, f)
+
+
+def test_pipelined_detector_matches_single_stream(ld, oracle):
+    cfg = synth.CONFIGS["cfg3"]
+    c, s = synth.q15_table(cfg.n_theta)
+    frames = [synth.gen_batch("cfg3", 8 * i, 8) for i in range(5)]
+    pd = ld.PipelinedDetector(1280, 720, 8, cfg.n_theta, c, s, cfg.threshold, cfg.k,
+                              cfg.half_theta, cfg.half_rho, cfg.min_votes, streams=3)
+    outs = []
+    inputs = [cuda(f) for f in frames]  # 1280 is a multiple of 16: pitch == width
+    for g in inputs:
+        pk, npk, cnt, ev = pd.submit(g)
+        ev.synchronize()
+        outs.append((pk.clone(), npk.clone(), cnt.clone()))
+    for i, f in enumerate(frames):
+        ref = ld.detect_batch(inputs[i], cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+                              cfg.min_votes, cfg.k, export_acc=False)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i][0], ref[0]) and torch.equal(outs[i][1], ref[1])
+        assert torch.equal(outs[i][2], ref[2])
+    r = oracle.detect(frames[2][3], cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+                      cfg.min_votes, cfg.k, want_binary=False, want_acc=False)
+    assert peak_tuples(outs[2][0][3].cpu()) == oracle_peak_tuples(r["peaks"])
