@@ -257,13 +257,14 @@ def paper_latency(reps=50):
     pk_host = torch.empty((1, 4, 3), dtype=torch.int32).pin_memory()
     st = torch.cuda.current_stream()
 
-    def span(peaks, copy):
+    def span(peaks, copy, stream=None):
+        stream = st if stream is None else stream
         if copy:
             gray.copy_(host, non_blocking=True)
-        ld.ld_sobel_binarize(gray, img, 200, None, edges, stride, counts, st)
-        ld.ld_hough_accumulate(edges, counts, stride, 1, W, H, 180, c, s, acc, st)
+        ld.ld_sobel_binarize(gray, img, 200, None, edges, stride, counts, stream)
+        ld.ld_hough_accumulate(edges, counts, stride, 1, W, H, 180, c, s, acc, stream)
         if peaks:
-            ld.ld_hough_peaks(acc, 1, 180, n_rho, 2, 29, 1, 4, pk, npk, ws, wsb, st)
+            ld.ld_hough_peaks(acc, 1, 180, n_rho, 2, 29, 1, 4, pk, npk, ws, wsb, stream)
         if copy:
             pk_host.copy_(pk, non_blocking=True)
 
@@ -281,6 +282,28 @@ def paper_latency(reps=50):
             if i >= 5:
                 ts.append(e0.elapsed_time(e1))
         out[name] = float(np.median(ts))
+    # the same two spans replayed from a CUDA graph (launch overhead removed;
+    # the ABI calls are capturable: no host synchronisation inside)
+    for name, pk_on in (("paper_span_graph_ms", False), ("with_peaks_graph_ms", True)):
+        try:
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                span(pk_on, False, torch.cuda.current_stream())
+            ts = []
+            for i in range(reps + 5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(st)
+                graph.replay()
+                e1.record(st)
+                torch.cuda.synchronize()
+                if i >= 5:
+                    ts.append(e0.elapsed_time(e1))
+            out[name] = float(np.median(ts))
+        except Exception as exc:  # capture unsupported: report why, keep the eager numbers
+            out[name] = None
+            out["graph_error"] = str(exc)[:200]
     out.update({"frame": "512x512 synthetic cfg2-model road frame, T=200, 180 theta",
                 "edges": int(counts.item()), "paper_k80_ms": 4.874, "paper_zc706_ms": 2.62,
                 "note": "context only: different hardware, image and timing span details"})
