@@ -956,3 +956,24 @@ def test_pipelined_detector_matches_single_stream(ld, oracle):
     r = oracle.detect(frames[2][3], cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
                       cfg.min_votes, cfg.k, want_binary=False, want_acc=False)
     assert peak_tuples(outs[2][0][3].cpu()) == oracle_peak_tuples(r["peaks"])
+
+
+def test_detect_is_cuda_graph_capturable(ld):
+    # the C ABI enqueues without host synchronisation: a whole detect step
+    # captures into a CUDA graph and replays to the same result
+    cfg = synth.CONFIGS["cfg3"]
+    c, s = synth.q15_table(cfg.n_theta)
+    g = cuda(synth.gen_batch("cfg3", 0, 4))
+    det = ld.Detector(1280, 720, 4, cfg.n_theta, c, s, cfg.threshold, cfg.k, cfg.half_theta,
+                      cfg.half_rho, cfg.min_votes)
+    ref = [t.clone() for t in det(g)[:3]]
+    torch.cuda.synchronize()
+    for t in (det.peaks, det.n_peaks, det.counts):
+        t.fill_(-7)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        det(g, torch.cuda.current_stream())
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(det.peaks, ref[0]) and torch.equal(det.n_peaks, ref[1])
+    assert torch.equal(det.counts, ref[2])
