@@ -262,3 +262,44 @@ def hough_accumulate_f64(edges: np.ndarray, width: int, height: int, cos_f64: np
                                           n_theta, _ptr(c), _ptr(s), _ptr(acc)),
            "hough_accumulate_f64")
     return acc
+
+
+# ----------------------------------------------------------------------------
+# Frame-parallel harness (test/baseline infrastructure, no arithmetic of its
+# own): independent frames go to a thread pool.  ctypes releases the GIL for
+# the duration of each C call, so N threads run N single-threaded oracle
+# frames at once -- SURVEY 8(d) "frame-parallel across all cores".
+# ----------------------------------------------------------------------------
+def host_cores() -> int:
+    """Cores this process may run on (the affinity mask, else os.cpu_count())."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover - non-Linux
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    """The host CPU model string (/proc/cpuinfo), for the bench record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def map_frames(fn, items, workers: int | None = None):
+    """[fn(item) for item in items] on a pool of `workers` threads (default:
+    every host core), results in input order.  fn should spend its time in
+    oracle C calls (which run without the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    lib()  # load once, before the threads
+    items = list(items)
+    workers = max(1, min(workers or host_cores(), len(items) or 1))
+    if workers == 1:
+        return [fn(it) for it in items]
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(fn, items))
