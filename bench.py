@@ -1,33 +1,43 @@
 #!/usr/bin/env python
 """Benchmark of the lane-detection hot path (arXiv 2212.09460) on B200.
 
-Default workload: BASELINE.json configs[2] ("cfg3"), 256 synthetic 1280x720
-road frames per GPU, T=200, 180 theta bins, top-4 peaks -- the configuration
+Default workload: BASELINE.json configs[2] ("cfg3"), a batch of 256 synthetic
+1280x720 road frames, T=200, 180 theta bins, top-4 peaks -- the configuration
 the metric "1280x720 frames/s and Hough Gvotes/s at 1/2/4/8 B200; Sobel HBM
-GB/s" is quoted on.  One step = the whole hot path over the batch:
-ld_sobel_binarize (fused Sobel + binarize + compaction) -> ld_hough_accumulate
-(theta-band voting) -> ld_hough_peaks, each through the C ABI.
+GB/s" is quoted on.  One step = the whole hot path over the batch, through the
+C ABI: ld_sobel_binarize (fused Sobel + binarize + compaction) ->
+ld_hough_accumulate_hint (theta-band voting + accumulator write-out) ->
+ld_hough_peaks_hinted (top-k peaks).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg1..cfg5] [--scaling strong|weak] [--shard band|theta]
+
+Multi-GPU: ``--gpus N`` without a torchrun environment re-launches this script
+under ``torch.distributed.run`` with N ranks (one per GPU, NCCL, NCCL init
+logging on stderr); under torchrun (the driver's launch) it runs as the rank
+it is.  cfg3/cfg4 split the config's batch over the ranks as BASELINE.json
+says (frames [r B/N, (r+1) B/N) per rank, generated locally from their seeds:
+no data-path collective; ``--scaling weak`` gives every rank a whole batch
+instead); cfg5 splits one image into row bands (``--shard band``, NCCL
+all_reduce of the accumulator) or theta shards (``--shard theta``); cfg1/cfg2
+run replicas.  Time is the maximum over ranks of the device-timed region.
 
 Steps go round-robin to ``--streams`` streams (default 4), each with its own
-output buffers, as a serving pipeline double-buffers batches: one step's peak
-search (memory-latency-bound) overlaps the next step's Sobel (issue-bound).
-The headline is K such steps from a common start event to the join;
-per-kernel times (and the roofline) come from the same K steps serialised on
-one stream, reported next to it (``config.ms_per_step_one_stream``).
-
-N > 1 is launched by torchrun (one process per GPU, NCCL): frames shard across
-ranks with no data-path collective (weak scaling: 256 frames per rank); timing
-is the max over ranks.  ``--impl reference`` times the CPU oracle (the only
-"reference" this paper-only tier has) on a bounded sample of the same workload.
-Rank 0 prints ONE JSON line.
+output buffers, as a serving pipeline multi-buffers batches.  Per-kernel times
+(and the rooflines) come from the same K steps serialised on one stream.  At
+N=1 the oracle (oracle/, the CPU checker) then re-computes EVERY frame of the
+timed batch, frame-parallel on all host cores, and compares counts, edge sets,
+accumulators and peaks (``parity``); its speed is the ``cpu_baseline``.
+``--impl reference`` times that oracle alone (this paper-only tier has no
+other reference).  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -51,10 +61,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg3", choices=list(synth.CONFIGS))
-    ap.add_argument("--frames", type=int, default=None, help="frames per rank (default: config batch)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--frames", type=int, default=None,
+                    help="global batch (default: the config's batch)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's batch split over the ranks (BASELINE.json); "
+                         "weak: every rank runs a whole batch of its own frames")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the oracle re-computation of the timed batch (and cpu_baseline)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
+                    help="bound on the single-thread oracle sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--trig", default="q15", choices=["q15", "f64"],
                     help="voting table: the caller's Q15 table (the metric's) or SPEC's "
@@ -65,7 +81,7 @@ def parse():
                     help="plain ld_hough_accumulate + ld_hough_peaks (no peak hint)")
     ap.add_argument("--shard", default="band", choices=["band", "theta"],
                     help="cfg5 multi-GPU decomposition: row bands + all_reduce of the "
-                         "accumulator, or theta shards + all_gather of edge lists")
+                         "accumulator, or theta shards + all_gather of edge bitmaps")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo: plumbing check of N ranks on fewer GPUs)")
     return ap.parse_args()
@@ -76,6 +92,28 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with N local ranks (127.0.0.1 rendezvous); rank 0 prints the line."""
+    env = dict(os.environ)
+    if args.dist_backend == "nccl":
+        # NCCL init lines (rank, nranks, transport) on stderr, so stdout keeps
+        # exactly one JSON line
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=%d" % args.gpus, "--master-addr=127.0.0.1",
+           "--master-port=%d" % free_port(), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 # ----------------------------------------------------------------------------
@@ -95,7 +133,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -114,7 +152,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        sm, smax, power, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -123,6 +161,7 @@ class ClockSampler:
             try:
                 sm.append(float(parts[1]))
                 smax.append(float(parts[2]))
+                power.append(float(parts[3]))
             except ValueError:
                 continue
             for n, v in zip(names, parts[5:9]):
@@ -130,56 +169,174 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# record helpers
+# ----------------------------------------------------------------------------
+def measured_peaks():
+    peaks_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_file):
+        return json.load(open(peaks_file))
+    return {}
+
+
+def hbm_peak_gbs():
+    """Measured HBM copy bandwidth (driver-written MEASURED_PEAKS.json), else the
+    profiling guide's fallback."""
+    return float(measured_peaks().get("hbm_gbs", 6650.0))
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` on `workload` from the
+    round's committed ncu --set full capture (profiles/ncu_traffic.json,
+    written by tools/ncu_summary.py), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    rec = json.load(open(path)).get(workload, {})
+    for name, v in rec.items():
+        if name.startswith(kernel):
+            return v
+    return None
+
+
+def trig_hash(c, s) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(c, dtype=np.int32).tobytes())
+    h.update(np.ascontiguousarray(s, dtype=np.int32).tobytes())
+    return h.hexdigest()
+
+
+def host_info():
+    import oracle
+    return {"cpu_model": oracle.cpu_model(), "nproc": oracle.host_cores()}
+
+
+def vote_kernel_name(c, s):
+    """Which voting kernel libld.so picks for this table (label only): the
+    half-angle paired kernel for a symmetric table (C[n-t] = -C[t],
+    S[n-t] = S[t])."""
+    n = len(c)
+    sym = all(c[n - t] == -c[t] and s[n - t] == s[t] for t in range(1, n) if 2 * t != n)
+    return "hough_vote_pairs_kernel" if sym else "hough_vote_kernel"
+
+
+def smem_atomic_peaks(sm_mhz=None):
+    """B5 microbenchmark (conflict-free / random / same-address
+    red.shared.add.u32 on all SMs), measured in this run.  Per mode: warp-ATOMS
+    per clock per SM from the clock64 cycles of each CTA's timed loop (the
+    shared-memory pipe retires at most one wavefront per clock per SM,
+    tools/atoms_probe.cu), and G lane-atomics/s at the SM clock `sm_mhz`
+    (sampled under load; else the driver-measured maximum)."""
+    import torch
+    from paper_2212_09460_b200 import ld
+    sms = ld.ld_device_sm_count()
+    if not sm_mhz:
+        sm_mhz = measured_peaks().get("sm_max_mhz", 1965.0)
+    scratch = torch.zeros((sms * 34,), dtype=torch.int32, device="cuda")
+    out = {"sm_mhz": sm_mhz}
+    for mode, name in ((0, "conflict_free"), (1, "random"), (2, "same_address")):
+        iters = 16384 if mode < 2 else 1024
+        ld.ld_bench_smem_atomics(mode, 64, 1, scratch)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        n = ld.ld_bench_smem_atomics(mode, iters, 1, scratch)
+        e1.record()
+        torch.cuda.synchronize()
+        words = scratch.view(sms, 34).cpu().numpy().view(np.uint32).astype(np.uint64)
+        cycles = float(np.mean(words[:, 32] + (words[:, 33] << np.uint64(32))))
+        per_clk = 32.0 * iters / cycles  # warp-ATOMS per clock per SM (1024 threads = 32 warps)
+        out[name] = {"warp_atoms_per_clk_per_sm": per_clk,
+                     "gatomic_s": per_clk * 32 * sms * sm_mhz * 1e6 / 1e9,
+                     "gatomic_s_event_timed": n / (e0.elapsed_time(e1) / 1e3) / 1e9}
+    return out
+
+
+def vote_roofline(kernel, votes, vote_ms, atom, workload):
+    rate = votes / (vote_ms / 1e3) / 1e9
+    peak = atom["conflict_free"]["gatomic_s"]
+    return {"kernel": kernel, "bound": "smem_atomic", "achieved": rate, "peak": peak,
+            "unit": "Gatomic/s", "frac": rate / peak, "traffic": ncu_traffic(workload, kernel),
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + write.sum)",
+            "algorithmic": "E*n_theta votes per launch / mean launch time (CUDA events)",
+            "peak_source": "B5 in this run: %.3f warp-ATOMS/clk/SM x 32 lanes x SMs x %.0f MHz "
+                           "sampled SM clock" % (atom["conflict_free"]["warp_atoms_per_clk_per_sm"],
+                                                 atom["sm_mhz"])}
+
+
+def sobel_roofline(bytes_, ms, workload):
+    hbm = hbm_peak_gbs()
+    gbs = bytes_ / (ms / 1e3) / 1e9
+    return {"kernel": "sobel_binarize_compact_kernel", "bound": "hbm", "achieved": gbs,
+            "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+            "traffic": ncu_traffic(workload, "sobel_binarize_compact_kernel"),
+            "bytes_per_launch": bytes_,
+            "algorithmic": "sum over frames of W*H read + 4*E_f edge write + 4 count",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
 
 
 # ----------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and --impl reference)
 # ----------------------------------------------------------------------------
-def oracle_frames(name, first, budget_s, max_frames):
+def oracle_single_thread(name, frames, budget_s):
+    """The oracle on one host thread over the first frames of the batch, until
+    `budget_s` seconds of CPU work (at least 2 frames): frames/s."""
     import oracle
     cfg = synth.CONFIGS[name]
     c, s = synth.q15_table(cfg.n_theta)
-    frames = []
-    t_total = 0.0
-    n = 0
-    while n < max_frames and (t_total < budget_s or n < 2):
-        img = synth.gen_frame(name, first + n)
+    n, t = 0, 0.0
+    while n < len(frames) and (t < budget_s or n < 2):
         t0 = time.perf_counter()
-        oracle.detect(img, cfg.threshold, c, s, cfg.half_theta, cfg.half_rho, cfg.min_votes,
-                      cfg.k, want_binary=False, want_acc=False)
-        t_total += time.perf_counter() - t0
+        oracle.detect(frames[n], cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+                      cfg.min_votes, cfg.k, want_binary=False, want_acc=False)
+        t += time.perf_counter() - t0
         n += 1
-        frames.append(img)
-    return n, t_total
+    return n, t
 
 
 def run_reference(args, rank, world):
+    """The oracle as it stands, frame-parallel on the host cores, on the same
+    workload; every step is a bounded sample of the config's frames.  Under
+    torchrun rank 0 alone runs it."""
     if rank != 0:
         return
+    import oracle
     cfg = synth.CONFIGS[args.workload]
-    per_step = max(1, min(cfg.batch, 8 if cfg.width * cfg.height <= 2_100_000 else 1))
-    for i in range(args.warmup):
-        oracle_frames(args.workload, i * per_step, 0.0, per_step)
+    c, s = synth.q15_table(cfg.n_theta)
+    cores = oracle.host_cores()
+    big = cfg.width * cfg.height > 2_100_000
+    per_step = max(1, min(cfg.batch, 1 if big else 2 * cores))
+    frames = synth.gen_batch(args.workload, 0, per_step)
+
+    def one(f):
+        oracle.detect(frames[f], cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+                      cfg.min_votes, cfg.k, want_binary=False, want_acc=False)
+
+    for _ in range(args.warmup):
+        oracle.map_frames(one, range(per_step), cores)
     times = []
-    nfr = 0
-    for i in range(args.steps):
-        n, t = oracle_frames(args.workload, i * per_step, 0.0, per_step)
-        times.append(t)
-        nfr += n
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.map_frames(one, range(per_step), cores)
+        times.append(time.perf_counter() - t0)
     total = sum(times)
-    value = nfr / total
-    sample = "%d frames of %s per step (seeds from %d), single host thread, oracle -O2" % (
-        per_step, args.workload, synth.frame_seed(cfg, 0))
+    value = per_step * args.steps / total
+    sample = ("%d frames of %s per step (seeds from %d), oracle -O2 frame-parallel on %d host "
+              "threads" % (per_step, args.workload, synth.frame_seed(cfg, 0), min(cores, per_step)))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8/int32", "data": "synthetic",
+        "n_gpus": 0, "launched_with_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "none (host CPU)", "vs_baseline": None,
+        "dtype": "u8/int32", "data": "synthetic",
         "config": {"workload": args.workload, "frames_per_step": per_step,
                    "width": cfg.width, "height": cfg.height, "n_theta": cfg.n_theta},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+        "host": host_info(),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": min(cores, per_step),
+                         "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -187,56 +344,15 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------
-# roofline denominators
-# ----------------------------------------------------------------------------
-def vote_kernel_name(c, s):
-    """Which voting kernel libld.so picks for this table (label only): the
-    half-angle paired kernel for a symmetric table (C[n-t] = -C[t],
-    S[n-t] = S[t]) unless LD_VOTE_PAIRED=0."""
-    n = len(c)
-    sym = all(c[n - t] == -c[t] and s[n - t] == s[t] for t in range(1, n) if 2 * t != n)
-    return ("hough_vote_pairs_kernel" if sym and os.environ.get("LD_VOTE_PAIRED") != "0"
-            else "hough_vote_kernel")
-
-
-def smem_atomic_peaks():
-    """B5 microbenchmark (conflict-free / random / same-address red.shared.add.u32
-    on all SMs), measured in this run: Gatomic/s."""
-    import torch
-    from paper_2212_09460_b200 import ld
-    scratch = torch.empty((ld.ld_device_sm_count() * 2 * 32,), dtype=torch.int32, device="cuda")
-    atom = {}
-    for mode, name in ((0, "conflict_free"), (1, "random"), (2, "same_address")):
-        iters = 4096 if mode < 2 else 256
-        ld.ld_bench_smem_atomics(mode, iters, 1, scratch)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        n = ld.ld_bench_smem_atomics(mode, iters, 1, scratch)
-        e1.record()
-        torch.cuda.synchronize()
-        atom[name] = n / (e0.elapsed_time(e1) / 1e3) / 1e9  # Gatomic/s
-    return atom
-
-
-def hbm_peak_gbs():
-    """Measured HBM copy bandwidth (driver-written MEASURED_PEAKS.json), else the
-    profiling guide's fallback."""
-    peaks_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(peaks_file):
-        return float(json.load(open(peaks_file)).get("hbm_gbs", 6650.0))
-    return 6650.0
-
-
-# ----------------------------------------------------------------------------
-# our arm
+# our arm: batch configs (cfg1..cfg4)
 # ----------------------------------------------------------------------------
 def paper_latency(reps=50):
     """The paper's own measurement (Table 2): one 512x512 gray
     frame, pixel in -> Hough matrix (Sobel + binarize + compaction + voting,
     180 theta bins), here a synthetic cfg2-model road frame at 512x512 (the
-    paper's Fig. 9 image is not available).  Device-timed medians of single
-    launches: the paper's span, the span plus peaks, and the span plus peaks
-    with the H2D copy of the frame and the D2H of the peaks."""
+    paper's Fig. 9 image is not available).  Device-timed medians: the paper's
+    span, the span plus peaks, and with the H2D copy of the frame and the D2H of
+    the peaks; the two device-only spans also replayed from a CUDA graph."""
     import torch
     from paper_2212_09460_b200 import ld
     W = H = 512
@@ -250,6 +366,8 @@ def paper_latency(reps=50):
     counts = torch.empty((1,), dtype=torch.int32, device="cuda")
     n_rho = 2 * ld.ld_rho_offset(W, H) + 1
     acc = torch.empty((1, 180, n_rho), dtype=torch.int32, device="cuda")
+    hb = ld.ld_hough_hint_bytes(1, W, H, 180)
+    hint = torch.empty((hb,), dtype=torch.uint8, device="cuda")
     wsb = ld.ld_hough_peaks_workspace_bytes(1, 180, n_rho, 4)
     ws = torch.empty((wsb,), dtype=torch.uint8, device="cuda")
     pk = torch.empty((1, 4, 3), dtype=torch.int32, device="cuda")
@@ -262,45 +380,38 @@ def paper_latency(reps=50):
         if copy:
             gray.copy_(host, non_blocking=True)
         ld.ld_sobel_binarize(gray, img, 200, None, edges, stride, counts, stream)
-        ld.ld_hough_accumulate(edges, counts, stride, 1, W, H, 180, c, s, acc, stream)
+        ld.ld_hough_accumulate_hint(edges, counts, stride, 1, W, H, 180, c, s, acc, hint, hb,
+                                    stream)
         if peaks:
-            ld.ld_hough_peaks(acc, 1, 180, n_rho, 2, 29, 1, 4, pk, npk, ws, wsb, stream)
+            ld.ld_hough_peaks_hinted(acc, 1, 180, n_rho, 2, 29, 1, 4, hint, hb, pk, npk, ws, wsb,
+                                     stream)
         if copy:
             pk_host.copy_(pk, non_blocking=True)
 
-    out = {}
-    for name, pk_on, cp in (("paper_span_ms", False, False), ("with_peaks_ms", True, False),
-                            ("with_h2d_d2h_ms", True, True)):
+    def timed(fn):
         ts = []
         for i in range(reps + 5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(st)
-            span(pk_on, cp)
+            fn()
             e1.record(st)
             torch.cuda.synchronize()
             if i >= 5:
                 ts.append(e0.elapsed_time(e1))
-        out[name] = float(np.median(ts))
-    # the same two spans replayed from a CUDA graph (launch overhead removed;
-    # the ABI calls are capturable: no host synchronisation inside)
+        return float(np.median(ts))
+
+    out = {}
+    for name, pk_on, cp in (("paper_span_ms", False, False), ("with_peaks_ms", True, False),
+                            ("with_h2d_d2h_ms", True, True)):
+        out[name] = timed(lambda: span(pk_on, cp))
     for name, pk_on in (("paper_span_graph_ms", False), ("with_peaks_graph_ms", True)):
         try:
             torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 span(pk_on, False, torch.cuda.current_stream())
-            ts = []
-            for i in range(reps + 5):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                torch.cuda.synchronize()
-                e0.record(st)
-                graph.replay()
-                e1.record(st)
-                torch.cuda.synchronize()
-                if i >= 5:
-                    ts.append(e0.elapsed_time(e1))
-            out[name] = float(np.median(ts))
+            out[name] = timed(graph.replay)
         except Exception as exc:  # capture unsupported: report why, keep the eager numbers
             out[name] = None
             out["graph_error"] = str(exc)[:200]
@@ -310,30 +421,57 @@ def paper_latency(reps=50):
     return out
 
 
-def run_ours(args, rank, world, local):
+def parity_and_baseline(args, frames, bufs0, cfg, c, s, cnt):
+    """Every frame of the timed batch re-computed by the oracle, frame-parallel
+    on all host cores, and compared (oracle.parity); the oracle's frame rate
+    there is the cpu_baseline, next to a bounded single-thread sample."""
+    import oracle
+    from oracle import parity
+    pk = bufs0.peaks.cpu().numpy()
+    npk = bufs0.npk.cpu().numpy()
+    acc = bufs0.acc
+
+    def get(f):
+        e = bufs0.edges[f, : int(cnt[f])].cpu().numpy().view(np.uint32)
+        return cnt[f], pk[f], npk[f], acc[f].cpu().numpy(), e
+
+    r = parity.check_batch(frames, cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+                           cfg.min_votes, cfg.k, get)
+    n1, t1 = oracle_single_thread(args.workload, frames, args.cpu_seconds)
+    par = {"frames": r["frames"], "ok": r["ok"], "mismatches": r["mismatches"],
+           "first_mismatch": r["first_mismatch"],
+           "compared": "edge count, edge set, accumulator, peaks (exact) of every frame of the "
+                       "timed batch vs oracle/ld_oracle.c"}
+    cpu = {"value": r["frames"] / r["seconds"], "unit": "frames/s", "cores": r["workers"],
+           "kind": "oracle",
+           "sample": "all %d frames of the timed %s batch, oracle -O2 frame-parallel on %d host "
+                     "threads (includes the comparison)" % (r["frames"], args.workload,
+                                                            r["workers"]),
+           "single_thread": {"value": n1 / t1, "unit": "frames/s", "cores": 1,
+                             "sample": "first %d frames, one thread" % n1},
+           **host_info()}
+    return par, cpu
+
+
+def run_batch(args, rank, world, dist):
     import torch
-    import torch.distributed as dist
+    from paper_2212_09460_b200 import dist as pdist
     from paper_2212_09460_b200 import ld
 
-    # one process per GPU; with fewer GPUs than ranks (plumbing checks with the
-    # gloo backend only) ranks share devices round-robin
-    dev = local % max(torch.cuda.device_count(), 1)
-    torch.cuda.set_device(dev)
-    if world > 1:
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        else:
-            dist.init_process_group("gloo")
     cfg = synth.CONFIGS[args.workload]
-    if args.workload == "cfg5":
-        if args.shard == "theta":
-            return run_theta(args, rank, world, local)
-        return run_banded(args, rank, world, local)
-    B = args.frames or cfg.batch
+    B_global = args.frames or cfg.batch
+    replicas = cfg.batch == 1 and args.frames is None  # cfg1/cfg2: a single frame, no shard
+    if replicas or args.scaling == "weak":
+        first, B = rank * B_global, B_global
+        scaling = "weak"
+    else:
+        first, B = pdist.frame_shard(B_global, rank, world)
+        scaling = "strong"
+    if B < 1:
+        raise SystemExit("rank %d has no frames (batch %d over %d ranks)" % (rank, B_global, world))
+    frames_total = B * world if scaling == "weak" else B_global
     W, H = cfg.width, cfg.height
     c, s = synth.q15_table(cfg.n_theta)
-    first = rank * B  # weak scaling: every rank owns B frames of its own
-
     frames = synth.gen_batch(args.workload, first, B)
     pitch = ld._round_up(W, 16)
     host = torch.zeros((B, H, pitch), dtype=torch.uint8)
@@ -365,9 +503,6 @@ def run_ours(args, rank, world, local):
             self.peaks = torch.empty((B, cfg.k, 3), dtype=torch.int32, device="cuda")
             self.npk = torch.empty((B,), dtype=torch.int32, device="cuda")
 
-    # steps go round-robin to `--streams` streams with a buffer set each (a
-    # serving pipeline's double buffering): step i+1's Sobel can run while
-    # step i's peak search still streams its accumulators
     bufs = [Buffers(stream if i == 0 else torch.cuda.Stream()) for i in range(args.streams)]
     launches = [0]
 
@@ -405,8 +540,7 @@ def run_ours(args, rank, world, local):
     for i in range(max(args.warmup, len(bufs))):
         step(bufs[i % len(bufs)])
     torch.cuda.synchronize()
-    counts, acc, peaks = bufs[0].counts, bufs[0].acc, bufs[0].peaks
-    cnt = counts.cpu().numpy().astype(np.int64)
+    cnt = bufs[0].counts.cpu().numpy().astype(np.int64)
     votes = int(cnt.sum()) * cfg.n_theta
     if args.profile:
         for i in range(args.steps):
@@ -443,7 +577,7 @@ def run_ours(args, rank, world, local):
     gpu_launches = launches[0]
     elapsed_ms = float(e_start.elapsed_time(e_end))
     # (2) per-kernel times: the same K steps serialised on one stream with
-    # CUDA events between the kernels (the roofline's launch durations)
+    # CUDA events between the kernels (the rooflines' launch durations)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     torch.cuda.synchronize()
     for i in range(args.steps):
@@ -454,29 +588,21 @@ def run_ours(args, rank, world, local):
                       for i in range(args.steps)])  # ms
     serial_ms = float(evs[0][0].elapsed_time(evs[-1][3])) / args.steps
     for bf in bufs[1:]:  # every buffer set computed the same result
-        assert torch.equal(bf.peaks, peaks) and torch.equal(bf.npk, bufs[0].npk)
+        assert torch.equal(bf.peaks, bufs[0].peaks) and torch.equal(bf.npk, bufs[0].npk)
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    vt = torch.tensor([votes], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        vt = torch.tensor([votes], dtype=torch.float64, device="cuda")
         dist.all_reduce(vt, op=dist.ReduceOp.SUM)
-        total_votes = float(vt.item())
-    else:
-        total_votes = float(votes)
+    total_votes = float(vt.item())
     max_ms = float(t.item())
     ms_per_step = max_ms / args.steps
-    frames_total = B * world
     value = frames_total / (ms_per_step / 1e3)
-
-    # parity spot check of this run against the oracle is in tests/; here only
-    # the vote-conservation invariant on the timed output (cheap, on device)
-    sums = acc.view(B, -1).sum(dim=1, dtype=torch.int64).cpu().numpy()
-    assert np.array_equal(sums, cnt * cfg.n_theta), "vote conservation violated"
 
     e2e = None
     if not args.no_e2e:
         hd = ld.HostDetector(W, H, B, cfg.n_theta, c, s, cfg.threshold, cfg.k, cfg.half_theta,
-                             cfg.half_rho, cfg.min_votes, chunk_frames=32)
+                             cfg.half_rho, cfg.min_votes, chunk_frames=min(32, B))
         for _ in range(2):
             hd(host)
         if world > 1:
@@ -488,262 +614,100 @@ def run_ours(args, rank, world, local):
         et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d = B * H * pitch
         e2e = {"value": frames_total / float(et.item()), "unit": "frames/s",
-               "h2d_bytes_per_step": B * H * pitch,
-               "d2h_bytes_per_step": B * (cfg.k * 12 + 4 + 4),
-               "path": "ld_detect_batch_host (pinned host frames, chunks of 32)"}
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": B * (cfg.k * 12 + 8) * world,
+               "h2d_gbs_per_gpu": h2d / float(et.item()) / 1e9,
+               "path": "ld_detect_batch_host (pinned host frames, chunks of %d, copies on a "
+                       "second stream overlapping the kernels)" % min(32, B)}
+
+    par = cpu = None
+    if world == 1 and not args.no_parity and not f64:
+        par, cpu = parity_and_baseline(args, frames, bufs[0], cfg, c, s, cnt)
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
         return
-
-    atom = smem_atomic_peaks()
-
+    atom = smem_atomic_peaks(clocks.get("sm_mhz") if clocks else None)
     sob_ms, vote_ms, peak_ms = (float(stage[:, j].mean()) for j in range(3))
     sobel_bytes = B * (W * H + 4) + 4 * int(cnt.sum())
-    vote_rate = votes / (vote_ms / 1e3) / 1e9
-    peaks_bytes = B * cfg.n_theta * n_rho * 4
-    roofline = {"kernel": "hough_vote_f64_kernel" if f64 else vote_kernel_name(c, s),
-                "bound": "smem_atomic",
-                "achieved": vote_rate, "peak": atom["conflict_free"], "unit": "Gatomic/s",
-                "frac": vote_rate / atom["conflict_free"], "traffic": None,
-                "peak_source": "B5 microbenchmark (conflict-free red.shared.add.u32, all SMs), "
-                               "measured in this run"}
-    hbm_peak = hbm_peak_gbs()
-    sobel_gbs = sobel_bytes / (sob_ms / 1e3) / 1e9
-    cpu = None
-    if not args.no_cpu_baseline and world == 1 and not f64:
-        n, tcpu = oracle_frames(args.workload, 0, args.cpu_seconds, B)
-        cpu = {"value": n / tcpu, "unit": "frames/s", "cores": 1, "kind": "oracle",
-               "sample": "first %d frames of %s (same seeds as the GPU batch), single thread, "
-                         "detect without binary/acc export" % (n, args.workload)}
+    vkern = "hough_vote_f64_kernel" if f64 else vote_kernel_name(c, s)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8/int32", "data": "synthetic",
-        "config": {"workload": args.workload, "frames_per_gpu": B, "global_batch": frames_total,
-                   "width": W, "height": H, "threshold": cfg.threshold, "n_theta": cfg.n_theta,
-                   "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
-                   "parallelism": "frame-shard dp%d" % world,
-                   "peak_hint": use_hint,
-                   "trig": args.trig,
-                   "streams": args.streams,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "u8/int32", "data": "synthetic (BASELINE.json generator recipes, DESIGN.md 5)",
+        "config": {"workload": args.workload, "global_batch": frames_total,
+                   "frames_per_gpu": B, "width": W, "height": H, "threshold": cfg.threshold,
+                   "n_theta": cfg.n_theta, "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
+                   "parallelism": ("replicas x%d" % world if replicas else
+                                   "frame-shard dp%d (%s)" % (world, scaling)),
+                   "dist_backend": args.dist_backend if world > 1 else None,
+                   "peak_hint": use_hint, "trig": args.trig, "streams": args.streams,
                    "ms_per_step_one_stream": serial_ms,
-                   "l2": "inputs %.0f MB + accumulators %.0f MB per GPU exceed L2 (%.0f MB); no flush"
-                         % (B * H * pitch / 1e6, peaks_bytes / 1e6, ld.ld_device_l2_bytes() / 1e6)},
+                   "l2": "inputs %.0f MB + accumulators %.0f MB per GPU vs L2 %.0f MB; no flush"
+                         % (B * H * pitch / 1e6, B * cfg.n_theta * n_rho * 4 / 1e6,
+                            ld.ld_device_l2_bytes() / 1e6),
+                   "input_sha256": synth.sha256(frames),
+                   "trig_sha256": trig_hash(c, s)},
         "gvotes_per_s": total_votes / (ms_per_step / 1e3) / 1e9,
         "edges_per_frame": float(cnt.mean()),
         "stages_ms": {"sobel_binarize_compact": sob_ms, "hough_vote": vote_ms,
                       "hough_peaks": peak_ms},
-        "roofline": roofline,
-        "roofline_sobel": {"kernel": "sobel_binarize_compact_kernel", "bound": "hbm",
-                           "achieved": sobel_gbs, "peak": hbm_peak, "unit": "GB/s",
-                           "frac": sobel_gbs / hbm_peak, "traffic": None,
-                           "bytes_per_launch": sobel_bytes},
-        "smem_atomic_peaks_gatomic_s": atom,
+        "roofline": vote_roofline(vkern, votes, vote_ms, atom, args.workload),
+        "roofline_sobel": sobel_roofline(sobel_bytes, sob_ms, args.workload),
+        "smem_atomic_peaks": atom,
         "latency_512x512": paper_latency() if not args.no_e2e else None,
         "clocks": clocks,
         "gpu_launches": gpu_launches,
         "e2e": e2e,
+        "parity": par,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
-def run_banded(args, rank, world, local):
-    """cfg5: one 4096^2 image in row bands over the ranks, partial accumulators
-    summed by NCCL all_reduce inside the timed region (strong scaling)."""
+# ----------------------------------------------------------------------------
+# our arm: cfg5 (one 4096^2 image over the ranks)
+# ----------------------------------------------------------------------------
+def run_cfg5(args, rank, world, dist):
+    """Row bands (+ NCCL all_reduce of the accumulator) or theta shards (+
+    all_gather of the band edge bitmaps and of the per-rank top-k), strong
+    scaling; the result is identical on every rank and equal to the oracle's."""
     import torch
-    import torch.distributed as dist
     from paper_2212_09460_b200 import dist as pdist
-    from paper_2212_09460_b200 import ld
 
     cfg = synth.CONFIGS[args.workload]
     W, H = cfg.width, cfg.height
     c, s = synth.q15_table(cfg.n_theta)
     img = synth.gen_frame(args.workload, 0)  # replicated input, outside the timed region
-    det = pdist.BandedDetector(W, H, cfg.n_theta, c, s, cfg.threshold, cfg.k, cfg.half_theta,
-                               cfg.half_rho, cfg.min_votes, rank, world)
+    theta = args.shard == "theta"
+    Det = pdist.ThetaShardedDetector if theta else pdist.BandedDetector
+    det = Det(W, H, cfg.n_theta, c, s, cfg.threshold, cfg.k, cfg.half_theta, cfg.half_rho,
+              cfg.min_votes, rank, world)
     det.load(img)
     stream = torch.cuda.current_stream()
-    p = det.plan
+    names = (["sobel_binarize_compact", "edge_exchange", "hough_vote", "hough_peaks",
+              "topk_merge"] if theta else
+             ["sobel_binarize_compact", "hough_vote", "allreduce", "hough_peaks"])
+    nmarks = len(names) + 1
     launches = [0]
 
     def step(ev=None):
-        mark = (lambda j: ev[j].record(stream)) if ev is not None else (lambda j: None)
-        mark(0)
-        if p.rows > 0:
-            ld.ld_sobel_binarize(det.gray, det.img, cfg.threshold, None, det.edges,
-                                 det.edge_stride, det.count, stream)
-            launches[0] += ld.ld_last_launch_count()
-        else:
-            det.count.zero_()
-        mark(1)
-        if det.hint is not None:  # one rank: the whole accumulator, the hint is valid
-            ld.ld_hough_accumulate_hint(det.edges, det.count, det.edge_stride, 1, W, H,
-                                        cfg.n_theta, c, s, det.acc, det.hint, det.hint_bytes,
-                                        stream)
-        else:
-            ld.ld_hough_accumulate(det.edges, det.count, det.edge_stride, 1, W, H, cfg.n_theta,
-                                   c, s, det.acc, stream)
-        launches[0] += ld.ld_last_launch_count()
-        mark(2)
-        pdist.allreduce_accumulator(det.acc)
-        mark(3)
-        if det.hint is not None:
-            ld.ld_hough_peaks_hinted(det.acc, 1, cfg.n_theta, det.n_rho, cfg.half_theta,
-                                     cfg.half_rho, cfg.min_votes, cfg.k, det.hint,
-                                     det.hint_bytes, det.peaks, det.n_peaks, det.ws, det.ws_bytes,
-                                     stream)
-        else:
-            ld.ld_hough_peaks(det.acc, 1, cfg.n_theta, det.n_rho, cfg.half_theta, cfg.half_rho,
-                              cfg.min_votes, cfg.k, det.peaks, det.n_peaks, det.ws, det.ws_bytes,
-                              stream)
-        launches[0] += ld.ld_last_launch_count()
-        mark(4)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    my_edges = int(det.count.item())
-    ecount = torch.tensor([my_edges], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(ecount)
-    edges_total = int(ecount.item())
-    votes = edges_total * cfg.n_theta
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
-    if sampler:
-        sampler.start()
-        time.sleep(0.3)
-    launches[0] = 0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        step(evs[i])
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop() if sampler else None
-    stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(4)]
-                      for i in range(args.steps)])
-    t = torch.tensor([evs[0][0].elapsed_time(evs[-1][4])], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t.item()) / args.steps
-    # invariant on the reduced accumulator: every edge voted once per theta
-    assert int(det.acc.sum(dtype=torch.int64).item()) == votes, "vote conservation violated"
-
-    e2e = None
-    if not args.no_e2e:
-        host = torch.from_numpy(img[p.read_begin:p.read_end].copy()).pin_memory()
-        pk_host = torch.empty((1, cfg.k, 3), dtype=torch.int32).pin_memory()
-        for _ in range(2):
-            det.gray[:, :W].copy_(host, non_blocking=True)
-            det()
-            pk_host.copy_(det.peaks, non_blocking=True)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            det.gray[:, :W].copy_(host, non_blocking=True)
-            det()
-            pk_host.copy_(det.peaks, non_blocking=True)
-            torch.cuda.synchronize()
-        et = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64,
-                          device="cuda")
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": 1.0 / float(et.item()), "unit": "frames/s",
-               "h2d_bytes_per_step": int(host.numel()), "d2h_bytes_per_step": cfg.k * 12,
-               "path": "band rows from pinned host -> BandedDetector -> peaks to host"}
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-    atom = smem_atomic_peaks()
-    sob_ms, vote_ms, ar_ms, peak_ms = (float(stage[:, j].mean()) for j in range(4))
-    my_votes = my_edges * cfg.n_theta
-    vote_rate = my_votes / (vote_ms / 1e3) / 1e9
-    sobel_bytes = p.rows * W + 4 * my_edges + 4
-    hbm = hbm_peak_gbs()
-    cpu = None
-    if not args.no_cpu_baseline and world == 1:
-        n, tcpu = oracle_frames(args.workload, 0, args.cpu_seconds, 1)
-        cpu = {"value": n / tcpu, "unit": "frames/s", "cores": 1, "kind": "oracle",
-               "sample": "the cfg5 image (seed 3), whole detect, single thread"}
-    line = {
-        "metric": METRIC, "value": 1e3 / ms_per_step, "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u8/int32", "data": "synthetic",
-        "config": {"workload": "cfg5", "width": W, "height": H, "threshold": cfg.threshold,
-                   "n_theta": cfg.n_theta, "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
-                   "parallelism": "row-band x%d + %s all_reduce(SUM) of %d B" %
-                                  (world, args.dist_backend.upper(), det.acc.numel() * 4),
-                   "l2": "single image (16.8 MB) + acc (47.5 MB) fit in L2: latency measurement"},
-        "gvotes_per_s": votes / (ms_per_step / 1e3) / 1e9,
-        "edges_total": edges_total,
-        "stages_ms": {"sobel_binarize_compact": sob_ms, "hough_vote": vote_ms,
-                      "allreduce": ar_ms, "hough_peaks": peak_ms},
-        "roofline": {"kernel": vote_kernel_name(c, s), "bound": "smem_atomic", "achieved": vote_rate,
-                     "peak": atom["conflict_free"], "unit": "Gatomic/s",
-                     "frac": vote_rate / atom["conflict_free"], "traffic": None,
-                     "peak_source": "B5 microbenchmark measured in this run"},
-        "roofline_sobel": {"kernel": "sobel_binarize_compact_kernel", "bound": "hbm",
-                           "achieved": sobel_bytes / (sob_ms / 1e3) / 1e9, "peak": hbm,
-                           "unit": "GB/s", "frac": sobel_bytes / (sob_ms / 1e3) / 1e9 / hbm,
-                           "traffic": None, "bytes_per_launch": sobel_bytes},
-        "smem_atomic_peaks_gatomic_s": atom,
-        "clocks": clocks,
-        "gpu_launches": launches[0],
-        "e2e": e2e,
-        "cpu_baseline": cpu,
-    }
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-
-
-def run_theta(args, rank, world, local):
-    """cfg5 theta-sharded: Sobel on the row band, edge
-    lists all-gathered, every rank votes all edges into its theta shard (+halo
-    rows), peaks of its own rows, top-k lists all-gathered and merged on the
-    device.  Strong scaling; the result is identical on every rank."""
-    import torch
-    import torch.distributed as dist
-    from paper_2212_09460_b200 import dist as pdist
-
-    cfg = synth.CONFIGS[args.workload]
-    W, H = cfg.width, cfg.height
-    c, s = synth.q15_table(cfg.n_theta)
-    img = synth.gen_frame(args.workload, 0)
-    det = pdist.ThetaShardedDetector(W, H, cfg.n_theta, c, s, cfg.threshold, cfg.k,
-                                     cfg.half_theta, cfg.half_rho, cfg.min_votes, rank, world)
-    det.load(img)
-    stream = torch.cuda.current_stream()
-    launches = [0]
-
-    def step(ev=None):
-        det((lambda j: ev[j].record(stream)) if ev is not None else None)
+        det(mark=(lambda j: ev[j].record(stream)) if ev is not None else None)
         launches[0] += det.launches
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    my_edges = int(det.band.count.item())
+    band = det.band if theta else det
+    my_edges = int(band.count.item())
     ecount = torch.tensor([my_edges], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ecount)
     edges_total = int(ecount.item())
     votes = edges_total * cfg.n_theta
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nmarks)]
+           for _ in range(args.steps)]
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -758,79 +722,129 @@ def run_theta(args, rank, world, local):
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
-    stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(5)]
+    stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(nmarks - 1)]
                       for i in range(args.steps)])
-    t = torch.tensor([evs[0][0].elapsed_time(evs[-1][5])], dtype=torch.float64, device="cuda")
+    t = torch.tensor([evs[0][0].elapsed_time(evs[-1][nmarks - 1])], dtype=torch.float64,
+                     device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
-    # invariant on the shard accumulator: every edge voted once per slice row
-    slice_rows = det.g1 - det.g0
-    assert int(det.acc.sum(dtype=torch.int64).item()) == edges_total * slice_rows, \
-        "vote conservation violated"
-
+    peaks, npk = det.result
+    # parity of the timed result against the whole-image oracle (rank 0 at N=1;
+    # the GPU tests cover N = 2/4/8 with every rank emulated)
+    par = cpu = None
+    if rank == 0 and world == 1 and not args.no_parity:
+        import oracle
+        t0 = time.perf_counter()
+        want = oracle.detect(img, cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+                             cfg.min_votes, cfg.k, want_binary=False)
+        dt = time.perf_counter() - t0
+        acc_ok = (None if theta else
+                  bool(np.array_equal(det.acc.cpu().numpy().view(np.uint32)[0], want["acc"])))
+        got = [tuple(int(v) for v in p) for p in peaks.reshape(-1, 3).cpu().numpy()]
+        got = [(a, b_, int(np.uint32(np.int32(v)))) for a, b_, v in got][: int(npk.reshape(-1)[0])]
+        wp = [(int(p["theta_bin"]), int(p["rho_bin"]), int(p["votes"]))
+              for p in want["peaks"][: want["n_peaks"]]]
+        ok = edges_total == want["n_edges"] and got == wp and acc_ok is not False
+        par = {"frames": 1, "ok": ok, "mismatches": 0 if ok else 1,
+               "first_mismatch": None if ok else "edges %d/%d peaks %s vs %s" % (
+                   edges_total, want["n_edges"], got[:3], wp[:3]),
+               "compared": "edge count, %speaks vs oracle" % ("" if theta else "accumulator, ")}
+        cpu = {"value": 1.0 / dt, "unit": "frames/s", "cores": 1, "kind": "oracle",
+               "sample": "the cfg5 image (seed 3), whole detect, one thread (a single frame "
+                         "does not split across cores)", **host_info()}
     e2e = None
     if not args.no_e2e:
-        p = det.band.plan
+        p = band.plan
         host = torch.from_numpy(img[p.read_begin:p.read_end].copy()).pin_memory()
-        pk_host = torch.empty((1, cfg.k, 3), dtype=torch.int32).pin_memory()
+        pk_host = torch.empty((cfg.k, 3), dtype=torch.int32).pin_memory()
         times = []
         for i in range(args.steps + 2):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            det.band.gray[:, :W].copy_(host, non_blocking=True)
-            pk, _ = det()
-            pk_host.copy_(pk, non_blocking=True)
+            band.gray[:, :W].copy_(host, non_blocking=True)
+            det()
+            pk_host.copy_(det.result[0].reshape(cfg.k, 3), non_blocking=True)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
         et = torch.tensor([sum(times[2:]) / args.steps], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": 1.0 / float(et.item()), "unit": "frames/s",
-               "h2d_bytes_per_step": int(host.numel()), "d2h_bytes_per_step": cfg.k * 12,
-               "path": "band rows from pinned host -> ThetaShardedDetector -> peaks to host"}
+               "h2d_bytes_per_step": int(host.numel()) * world,
+               "d2h_bytes_per_step": cfg.k * 12 * world,
+               "path": "band rows from pinned host -> %s -> peaks to host" % Det.__name__}
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
         return
-    atom = smem_atomic_peaks()
-    sob_ms, xch_ms, vote_ms, peak_ms, merge_ms = (float(stage[:, j].mean()) for j in range(5))
-    my_votes = edges_total * slice_rows
-    vote_rate = my_votes / (vote_ms / 1e3) / 1e9
+    atom = smem_atomic_peaks(clocks.get("sm_mhz") if clocks else None)
+    if theta:
+        my_votes = edges_total * (det.g1 - det.g0)
+        vkern = vote_kernel_name(det.cos_s, det.sin_s)
+        par_desc = "theta-shard x%d (+%d halo rows) + %s all_gather of band edge bitmaps" % (
+            world, cfg.half_theta, args.dist_backend.upper())
+    else:
+        my_votes = my_edges * cfg.n_theta
+        vkern = vote_kernel_name(c, s)
+        par_desc = "row-band x%d + %s all_reduce(SUM) of %d B" % (
+            world, args.dist_backend.upper(), det.acc.numel() * 4)
+    sm = {n: float(stage[:, j].mean()) for j, n in enumerate(names)}
+    sobel_bytes = band.plan.rows * W + 4 * my_edges + 4
     line = {
         "metric": METRIC, "value": 1e3 / ms_per_step, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u8/int32", "data": "synthetic",
+        "dtype": "u8/int32", "data": "synthetic (BASELINE.json generator recipe, DESIGN.md 5)",
         "config": {"workload": "cfg5", "width": W, "height": H, "threshold": cfg.threshold,
                    "n_theta": cfg.n_theta, "k": cfg.k, "window": [cfg.half_theta, cfg.half_rho],
-                   "parallelism": "theta-shard x%d (+%d halo rows) + %s all_gather of edge lists"
-                                  % (world, cfg.half_theta, args.dist_backend.upper()),
-                   "l2": "single image (16.8 MB) + acc slice fit in L2: latency measurement"},
+                   "parallelism": par_desc,
+                   "dist_backend": args.dist_backend if world > 1 else None,
+                   "l2": "single image (16.8 MB) + acc (47.5 MB) fit in L2: latency measurement",
+                   "input_sha256": synth.sha256(img), "trig_sha256": trig_hash(c, s)},
         "gvotes_per_s": votes / (ms_per_step / 1e3) / 1e9,
         "edges_total": edges_total,
-        "stages_ms": {"sobel_binarize_compact": sob_ms, "edge_allgather": xch_ms,
-                      "hough_vote": vote_ms, "hough_peaks": peak_ms, "topk_merge": merge_ms},
-        "roofline": {"kernel": vote_kernel_name(det.cos_s, det.sin_s), "bound": "smem_atomic", "achieved": vote_rate,
-                     "peak": atom["conflict_free"], "unit": "Gatomic/s",
-                     "frac": vote_rate / atom["conflict_free"], "traffic": None,
-                     "peak_source": "B5 microbenchmark measured in this run"},
-        "smem_atomic_peaks_gatomic_s": atom,
+        "stages_ms": sm,
+        "roofline": vote_roofline(vkern, my_votes, sm["hough_vote"], atom, "cfg5"),
+        "roofline_sobel": sobel_roofline(sobel_bytes, sm["sobel_binarize_compact"], "cfg5"),
+        "smem_atomic_peaks": atom,
         "clocks": clocks,
         "gpu_launches": launches[0],
         "e2e": e2e,
-        "cpu_baseline": None,
+        "parity": par,
+        "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    # one process per GPU; with fewer GPUs than ranks (plumbing checks with the
+    # gloo backend only) ranks share devices round-robin
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.destroy_process_group()
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    try:
+        if args.workload == "cfg5":
+            run_cfg5(args, rank, world, dist)
+        else:
+            run_batch(args, rank, world, dist)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
 
 
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

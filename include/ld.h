@@ -161,6 +161,19 @@ int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
                             int32_t height, int32_t n_theta, const double *cos_f64,
                             const double *sin_f64, uint32_t *acc, void *stream);
 
+/* ld_hough_accumulate / ld_hough_accumulate_hint (below) with options:
+ *  flags : 0, or LD_VOTE_PLAIN -- use the unpaired voting kernel even for a
+ *          symmetric table (the half-angle pairing of Eq. 4-5 is otherwise
+ *          chosen automatically; both give identical accumulators).  Any other
+ *          bit: LD_ERR_INVALID_ARG.
+ *  hint  : nullable; as ld_hough_accumulate_hint when given. */
+#define LD_VOTE_PLAIN 1u
+int ld_hough_accumulate_opt(const uint32_t *edge_xy, const uint32_t *edge_count,
+                            int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
+                            int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
+                            uint32_t flags, uint32_t *acc, void *hint, size_t hint_bytes,
+                            void *stream);
+
 /* Step 4 ("picking the line with the most pixel value"), made
  * deterministic (DESIGN R13, R14): key(t, r) = (acc[t][r], -t, -r),
  * lexicographic.  (t, r) is a peak candidate iff acc[t][r] >= max(1, min_votes)
@@ -205,8 +218,12 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
  * the candidate definition above (a full window test on acc): verified cells
  * are distinct candidates, so the value of the k-th verified one is a lower
  * bound on the frame's k-th best candidate, and the search starts from it
- * instead of min_votes.  peaks / n_peaks are bit-identical to
- * ld_hough_peaks.  The hint must come from the ld_hough_accumulate_hint call
+ * instead of min_votes.  While each band is in shared memory the voting
+ * kernel also records the maximum of every 32-cell segment of every row; with
+ * a certified bound the search then only reads those maxima and tests the
+ * cells of the segments that reach the bound (the sparse search, DESIGN R30),
+ * falling back to the full search for a frame whose bound is not certified.
+ * peaks / n_peaks are bit-identical to ld_hough_peaks.  The hint must come from the ld_hough_accumulate_hint call
  * that produced acc; a hint whose header (written by that call) does not
  * match batch, n_theta and n_rho is ignored.
  *  hint : device, >= ld_hough_hint_bytes(batch, width, height, n_theta),
@@ -222,6 +239,27 @@ int ld_hough_peaks_hinted(const uint32_t *acc, int32_t batch, int32_t n_theta, i
                           int32_t k, const void *hint, size_t hint_bytes, ld_peak *peaks,
                           int32_t *n_peaks, void *workspace, size_t workspace_bytes,
                           void *stream);
+
+/* The peak search with every option (ld_hough_peaks, _ex and _hinted are
+ * this call with defaults): candidate rows and theta offset as
+ * ld_hough_peaks_ex; hint nullable (as ld_hough_peaks_hinted; ignored for a
+ * restricted row range); flags select the search kernels -- every choice
+ * returns the same peaks:
+ *  LD_PEAKS_DENSE        : no sparse search (DESIGN R30) even with a hint
+ *  LD_PEAKS_FORCE_STREAM : the CTA streaming kernel instead of the warp kernel
+ *  LD_PEAKS_FORCE_TILE   : the tiled kernel (unrestricted searches only)
+ *  LD_PEAKS_FORCE_BAND   : the generic per-cell window scan
+ * Any other bit: LD_ERR_INVALID_ARG. */
+#define LD_PEAKS_DENSE 1u
+#define LD_PEAKS_FORCE_STREAM 2u
+#define LD_PEAKS_FORCE_TILE 4u
+#define LD_PEAKS_FORCE_BAND 8u
+int ld_hough_peaks_opt(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                       int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                       int32_t cand_row_begin, int32_t cand_row_end, int32_t theta_offset,
+                       const void *hint, size_t hint_bytes, uint32_t flags, ld_peak *peaks,
+                       int32_t *n_peaks, void *workspace, size_t workspace_bytes,
+                       void *stream);
 
 /* ---------------------------------------------------------------------------
  * Lanes module: Fig. 1 step 4, "draw the
@@ -316,6 +354,46 @@ int ld_detect_batch_host(const uint8_t *gray_host, const ld_image *img,
                          int32_t chunk_frames, void *workspace, size_t workspace_bytes,
                          void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU helpers of the theta-sharded path (DESIGN
+ * section 8; the paper's theta partitioning, lifted across GPUs).  All
+ * device-side: no host synchronisation, fixed-size buffers for collectives.
+ * ------------------------------------------------------------------------- */
+#define LD_MAX_BLOCKS 64 /* row blocks (ranks) of one bitmap */
+
+/* Words of a row-band edge bitmap: rows * ceil(width / 32) uint32. */
+int64_t ld_edge_bitmask_words(int32_t width, int32_t rows);
+
+/* The edge set of one row band as a bitmap: bits [rows][ceil(width/32)]
+ * (device, 16-B aligned, fully overwritten); bit (x & 31) of word
+ * [y - row_begin][x >> 5] is set iff edge (y << 16) | x is in
+ * edge_xy[0 .. *edge_count) (device count) and row_begin <= y < row_begin + rows.
+ * 1 <= width <= LD_MAX_DIM, rows >= 1. */
+int ld_edges_to_bitmask(const uint32_t *edge_xy, const uint32_t *edge_count, int32_t width,
+                        int32_t row_begin, int32_t rows, uint32_t *bits, void *stream);
+
+/* The union of n_blocks band bitmaps back to one edge list (order
+ * unspecified, a set: DESIGN R15).  bits: device [n_blocks][block_stride_rows]
+ * [ceil(width/32)] (the layout an all_gather of equal-size band bitmaps
+ * produces); block b holds global rows block_row_begin[b] ..
+ * + block_rows[b] - 1 (HOST arrays, block_rows[b] <= block_stride_rows).
+ * edge_count (device) receives the number of edges; entries beyond
+ * edge_capacity are not written (size the list by the rows: capacity >=
+ * sum(block_rows) * width makes overflow impossible).
+ * 1 <= n_blocks <= LD_MAX_BLOCKS. */
+int ld_bitmask_to_edges(const uint32_t *bits, int32_t width, int32_t n_blocks,
+                        const int32_t *block_row_begin, const int32_t *block_rows,
+                        int32_t block_stride_rows, uint32_t *edge_xy, int64_t edge_capacity,
+                        uint32_t *edge_count, void *stream);
+
+/* The global top k of n_lists top-k lists (peaks [n_lists][k] and n_peaks
+ * [n_lists], device; theta_bin global, e.g. the all-gathered results of
+ * ld_hough_peaks_ex on theta slices) by the key (votes, -theta, -rho) of
+ * DESIGN R14: out [k] (sentinel-filled) and n_out [1], device.  Requires
+ * n_lists * k <= 16384 (one CTA sorts them in shared memory). */
+int ld_merge_peak_lists(const ld_peak *peaks, const int32_t *n_peaks, int32_t n_lists,
+                        int32_t k, int32_t n_rho, ld_peak *out, int32_t *n_out, void *stream);
+
 /* B5 microbenchmark of the shared-memory atomic pipe (the roofline of the
  * voting stage).  Launches one CTA per SM x blocks_per_sm, each thread issuing
  * `iters` red.shared.add.u32 with the given address pattern:
@@ -323,7 +401,9 @@ int ld_detect_batch_host(const uint8_t *gray_host, const ld_image *img,
  *   mode 1: pseudo-random addresses over a 48 K-word array
  *   mode 2: one address per warp (fully serialised)
  * *atomics_out (host) receives the total atomics issued.  scratch: device,
- * >= 4 * grid * 32 bytes (per-CTA checksums). */
+ * >= 4 * grid * 34 bytes: per CTA 34 words, 32 checksum words then the clock64
+ * cycles of its timed loop (uint64, low word first), so the rate per clock per
+ * SM excludes the prologue and the checksum (grid = SMs x blocks_per_sm). */
 int ld_bench_smem_atomics(int32_t mode, int32_t iters, int32_t blocks_per_sm,
                           uint64_t *atomics_out, void *scratch, void *stream);
 

@@ -8,7 +8,6 @@
 #include <cstring>
 #include <mutex>
 
-#include <cstdlib>
 #include "ld_internal.cuh"
 
 namespace ld {
@@ -148,12 +147,9 @@ static int check_trig(int32_t n_theta, const int32_t *c, const int32_t *s, int32
 // Half-angle pairing (NEXT 2) is exact iff the table is symmetric,
 // C[n-t] = -C[t] and S[n-t] = S[t] for 0 < t < n, t != n/2; the unpaired rows
 // (t = 0, t = n/2) also vote their mirror (-C[t], S[t]) into a scratch row,
-// whose bins must pass the same corner range proof.  LD_VOTE_PAIRED=0
-// disables the paired kernel.
+// whose bins must pass the same corner range proof.
 static bool pairable_trig(int32_t n_theta, const int32_t *c, const int32_t *s, int32_t w,
                           int32_t h, int32_t d) {
-  const char *env = getenv("LD_VOTE_PAIRED");
-  if (env && env[0] == '0') return false;
   for (int t = 1; t < n_theta; ++t)
     if (2 * t != n_theta && (c[n_theta - t] != -c[t] || s[n_theta - t] != s[t])) return false;
   const int64_t n_rho = 2 * static_cast<int64_t>(d) + 1;
@@ -234,10 +230,22 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
   return LD_OK;
 }
 
+static size_t hint_keys_bytes(int32_t batch, int32_t n_theta) {
+  // the band count never exceeds n_theta
+  return sizeof(unsigned long long) * static_cast<size_t>(batch) * n_theta * HINT_MAX_RANGES;
+}
+
+static int32_t n_seg_of(int32_t n_rho) { return (n_rho + SEG_CELLS - 1) / SEG_CELLS; }
+
+static size_t hint_bytes(int32_t batch, int32_t n_theta, int32_t n_rho) {
+  return HINT_HDR_BYTES + hint_keys_bytes(batch, n_theta) +
+         sizeof(uint32_t) * static_cast<size_t>(batch) * n_theta * n_seg_of(n_rho);
+}
+
 static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
                       int32_t batch, int32_t width, int32_t height, int32_t n_theta,
                       const int32_t *cos_q15, const int32_t *sin_q15, uint32_t *acc,
-                      cudaStream_t stream, void *hint = nullptr) {
+                      cudaStream_t stream, void *hint = nullptr, uint32_t flags = 0) {
   DevInfo dev;
   int rc = device_info(&dev);
   if (rc) return rc;
@@ -246,7 +254,8 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   const int n_rho = 2 * d + 1;
   int ctas = 1, rpb = 0, n_bands = 0;
   size_t smem = 0;
-  const bool paired = pairable_trig(n_theta, cos_q15, sin_q15, width, height, d) &&
+  const bool paired = !(flags & LD_VOTE_PLAIN) &&
+                      pairable_trig(n_theta, cos_q15, sin_q15, width, height, d) &&
                       hough_plan_pairs(n_theta, n_rho, static_cast<size_t>(dev.smem_optin), &ctas,
                                        &rpb, &n_bands, &smem);
   if (!paired &&
@@ -269,8 +278,11 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   p.hint_hdr = static_cast<uint32_t *>(hint);
   p.hint_keys = hint ? reinterpret_cast<unsigned long long *>(static_cast<char *>(hint) + HINT_HDR_BYTES)
                      : nullptr;
+  p.segmax = hint ? reinterpret_cast<uint32_t *>(static_cast<char *>(hint) + HINT_HDR_BYTES +
+                                                 hint_keys_bytes(batch, n_theta))
+                  : nullptr;
+  p.n_seg = n_seg_of(n_rho);
   p.n_pairs = paired ? hough_pair_count(n_theta) : 0;
-  p.pair_delta = static_cast<uint32_t>(rpb) * static_cast<uint32_t>(n_rho) * 4u;
   cudaError_t e = paired ? launch_hough_pairs(p, trig, ctas, smem, stream)
                          : launch_hough(p, trig, ctas, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");
@@ -281,7 +293,7 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
                       int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
                       ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t ws_bytes,
                       cudaStream_t stream, int32_t cand_t0 = 0, int32_t cand_t1 = -1,
-                      int32_t theta_offset = 0, const void *hint = nullptr) {
+                      int32_t theta_offset = 0, const void *hint = nullptr, uint32_t flags = 0) {
   PeaksParams p;
   p.acc = acc;
   p.batch = batch;
@@ -299,14 +311,21 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   p.hint_keys = hint ? reinterpret_cast<const unsigned long long *>(static_cast<const char *>(hint) +
                                                                     HINT_HDR_BYTES)
                      : nullptr;
-  // workspace: [batch] uint32 per-frame thresholds (256-B padded), then the keys
-  p.gtau = static_cast<uint32_t *>(workspace);
-  p.band_keys = reinterpret_cast<unsigned long long *>(
-      static_cast<char *>(workspace) + align_up(sizeof(uint32_t) * static_cast<size_t>(batch), 256));
+  p.segmax = hint ? reinterpret_cast<const uint32_t *>(static_cast<const char *>(hint) +
+                                                       HINT_HDR_BYTES + hint_keys_bytes(batch, n_theta))
+                  : nullptr;
+  p.n_seg = n_seg_of(n_rho);
+  const PeaksLayout W = peaks_layout(batch, n_theta, n_rho, k);
+  char *ws = static_cast<char *>(workspace);
+  p.gtau = reinterpret_cast<uint32_t *>(ws + W.gtau);
+  p.resolved = reinterpret_cast<uint32_t *>(ws + W.resolved);
+  p.ncand = reinterpret_cast<uint32_t *>(ws + W.ncand);
+  p.cand = reinterpret_cast<unsigned long long *>(ws + W.cand);
+  p.band_keys = reinterpret_cast<unsigned long long *>(ws + W.keys);
   p.peaks = peaks;
   p.n_peaks = n_peaks;
   (void)ws_bytes;
-  cudaError_t e = launch_peaks(p, stream);
+  cudaError_t e = launch_peaks(p, flags, stream);
   if (e != cudaSuccess) return cuda_fail(e, "peaks kernels launch");
   return LD_OK;
 }
@@ -324,10 +343,6 @@ static int check_peaks_args(const uint32_t *acc, int32_t batch, int32_t n_theta,
   return LD_OK;
 }
 
-static size_t hint_bytes(int32_t batch, int32_t n_theta) {
-  // the band count never exceeds n_theta
-  return HINT_HDR_BYTES + sizeof(unsigned long long) * static_cast<size_t>(batch) * n_theta * HINT_MAX_RANGES;
-}
 
 struct DetectLayout {
   size_t counts_off, edges_off, acc_off, hint_off, peaks_off, total;
@@ -348,7 +363,7 @@ static DetectLayout detect_layout(const ld_image *img, int32_t n_theta, int32_t 
   L.acc_off = off;
   if (acc_ws) off = align_up(off + acc_bytes, 256);
   L.hint_off = off;
-  off = align_up(off + hint_bytes(img->batch, n_theta), 256);
+  off = align_up(off + hint_bytes(img->batch, n_theta, 2 * d + 1), 256);
   L.peaks_off = off;
   off = align_up(off + peaks_workspace_bytes(img->batch, n_theta, 2 * d + 1, k), 256);
   L.total = off;
@@ -416,19 +431,44 @@ int ld_sobel_binarize(const uint8_t *gray, const ld_image *img, int32_t threshol
                               stream);
 }
 
-int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
-                        int32_t batch, int32_t width, int32_t height, int32_t n_theta,
-                        const int32_t *cos_q15, const int32_t *sin_q15, uint32_t *acc,
-                        void *stream) {
-  g_launches = 0;
+static int check_vote_args(const uint32_t *edge_xy, const uint32_t *edge_count, const uint32_t *acc,
+                           int64_t edge_stride, int32_t batch, int32_t width, int32_t height) {
   if (!edge_xy || !edge_count || !acc) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
   if (batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
   if (width < 1 || height < 1 || width > LD_MAX_DIM || height > LD_MAX_DIM)
     return fail(LD_ERR_INVALID_ARG, "width/height outside [1, %d]", LD_MAX_DIM);
   if (!aligned(edge_xy, 16) || edge_stride < 0 || edge_stride % 4 != 0)
     return fail(LD_ERR_INVALID_ARG, "edge_xy must be 16-byte aligned and edge_stride a multiple of 4");
+  return LD_OK;
+}
+
+int ld_hough_accumulate_opt(const uint32_t *edge_xy, const uint32_t *edge_count,
+                            int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
+                            int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
+                            uint32_t flags, uint32_t *acc, void *hint, size_t hint_bytes_,
+                            void *stream) {
+  g_launches = 0;
+  int rc = check_vote_args(edge_xy, edge_count, acc, edge_stride, batch, width, height);
+  if (rc) return rc;
+  if (flags & ~static_cast<uint32_t>(LD_VOTE_PLAIN))
+    return fail(LD_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
+  if (n_theta < 1 || n_theta > LD_MAX_THETA)
+    return fail(LD_ERR_INVALID_ARG, "n_theta %d outside [1, %d]", n_theta, LD_MAX_THETA);
+  if (hint) {
+    const size_t need = hint_bytes(batch, n_theta, 2 * rho_offset(width, height) + 1);
+    if (!aligned(hint, 16) || hint_bytes_ < need)
+      return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned", need);
+  }
   return hough_impl(edge_xy, edge_count, edge_stride, batch, width, height, n_theta, cos_q15,
-                    sin_q15, acc, static_cast<cudaStream_t>(stream));
+                    sin_q15, acc, static_cast<cudaStream_t>(stream), hint, flags);
+}
+
+int ld_hough_accumulate(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
+                        int32_t batch, int32_t width, int32_t height, int32_t n_theta,
+                        const int32_t *cos_q15, const int32_t *sin_q15, uint32_t *acc,
+                        void *stream) {
+  return ld_hough_accumulate_opt(edge_xy, edge_count, edge_stride, batch, width, height, n_theta,
+                                 cos_q15, sin_q15, 0u, acc, nullptr, 0, stream);
 }
 
 int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
@@ -436,12 +476,8 @@ int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
                             int32_t n_theta, const double *cos_f64, const double *sin_f64,
                             uint32_t *acc, void *stream) {
   g_launches = 0;
-  if (!edge_xy || !edge_count || !acc) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
-  if (batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
-  if (width < 1 || height < 1 || width > LD_MAX_DIM || height > LD_MAX_DIM)
-    return fail(LD_ERR_INVALID_ARG, "width/height outside [1, %d]", LD_MAX_DIM);
-  if (!aligned(edge_xy, 16) || edge_stride < 0 || edge_stride % 4 != 0)
-    return fail(LD_ERR_INVALID_ARG, "edge_xy must be 16-byte aligned and edge_stride a multiple of 4");
+  const int rc0 = check_vote_args(edge_xy, edge_count, acc, edge_stride, batch, width, height);
+  if (rc0) return rc0;
   if (n_theta < 1 || n_theta > LD_MAX_THETA_F64)
     return fail(LD_ERR_INVALID_ARG, "n_theta %d outside [1, %d]", n_theta, LD_MAX_THETA_F64);
   if (!cos_f64 || !sin_f64) return fail(LD_ERR_INVALID_ARG, "trig table pointer is NULL");
@@ -494,42 +530,38 @@ int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
 
 size_t ld_hough_hint_bytes(int32_t batch, int32_t width, int32_t height, int32_t n_theta) {
   if (batch < 1 || width < 1 || height < 1 || n_theta < 1) return 0;
-  return hint_bytes(batch, n_theta);
+  return hint_bytes(batch, n_theta, 2 * rho_offset(width, height) + 1);
 }
 
 int ld_hough_accumulate_hint(const uint32_t *edge_xy, const uint32_t *edge_count,
                              int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
                              int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
                              uint32_t *acc, void *hint, size_t hint_bytes_, void *stream) {
-  g_launches = 0;
-  if (!edge_xy || !edge_count || !acc || !hint) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
-  if (batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
-  if (width < 1 || height < 1 || width > LD_MAX_DIM || height > LD_MAX_DIM)
-    return fail(LD_ERR_INVALID_ARG, "width/height outside [1, %d]", LD_MAX_DIM);
-  if (!aligned(edge_xy, 16) || edge_stride < 0 || edge_stride % 4 != 0)
-    return fail(LD_ERR_INVALID_ARG, "edge_xy must be 16-byte aligned and edge_stride a multiple of 4");
-  if (n_theta < 1 || n_theta > LD_MAX_THETA)
-    return fail(LD_ERR_INVALID_ARG, "n_theta %d outside [1, %d]", n_theta, LD_MAX_THETA);
-  if (!aligned(hint, 16) || hint_bytes_ < hint_bytes(batch, n_theta))
-    return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned", hint_bytes(batch, n_theta));
-  return hough_impl(edge_xy, edge_count, edge_stride, batch, width, height, n_theta, cos_q15,
-                    sin_q15, acc, static_cast<cudaStream_t>(stream), hint);
+  if (!hint) {
+    g_launches = 0;
+    return fail(LD_ERR_INVALID_ARG, "NULL hint");
+  }
+  return ld_hough_accumulate_opt(edge_xy, edge_count, edge_stride, batch, width, height, n_theta,
+                                 cos_q15, sin_q15, 0u, acc, hint, hint_bytes_, stream);
 }
 
 size_t ld_hough_peaks_workspace_bytes(int32_t batch, int32_t n_theta, int32_t n_rho, int32_t k) {
-  (void)n_rho;
   if (batch < 1 || n_theta < 1 || n_rho < 1 || k < 1) return 0;
   return peaks_workspace_bytes(batch, n_theta, n_rho, k);
 }
 
-int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
-                      int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
-                      int32_t cand_row_begin, int32_t cand_row_end, int32_t theta_offset,
-                      ld_peak *peaks, int32_t *n_peaks, void *workspace,
-                      size_t workspace_bytes, void *stream) {
+int ld_hough_peaks_opt(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                       int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                       int32_t cand_row_begin, int32_t cand_row_end, int32_t theta_offset,
+                       const void *hint, size_t hint_bytes_, uint32_t flags, ld_peak *peaks,
+                       int32_t *n_peaks, void *workspace, size_t workspace_bytes,
+                       void *stream) {
   g_launches = 0;
   int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
   if (rc) return rc;
+  if (flags & ~static_cast<uint32_t>(LD_PEAKS_DENSE | LD_PEAKS_FORCE_STREAM | LD_PEAKS_FORCE_TILE |
+                                     LD_PEAKS_FORCE_BAND))
+    return fail(LD_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
   if (cand_row_begin < 0 || cand_row_end < cand_row_begin || cand_row_end > n_theta)
     return fail(LD_ERR_INVALID_ARG, "candidate rows [%d, %d) outside [0, %d]", cand_row_begin,
                 cand_row_end, n_theta);
@@ -537,6 +569,9 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
       (static_cast<int64_t>(theta_offset) + n_theta) * n_rho >= (1ll << 32) - 1)
     return fail(LD_ERR_INVALID_ARG, "theta_offset %d: global cell index exceeds 32 bits",
                 theta_offset);
+  if (hint && (!aligned(hint, 16) || hint_bytes_ < hint_bytes(batch, n_theta, n_rho)))
+    return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned",
+                hint_bytes(batch, n_theta, n_rho));
   DevInfo dev;
   if ((rc = device_info(&dev))) return rc;
   if (!workspace || !aligned(workspace, 16) ||
@@ -545,35 +580,43 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
                 peaks_workspace_bytes(batch, n_theta, n_rho, k));
   return peaks_impl(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
                     n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
-                    cand_row_begin, cand_row_end, theta_offset);
+                    cand_row_begin, cand_row_end, theta_offset, hint, flags);
+}
+
+int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                      int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
+                      int32_t cand_row_begin, int32_t cand_row_end, int32_t theta_offset,
+                      ld_peak *peaks, int32_t *n_peaks, void *workspace,
+                      size_t workspace_bytes, void *stream) {
+  return ld_hough_peaks_opt(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k,
+                            cand_row_begin, cand_row_end, theta_offset, nullptr, 0, 0u, peaks,
+                            n_peaks, workspace, workspace_bytes, stream);
 }
 
 int ld_hough_peaks_hinted(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
                           int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
                           const void *hint, size_t hint_bytes_, ld_peak *peaks, int32_t *n_peaks,
                           void *workspace, size_t workspace_bytes, void *stream) {
-  g_launches = 0;
-  int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
-  if (rc) return rc;
-  if (!hint || !aligned(hint, 16) || hint_bytes_ < hint_bytes(batch, n_theta))
-    return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned", hint_bytes(batch, n_theta));
-  DevInfo dev;
-  if ((rc = device_info(&dev))) return rc;
-  if (!workspace || !aligned(workspace, 16) ||
-      workspace_bytes < peaks_workspace_bytes(batch, n_theta, n_rho, k))
-    return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 16-byte aligned",
-                peaks_workspace_bytes(batch, n_theta, n_rho, k));
-  return peaks_impl(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, peaks,
-                    n_peaks, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), 0, -1,
-                    0, hint);
+  if (!hint) {
+    g_launches = 0;
+    const int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks,
+                                    n_peaks);
+    if (rc) return rc;
+    return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned",
+                hint_bytes(batch, n_theta, n_rho));
+  }
+  return ld_hough_peaks_opt(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, 0,
+                            n_theta, 0, hint, hint_bytes_, 0u, peaks, n_peaks, workspace,
+                            workspace_bytes, stream);
 }
 
 int ld_hough_peaks(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
                    int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
                    ld_peak *peaks, int32_t *n_peaks, void *workspace, size_t workspace_bytes,
                    void *stream) {
-  return ld_hough_peaks_ex(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, 0,
-                           n_theta, 0, peaks, n_peaks, workspace, workspace_bytes, stream);
+  return ld_hough_peaks_opt(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, 0,
+                            n_theta, 0, nullptr, 0, 0u, peaks, n_peaks, workspace,
+                            workspace_bytes, stream);
 }
 
 size_t ld_detect_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k,
@@ -809,6 +852,35 @@ static HostLayout host_layout(const ld_image *img, int32_t n_theta, int32_t k, i
   return L;
 }
 
+// The host path's copy stream and its 4 events, created once per (host
+// thread, device) and kept for the thread's lifetime (a thread-local cache:
+// no shared mutable state, no per-call creation).  Each call synchronises
+// both streams before returning, so reuse is safe.
+struct HostStreams {
+  bool ok = false;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+};
+
+static int host_streams(HostStreams **out) {
+  static thread_local HostStreams per_dev[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  HostStreams &h = per_dev[dev & 63];
+  if (!h.ok) {
+    e = cudaStreamCreateWithFlags(&h.copy, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&h.copied[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.done[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "stream/event creation");
+    h.ok = true;
+  }
+  *out = &h;
+  return LD_OK;
+}
+
 size_t ld_detect_host_workspace_bytes(const ld_image *img, int32_t n_theta, int32_t k,
                                       int32_t chunk_frames) {
   if (!img || img->batch < 1 || chunk_frames < 1 || n_theta < 1 || k < 1) return 0;
@@ -833,15 +905,11 @@ int ld_detect_batch_host(const uint8_t *gray_host, const ld_image *img, int32_t 
     return fail(LD_ERR_WORKSPACE, "workspace needs %zu bytes, 256-byte aligned", L.total);
   int launches = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaStream_t cs = nullptr;
-  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
-  int rc = LD_OK;
-  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-    e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
-  }
-  if (e != cudaSuccess) rc = cuda_fail(e, "stream/event creation");
+  HostStreams *hs = nullptr;
+  int rc = host_streams(&hs);
+  cudaError_t e = cudaSuccess;
+  cudaStream_t cs = hs ? hs->copy : nullptr;
+  cudaEvent_t *copied = hs ? hs->copied : nullptr, *done = hs ? hs->done : nullptr;
   char *ws = static_cast<char *>(workspace);
   const int n_chunks = (img->batch + chunk - 1) / chunk;
   // the copy stream must not start before earlier work on `stream` that may use the workspace
@@ -889,13 +957,72 @@ int ld_detect_batch_host(const uint8_t *gray_host, const ld_image *img, int32_t 
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess && rc == LD_OK) rc = cuda_fail(e, "cudaStreamSynchronize");
   if (cs) cudaStreamSynchronize(cs);
-  for (int i = 0; i < 2; ++i) {
-    if (copied[i]) cudaEventDestroy(copied[i]);
-    if (done[i]) cudaEventDestroy(done[i]);
-  }
-  if (cs) cudaStreamDestroy(cs);
   g_launches = launches;
   return rc;
+}
+
+int64_t ld_edge_bitmask_words(int32_t width, int32_t rows) {
+  if (width < 1 || rows < 1) return 0;
+  return static_cast<int64_t>(rows) * ((width + 31) / 32);
+}
+
+int ld_edges_to_bitmask(const uint32_t *edge_xy, const uint32_t *edge_count, int32_t width,
+                        int32_t row_begin, int32_t rows, uint32_t *bits, void *stream) {
+  g_launches = 0;
+  if (!edge_xy || !edge_count || !bits) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
+  if (width < 1 || width > LD_MAX_DIM || rows < 1 || row_begin < 0 ||
+      row_begin + rows > LD_MAX_DIM)
+    return fail(LD_ERR_INVALID_ARG, "bad band: width %d, rows [%d, %d)", width, row_begin,
+                row_begin + rows);
+  if (!aligned(bits, 16)) return fail(LD_ERR_INVALID_ARG, "bits must be 16-byte aligned");
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  cudaError_t e = launch_edges_to_bitmask(edge_xy, edge_count, width, row_begin, rows, bits,
+                                          dev.sm_count, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "edges_to_bitmask_kernel launch");
+  return LD_OK;
+}
+
+int ld_bitmask_to_edges(const uint32_t *bits, int32_t width, int32_t n_blocks,
+                        const int32_t *block_row_begin, const int32_t *block_rows,
+                        int32_t block_stride_rows, uint32_t *edge_xy, int64_t edge_capacity,
+                        uint32_t *edge_count, void *stream) {
+  g_launches = 0;
+  if (!bits || !edge_xy || !edge_count) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
+  if (!block_row_begin || !block_rows) return fail(LD_ERR_INVALID_ARG, "NULL block table");
+  if (width < 1 || width > LD_MAX_DIM || n_blocks < 1 || n_blocks > LD_MAX_BLOCKS ||
+      block_stride_rows < 1 || edge_capacity < 0)
+    return fail(LD_ERR_INVALID_ARG, "bad bitmap geometry");
+  for (int b = 0; b < n_blocks; ++b)
+    if (block_rows[b] < 0 || block_rows[b] > block_stride_rows || block_row_begin[b] < 0 ||
+        block_row_begin[b] + block_rows[b] > LD_MAX_DIM)
+      return fail(LD_ERR_INVALID_ARG, "block %d: rows [%d, +%d) invalid", b, block_row_begin[b],
+                  block_rows[b]);
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  cudaError_t e = launch_bitmask_to_edges(bits, width, n_blocks, block_row_begin, block_rows,
+                                          block_stride_rows, edge_xy, edge_capacity, edge_count,
+                                          static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "bitmask_to_edges_kernel launch");
+  return LD_OK;
+}
+
+int ld_merge_peak_lists(const ld_peak *peaks, const int32_t *n_peaks, int32_t n_lists,
+                        int32_t k, int32_t n_rho, ld_peak *out, int32_t *n_out, void *stream) {
+  g_launches = 0;
+  if (!peaks || !n_peaks || !out || !n_out) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
+  if (n_lists < 1 || k < 1 || k > LD_MAX_K || n_rho < 1 ||
+      static_cast<int64_t>(n_lists) * k > 16384)
+    return fail(LD_ERR_INVALID_ARG, "bad merge: %d lists of %d", n_lists, k);
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  cudaError_t e = launch_merge_peak_lists(peaks, n_peaks, n_lists, k, n_rho, out, n_out,
+                                          static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "merge_peak_lists_kernel launch");
+  return LD_OK;
 }
 
 int ld_bench_smem_atomics(int32_t mode, int32_t iters, int32_t blocks_per_sm,

@@ -3,32 +3,140 @@
 //
 // Paper: Eq. 3, voting, 180 one-degree PEs, the GPU
 // design of one thread block per theta with the voting space in block shared
-// memory and atomic adds for colliding votes.  DESIGN.md 6.2.
+// memory and atomic adds for colliding votes; the half-angle
+// symmetry of Eq. 4-5.  DESIGN.md 6.2.
 //
 // Design: the paper gives each theta its own 48 KB block (K80).  On sm_100a a
 // CTA owns a BAND of theta rows -- as many rows of n_rho uint32 counters as fit
-// in the 227 KB opt-in shared memory -- so each frame's edge list is streamed
-// n_theta / rows times instead of n_theta times.  Every thread holds 4 edges
-// and, for each row of the band, issues one red.shared.add.u32 per edge at
-// ((x*C + y*S + 2^14 + (D << 15)) >> 15) (SASS: ATOMS.POPC.INC).  The
-// range proof done on the host (ld_api.cu) makes a per-vote bounds check
-// unnecessary.  The band is then written to HBM with plain coalesced stores:
-// no global atomics anywhere.
+// in half of the 227 KB opt-in shared memory (two CTAs per SM, so one CTA's
+// prologue and write-out overlap the other's voting) -- and each frame's edge
+// list is streamed n_theta / rows times instead of n_theta times.  For every
+// row of the band a lane issues one red.shared.add.u32 per edge at
+// ((x*C + y*S + 2^14 + (D << 15)) >> 15) (SASS: ATOMS.POPC.INC; lanes that
+// hit the same counter merge in hardware).  The host range proof (ld_api.cu)
+// makes a per-vote bounds check unnecessary.  The band leaves shared memory
+// by bulk (TMA engine) copies: no global atomics anywhere.
+//
+// Measured cost model of ATOMS on B200 (tools/atoms_probe.cu,
+// profiles/r02_atoms_probe.md): one wavefront per clock per SM; lanes on the
+// same address merge for free; k distinct addresses in one bank cost k
+// wavefronts.  So a warp's 32 votes cost one wavefront iff their rho bins span
+// fewer than 32 consecutive counters -- which is why ld_sobel.cu emits edges
+// in a spatially compact order.
+//
+// While a band is in shared memory the kernel also writes, for the peak
+// search (DESIGN R25, R30), (a) per warp the largest count it saw and its
+// cell, and (b) the maximum of every 32-cell segment of every row.
 #include <cstdlib>
 
 #include "ld_internal.cuh"
 
+namespace ld {
+
 #ifndef LD_HV_UNROLL
-#define LD_HV_UNROLL 4  // band rows per unrolled step
+#define LD_HV_UNROLL 4  // band rows per unrolled step (plain kernel)
 #endif
 
-namespace ld {
+// ---------------------------------------------------------------------------
+// Shared pieces
+// ---------------------------------------------------------------------------
+
+// dst[0 .. ncell) = src[0 .. ncell), src and dst congruent modulo 16 bytes:
+// the aligned middle by one bulk shared->global copy (issued by thread 0 and
+// committed as a bulk group; the caller waits for it before the CTA exits),
+// the <= 3 head and tail words by plain stores.  The caller must have made
+// the shared-memory writes visible to the async proxy (fence.proxy.async by
+// every writing thread, then a barrier).
+__device__ __forceinline__ void bulk_rows_out(uint32_t *dst, const uint32_t *src, int ncell,
+                                              int tid, int nt) {
+  if (ncell <= 0) return;
+  const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(dst) & 15u) >> 2);
+  const int head = min((4 - mis) & 3, ncell);
+  const int mid = ((ncell - head) >> 2) << 2;
+  if (tid < head) dst[tid] = src[tid];
+  for (int i = head + mid + tid; i < ncell; i += nt) dst[i] = src[i];
+  if (tid == 0 && mid > 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
+                 "r"(smem_u32(src + head)), "r"(static_cast<uint32_t>(mid) * 4u)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Running per-warp best of the summaries: the largest segment maximum seen
+// and where (a shared-memory pointer to the segment, its global row and
+// segment index).  Segments are visited in increasing cell order per warp, so
+// the strict '>' keeps the first (lowest-index) segment among equal maxima.
+struct SegBest {
+  uint32_t v = 0;
+  int row = 0, seg = 0;
+  const uint32_t *ptr = nullptr;
+};
+
+// Segment maxima of rows [0, nrows) of a shared-memory block (row j at
+// rows + j*n_rho, global row g0 + j): warp `wi` of `nw` takes segments
+// wi, wi+nw, ... of every row; one LDS + REDUX.MAX per segment of 32 cells.
+__device__ __forceinline__ void summarize_rows(const uint32_t *rows, int nrows, int g0, int n_rho,
+                                               int nseg, uint32_t *segmax_frame, int wi, int nw,
+                                               int lane, SegBest &best) {
+  for (int j = 0; j < nrows; ++j) {
+    const uint32_t *row = rows + j * n_rho;
+    uint32_t *out = segmax_frame + static_cast<int64_t>(g0 + j) * nseg;
+    for (int s = wi; s < nseg; s += nw) {
+      const int c = s * 32 + lane;
+      const uint32_t v = c < n_rho ? row[c] : 0u;
+      const uint32_t m = __reduce_max_sync(0xffffffffu, v);
+      if (lane == 0) out[s] = m;
+      if (m > best.v) {
+        best.v = m;
+        best.row = g0 + j;
+        best.seg = s;
+        best.ptr = row + s * 32;
+      }
+    }
+  }
+}
+
+// The warp's hint key (value << 32 | ~cell index) from its best segment: the
+// first lane holding the maximum.  0 when the warp saw only zeros.
+__device__ __forceinline__ unsigned long long seg_best_key(const SegBest &b, int n_rho, int lane) {
+  if (b.v == 0u) return 0ull;
+  const int c = b.seg * 32 + lane;
+  const uint32_t v = c < n_rho ? b.ptr[lane] : 0u;
+  const uint32_t hit = __ballot_sync(0xffffffffu, v == b.v);
+  const uint32_t idx = static_cast<uint32_t>(b.row) * static_cast<uint32_t>(n_rho) +
+                       static_cast<uint32_t>(b.seg * 32 + __ffs(hit) - 1);
+  return (static_cast<unsigned long long>(b.v) << 32) | (0xFFFFFFFFu - idx);
+}
+
+__device__ __forceinline__ void write_hint_header(const HoughParams &p, int nwarps) {
+  uint32_t *h = p.hint_hdr;
+  h[0] = HINT_MAGIC;
+  h[1] = static_cast<uint32_t>(p.batch);
+  h[2] = static_cast<uint32_t>(p.n_theta);
+  h[3] = static_cast<uint32_t>(p.n_rho);
+  h[4] = static_cast<uint32_t>(p.n_bands);
+  h[5] = static_cast<uint32_t>(nwarps);
+  h[6] = static_cast<uint32_t>(p.n_seg);
+}
+
+// ---------------------------------------------------------------------------
+// Plain kernel (any table): one block of rows t0 .. t0+nr-1 per CTA
+// ---------------------------------------------------------------------------
 
 // One block of 32 x EPL consecutive list entries of a warp (entry
 // blk + 32j + lane in lane `lane`), voted into every row of the band.
-template <int EPL, bool FULL>
 // Entries past `end` (FULL = false) vote into the scratch word instead of
 // being branched around: no divergent control flow in the tail.
+template <int EPL, bool FULL>
 __device__ __forceinline__ void vote_block(const uint32_t *el, uint32_t blk, uint32_t end,
                                            int lane, int nr, const uint4 *rowk,
                                            uint32_t scratch) {
@@ -47,8 +155,7 @@ __device__ __forceinline__ void vote_block(const uint32_t *el, uint32_t blk, uin
   for (int r = 0; r < nr; ++r) {
     const uint4 k = rowk[r];
 #pragma unroll
-    for (int j = 0; j < EPL; ++j)
-    {
+    for (int j = 0; j < EPL; ++j) {
       const uint32_t a = ((xs[j] * k.x + ys[j] * k.y + k.z) >> 13) & ~3u;
       red_shared_add(FULL || ok[j] ? a : scratch, 1u);
     }
@@ -59,10 +166,11 @@ template <int CTAS>
 __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
     hough_vote_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
   constexpr int NT = HV_THREADS / CTAS;
+  constexpr int NWARPS = NT / 32;
   extern __shared__ __align__(16) uint32_t slice_raw[];
   __shared__ uint4 rowk[HV_MAX_ROWS];  // per row: C, S, K = koff + (row address << 13)
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int band = blockIdx.x;
   const int f = blockIdx.y;
   const int t0 = band * p.rows_per_band;
@@ -70,7 +178,7 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   const int ncell = nr * p.n_rho;
   uint32_t *dst = p.acc + (static_cast<int64_t>(f) * p.n_theta + t0) * p.n_rho;
   // The slice starts at the same address modulo 16 as its destination, so the
-  // write-out can be one bulk (TMA) copy of its 16-byte-aligned middle part.
+  // write-out can be one bulk copy of its 16-byte-aligned middle part.
   const int mw = static_cast<int>((reinterpret_cast<uintptr_t>(dst) & 15u) >> 2);
   uint32_t *slice = slice_raw + mw;
   const uint32_t sbase = smem_u32(slice);
@@ -78,7 +186,7 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
 
   {
     uint4 *s4 = reinterpret_cast<uint4 *>(slice_raw);
-    const int n4 = (mw + ncell + 3) >> 2;
+    const int n4 = (mw + ncell + 1 + 3) >> 2;
     for (int i = tid; i < n4; i += NT) s4[i] = make_uint4(0u, 0u, 0u, 0u);
     // The byte address of the counter of (row r, bin rho) is
     //   sbase + r*row_bytes + 4*rho = ((v + ((sbase + r*row_bytes) << 13)) >> 13) & ~3
@@ -96,13 +204,7 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   // Warps take blocks of consecutive list entries, interleaved across the
   // CTA's warps: 16 entries per lane while whole rounds of such blocks remain
   // (fewer edge loads per vote), then 8 per lane, then a predicated tail, so
-  // the warps finish within one short block of each other.  At step j a
-  // warp's 32 lanes hold the 32 consecutive entries blk + 32j + lane, which
-  // the compaction made spatially compact (ld_sobel.cu): per theta they fall
-  // into few consecutive rho bins, i.e. distinct banks, and equal bins merge
-  // in ATOMS.POPC.INC.
-  const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NWARPS = NT / 32;
+  // the warps finish within one short block of each other.
   uint32_t base = 0;
   const uint32_t scratch = smem_u32(slice + ncell);  // inside the allocation, never written out
   for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
@@ -111,79 +213,19 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
     vote_block<8, true>(el, blk, n_edges, lane, nr, rowk, scratch);
   if (blk < n_edges) vote_block<8, false>(el, blk, n_edges, lane, nr, rowk, scratch);
+  fence_proxy_async_smem();
   __syncthreads();
 
-  // write-out: unaligned head and tail words by threads, the aligned middle
-  // by one bulk shared->global copy (async proxy: fence the ATOMS writes first)
-  const int head = min((4 - mw) & 3, ncell);
-  const int mid = ((ncell - head) >> 2) << 2;  // words, multiple of 4
-  if (tid < head) dst[tid] = slice[tid];
-  for (int i = head + mid + tid; i < ncell; i += NT) dst[i] = slice[i];
-  if (tid == 0 && mid > 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
-                 "r"(smem_u32(slice + head)), "r"(static_cast<uint32_t>(mid) * 4u)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
+  bulk_rows_out(dst, slice, ncell, tid, NT);
   if (p.hint_keys) {
-    // Peak hint (DESIGN R25), while the bulk copy reads the slice: the band's
-    // cells, row-major, split into one contiguous range per warp; for each
-    // the largest count and its first cell.  Lanes scan with 16-byte loads
-    // (the slice is 16-byte aligned at slice_raw); a lane keeps the first
-    // vector where its running maximum rose, and the warp reduction keeps the
-    // lowest cell index among equal counts.  No barrier: each warp writes its
-    // own key.
-    const int c0 = static_cast<int>((static_cast<int64_t>(ncell) * warp) / NWARPS);
-    const int c1 = static_cast<int>((static_cast<int64_t>(ncell) * (warp + 1)) / NWARPS);
-    const uint4 *v4 = reinterpret_cast<const uint4 *>(slice_raw);
-    const int w0 = (mw + c0) >> 2, w1 = (mw + c1 + 3) >> 2;
-    auto vec = [&](int w) {  // the vector's words outside [c0, c1) read as 0
-      uint4 q = v4[w];
-      const int i0 = w * 4 - mw;
-      if (i0 < c0 || i0 + 4 > c1) {
-        q.x = (i0 >= c0 && i0 < c1) ? q.x : 0u;
-        q.y = (i0 + 1 >= c0 && i0 + 1 < c1) ? q.y : 0u;
-        q.z = (i0 + 2 >= c0 && i0 + 2 < c1) ? q.z : 0u;
-        q.w = (i0 + 3 >= c0 && i0 + 3 < c1) ? q.w : 0u;
-      }
-      return q;
-    };
-    uint32_t run = 0;
-    int pos = -1;
-    for (int w = w0 + lane; w < w1; w += 32) {
-      const uint4 q = vec(w);
-      const uint32_t m4 = max(max(q.x, q.y), max(q.z, q.w));
-      if (m4 > run) {
-        run = m4;
-        pos = w;
-      }
-    }
-    unsigned long long key = 0ull;
-    if (run) {
-      const uint4 q = vec(pos);
-      const int j = q.x == run ? 0 : q.y == run ? 1 : q.z == run ? 2 : 3;
-      const uint32_t idx = static_cast<uint32_t>(t0) * static_cast<uint32_t>(p.n_rho) +
-                           static_cast<uint32_t>(pos * 4 + j - mw);
-      key = (static_cast<unsigned long long>(run) << 32) | (0xFFFFFFFFu - idx);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-      key = other > key ? other : key;
-    }
+    SegBest best;
+    uint32_t *segmax = p.segmax + static_cast<int64_t>(f) * p.n_theta * p.n_seg;
+    summarize_rows(slice, nr, t0, p.n_rho, p.n_seg, segmax, warp, NWARPS, lane, best);
+    const unsigned long long key = seg_best_key(best, p.n_rho, lane);
     if (lane == 0) p.hint_keys[(static_cast<int64_t>(f) * p.n_bands + band) * NWARPS + warp] = key;
-    if (f == 0 && band == 0 && tid == 0) {
-      uint32_t *h = p.hint_hdr;
-      h[0] = HINT_MAGIC;
-      h[1] = static_cast<uint32_t>(p.batch);
-      h[2] = static_cast<uint32_t>(p.n_theta);
-      h[3] = static_cast<uint32_t>(p.n_rho);
-      h[4] = static_cast<uint32_t>(p.n_bands);
-      h[5] = NWARPS;
-    }
+    if (f == 0 && band == 0 && tid == 0) write_hint_header(p, NWARPS);
   }
-  if (tid == 0 && mid > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  if (tid == 0) bulk_wait_read();
 }
 
 static int rows_per_band(int n_theta, int n_rho, size_t limit, int *n_bands) {
@@ -198,8 +240,8 @@ static int rows_per_band(int n_theta, int n_rho, size_t limit, int *n_bands) {
 
 int hough_plan(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *rpb, int *n_bands,
                size_t *smem_bytes) {
-  // per CTA: the slice (+16 bytes of alignment shift), rowk, and a margin
-  const size_t fixed = sizeof(uint4) * HV_MAX_ROWS + 1024 + 16;
+  // per CTA: the slice (+16 bytes of alignment shift, +1 scratch word), rowk, a margin
+  const size_t fixed = sizeof(uint4) * HV_MAX_ROWS + 1024 + 32;
   int nb1 = 0, nb2 = 0;
   const int r1 = rows_per_band(n_theta, n_rho, smem_optin - fixed, &nb1);
   if (r1 < 1) return 0;
@@ -208,28 +250,17 @@ int hough_plan(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *rpb, i
   *ctas = two ? 2 : 1;
   *rpb = two ? r2 : r1;
   *n_bands = two ? nb2 : nb1;
-  *smem_bytes = ((static_cast<size_t>(*rpb) * n_rho * 4 + 15) / 16) * 16 + 16;
+  *smem_bytes = ((static_cast<size_t>(*rpb) * n_rho * 4 + 15) / 16) * 16 + 32;
   return 1;
 }
 
-static bool g_hough_attr[64][3];
+static AttrOnce g_hough_attr[3];
 
 cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, size_t smem_bytes,
                          cudaStream_t stream) {
-  int dev = 0;
-  cudaGetDevice(&dev);
   auto kern = ctas == 2 ? hough_vote_kernel<2> : hough_vote_kernel<1>;
-  if (!g_hough_attr[dev & 63][ctas]) {
-    // the largest slice hough_plan can request for this CTA count, next to the
-    // kernel's static shared memory (rowk, the hint reduction)
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024 / ctas - static_cast<int>(fa.sharedSizeBytes));
-    if (e != cudaSuccess) return e;
-    g_hough_attr[dev & 63][ctas] = true;
-  }
+  cudaError_t e = ensure_smem_attr(g_hough_attr[ctas], kern, -(227 * 1024 / ctas));
+  if (e != cudaSuccess) return e;
   dim3 grid(p.n_bands, p.batch);
   kern<<<grid, HV_THREADS / ctas, smem_bytes, stream>>>(p, trig);
   note_launch();
@@ -239,30 +270,29 @@ cudaError_t launch_hough(const HoughParams &p, const TrigTable &trig, int ctas, 
 // ---------------------------------------------------------------------------
 // Half-angle paired voting (NEXT 2; the paper's Eq. 4-5): for a
 // table with C[n-t] = -C[t] and S[n-t] = S[t], the rows t and n - t share
-// Q = y*S[t] + K: V_t = Q + x*C[t], V_{n-t} = Q - x*C[t].  A CTA holds pairs
-// p0 .. p0+np-1: rows t = p0 + i in the first half of its slice (in order,
-// like the unpaired kernel), their partners n - t in the second half at the
-// same slot i, i.e. a CONSTANT distance delta = rows_per_band * 4 n_rho bytes
-// above, which the compiler folds into the ATOMS as a uniform-register offset
-// ([R+UR]):
-//   addr(t)   = ((x*C + Q) >> 13) & ~3          (Q = y*S + koff + (row t address << 13))
-//   addr(n-t) = ((x*(-C) + Q) >> 13) & ~3, + delta
-// 9 instructions per 2 votes instead of 10; consecutive bins stay in distinct
-// banks.  Folding is exact as in the unpaired kernel: V in [0, 2^31) for both
-// rows (host range proof, mirrored entries included), addresses < 2^18.
+// Q = y*S[t] + K:  V_t = x*C[t] + Q,  V_{n-t} = Q - x*C[t] = V_t - 2x*C[t].
+// A CTA holds pairs p0 .. p0+np-1.  Its shared memory has two blocks of np
+// rows: block 1 holds rows t = p0 + i at slot i (ascending, like acc); block 2
+// holds the partners n - t at slot np-1-i, i.e. rows n-p0-np+1 .. n-p0
+// ASCENDING as well -- so each block leaves by ONE bulk copy.  The partner of
+// slot i lies delta_i = (block-2 row np-1-i) - (block-1 row i) bytes above it;
+// delta_i is warp-uniform per pair, so it folds into the ATOMS address as a
+// uniform-register offset ([R+UR]):
+//   addr(t)   = ((x*C + Q) >> 13) & ~3              (Q = y*S + koff + (row address << 13))
+//   addr(n-t) = ((x*(-2C) + V_t) >> 13) & ~3, + delta_i
+// 9 instructions per 2 votes (3 IMAD, 2 SHF, 2 LOP3, 2 ATOMS).  Folding is
+// exact as in the plain kernel: V in [0, 2^31) for both rows (host range
+// proof, mirrored entries included), addresses < 2^18.
 // Pair p = 0 and p = n/2 (n even) have no partner: their mirror votes land in
-// a scratch row that is not written out.
+// a block-2 row that is not written out (row n, and row n/2 a second time).
 // ---------------------------------------------------------------------------
-__host__ __device__ __forceinline__ int pair_partner(int t, int n_theta) {
-  return (t == 0 || 2 * t == n_theta) ? -1 : n_theta - t;
-}
-
 int hough_pair_count(int n_theta) { return n_theta / 2 + 1; }
 
 template <int EPL, bool FULL>
 __device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t blk, uint32_t end,
                                                  int lane, int np, const uint4 *rowk,
-                                                 uint32_t delta, uint32_t scratch) {
+                                                 uint32_t delta0, uint32_t row_bytes2,
+                                                 uint32_t scratch) {
   uint32_t xs[EPL], ys[EPL];
   bool ok[EPL];
 #pragma unroll
@@ -275,15 +305,14 @@ __device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t bl
   }
 #pragma unroll 2
   for (int r = 0; r < np; ++r) {
-    const uint4 k = rowk[r];  // C, S, K, -C
+    const uint4 k = rowk[r];  // C, S, K, -2C
+    const uint32_t delta = delta0 - static_cast<uint32_t>(r) * row_bytes2;  // uniform
 #pragma unroll
-    for (int j = 0; j < EPL; ++j)
-    {
-      const uint32_t q = ys[j] * k.y + k.z;
-      const uint32_t a1 = ((xs[j] * k.x + q) >> 13) & ~3u;
-      const uint32_t a2 = ((xs[j] * k.w + q) >> 13) & ~3u;
-      red_shared_add(FULL || ok[j] ? a1 : scratch, 1u);
-      red_shared_add((FULL || ok[j] ? a2 : scratch - delta) + delta, 1u);
+    for (int j = 0; j < EPL; ++j) {
+      const uint32_t v1 = xs[j] * k.x + (ys[j] * k.y + k.z);
+      const uint32_t v2 = xs[j] * k.w + v1;
+      red_shared_add(FULL || ok[j] ? (v1 >> 13) & ~3u : scratch, 1u);
+      red_shared_add((FULL || ok[j] ? (v2 >> 13) & ~3u : scratch - delta) + delta, 1u);
     }
   }
 }
@@ -294,7 +323,7 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   constexpr int NT = HV_THREADS / CTAS;
   constexpr int NWARPS = NT / 32;
   extern __shared__ __align__(16) uint32_t slice_raw[];
-  __shared__ uint4 rowk[HV_MAX_ROWS];  // per pair: C, S, K = koff + (row t address << 13), -C
+  __shared__ uint4 rowk[HV_MAX_ROWS];  // per pair: C, S, K = koff + (row t address << 13), -2C
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int band = blockIdx.x;
@@ -302,135 +331,75 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   const int n_rho = p.n_rho, n_theta = p.n_theta;
   const int p0 = band * p.rows_per_band;
   const int np = min(p.rows_per_band, p.n_pairs - p0);
-  const int ncell = np * n_rho;                       // first half (rows p0 ..)
-  const int half = p.rows_per_band * n_rho;           // words to the partner half
+  const int ncell = np * n_rho;
   uint32_t *frame = p.acc + static_cast<int64_t>(f) * n_theta * n_rho;
-  uint32_t *dst = frame + static_cast<int64_t>(p0) * n_rho;
-  // first half at the destination's address modulo 16 (bulk write-out)
-  const int mw = static_cast<int>((reinterpret_cast<uintptr_t>(dst) & 15u) >> 2);
-  uint32_t *slice = slice_raw + mw;
-  const uint32_t sbase = smem_u32(slice);
+  // block 1: rows p0 .. p0+np-1; block 2: rows g2 .. g2+np-1 with g2 = n-p0-np+1
+  const int g2 = n_theta - p0 - np + 1;
+  uint32_t *dst1 = frame + static_cast<int64_t>(p0) * n_rho;
+  uint32_t *dst2 = frame + static_cast<int64_t>(g2) * n_rho;  // may point one row past acc
+  // each block at its destination's address modulo 16 (bulk write-out)
+  const int mw1 = static_cast<int>((reinterpret_cast<uintptr_t>(dst1) & 15u) >> 2);
+  const int mw2 = static_cast<int>((reinterpret_cast<uintptr_t>(dst2) & 15u) >> 2);
+  const int h2 = ((mw1 + ncell + 3) >> 2) << 2;  // block 2's 16-byte-aligned base (words)
+  uint32_t *blk1 = slice_raw + mw1;
+  uint32_t *blk2 = slice_raw + h2 + mw2;
   const uint32_t row_bytes = static_cast<uint32_t>(n_rho) * 4u;
-  const uint32_t delta = p.pair_delta;
+  // partner distance of slot i: delta0 - i * 2 row_bytes
+  const uint32_t delta0 = smem_u32(blk2) - smem_u32(blk1) + static_cast<uint32_t>(np - 1) * row_bytes;
+  const uint32_t scratch = smem_u32(blk2 + ncell);  // inside the allocation, never written out
   {
     uint4 *s4 = reinterpret_cast<uint4 *>(slice_raw);
-    const int n4 = (mw + half + ncell + 3) >> 2;
+    const int n4 = (h2 + mw2 + ncell + 1 + 3) >> 2;
     for (int i = tid; i < n4; i += NT) s4[i] = make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t sbase = smem_u32(blk1);
     for (int i = tid; i < np; i += NT) {
       const int t = p0 + i;
       rowk[i] = make_uint4(static_cast<uint32_t>(trig.c[t]), static_cast<uint32_t>(trig.s[t]),
                            static_cast<uint32_t>(p.koff) + ((sbase + i * row_bytes) << 13),
-                           static_cast<uint32_t>(-trig.c[t]));
+                           static_cast<uint32_t>(-2 * trig.c[t]));
     }
   }
   __syncthreads();
 
   const uint32_t n_edges = p.counts[f];
   const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
-  // scratch word past the partner half (>= the partner offset): inside the
-  // allocation, never written out
-  const uint32_t scratch = smem_u32(slice + half + ncell);
+  const uint32_t rb2 = 2u * row_bytes;
   uint32_t base = 0;
   for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
-    vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, delta,
+    vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, delta0, rb2,
                                scratch);
   uint32_t blk = base + static_cast<uint32_t>(warp) * (32u * 8u);
   for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
-    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, delta, scratch);
-  if (blk < n_edges) vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, delta, scratch);
+    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, delta0, rb2, scratch);
+  if (blk < n_edges)
+    vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, delta0, rb2, scratch);
+  fence_proxy_async_smem();
   __syncthreads();
 
-  // write-out, first half: rows p0 .. p0+np-1 are consecutive in acc -- one
-  // bulk copy of the aligned middle, head and tail words by threads
-  const int head = min((4 - mw) & 3, ncell);
-  const int mid = ((ncell - head) >> 2) << 2;
-  if (tid < head) dst[tid] = slice[tid];
-  for (int i = head + mid + tid; i < ncell; i += NT) dst[i] = slice[i];
-  if (tid == 0 && mid > 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
-                 "r"(smem_u32(slice + head)), "r"(static_cast<uint32_t>(mid) * 4u)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
-  // second half: partner rows n - t descend as t ascends; coalesced thread
-  // stores (the scratch partner of an unpaired row is dropped).  The peak
-  // hint (R25) rides along here and scans the first half.
-  const bool hint = p.hint_keys != nullptr;
-  uint32_t run = 0, ridx = 0xFFFFFFFFu;
-  for (int i = 0; i < np; ++i) {
-    const int tp = pair_partner(p0 + i, n_theta);
-    if (tp < 0) continue;  // uniform
-    uint32_t *rb = frame + static_cast<int64_t>(tp) * n_rho;
-    const uint32_t *src = slice + half + i * n_rho;
-    const uint32_t ib = static_cast<uint32_t>(tp) * static_cast<uint32_t>(n_rho);
-    for (int j = tid; j < n_rho; j += NT) {
-      const uint32_t v = src[j];
-      rb[j] = v;
-      if (hint && v > run) {
-        run = v;
-        ridx = ib + static_cast<uint32_t>(j);
-      }
-    }
-  }
-  if (hint) {
-    unsigned long long key = run ? (static_cast<unsigned long long>(run) << 32) | (0xFFFFFFFFu - ridx) : 0ull;
-    // first half: this warp's contiguous share, 16-byte loads
-    const int c0 = static_cast<int>((static_cast<int64_t>(ncell) * warp) / NWARPS);
-    const int c1 = static_cast<int>((static_cast<int64_t>(ncell) * (warp + 1)) / NWARPS);
-    const uint4 *v4 = reinterpret_cast<const uint4 *>(slice_raw);
-    const int w0 = (mw + c0) >> 2, w1 = (mw + c1 + 3) >> 2;
-    auto vec = [&](int w) {
-      uint4 q = v4[w];
-      const int i0 = w * 4 - mw;
-      if (i0 < c0 || i0 + 4 > c1) {
-        q.x = (i0 >= c0 && i0 < c1) ? q.x : 0u;
-        q.y = (i0 + 1 >= c0 && i0 + 1 < c1) ? q.y : 0u;
-        q.z = (i0 + 2 >= c0 && i0 + 2 < c1) ? q.z : 0u;
-        q.w = (i0 + 3 >= c0 && i0 + 3 < c1) ? q.w : 0u;
-      }
-      return q;
-    };
-    uint32_t r2 = 0;
-    int pos = -1;
-    for (int w = w0 + lane; w < w1; w += 32) {
-      const uint4 q = vec(w);
-      const uint32_t m4 = max(max(q.x, q.y), max(q.z, q.w));
-      if (m4 > r2) {
-        r2 = m4;
-        pos = w;
-      }
-    }
-    if (r2) {
-      const uint4 q = vec(pos);
-      const int jj = q.x == r2 ? 0 : q.y == r2 ? 1 : q.z == r2 ? 2 : 3;
-      const uint32_t idx = static_cast<uint32_t>(p0) * static_cast<uint32_t>(n_rho) +
-                           static_cast<uint32_t>(pos * 4 + jj - mw);
-      const unsigned long long k2 = (static_cast<unsigned long long>(r2) << 32) | (0xFFFFFFFFu - idx);
-      key = k2 > key ? k2 : key;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-      key = other > key ? other : key;
-    }
+  // write-out: block 1 whole; block 2's rows that exist as partners: not row
+  // n (slot 0 of pair 0, block-2 row np-1) and not row n/2 a second time (pair
+  // n/2 of an even n, the last pair: block-2 row 0)
+  const int j0 = (n_theta % 2 == 0 && p0 + np - 1 == n_theta / 2) ? 1 : 0;
+  const int j1 = p0 == 0 ? np - 1 : np;
+  bulk_rows_out(dst1, blk1, ncell, tid, NT);
+  if (j1 > j0) bulk_rows_out(dst2 + j0 * n_rho, blk2 + j0 * n_rho, (j1 - j0) * n_rho, tid, NT);
+  if (p.hint_keys) {
+    SegBest best;
+    uint32_t *segmax = p.segmax + static_cast<int64_t>(f) * n_theta * p.n_seg;
+    summarize_rows(blk1, np, p0, n_rho, p.n_seg, segmax, warp, NWARPS, lane, best);
+    if (j1 > j0)
+      summarize_rows(blk2 + j0 * n_rho, j1 - j0, g2 + j0, n_rho, p.n_seg, segmax, warp, NWARPS,
+                     lane, best);
+    const unsigned long long key = seg_best_key(best, n_rho, lane);
     if (lane == 0) p.hint_keys[(static_cast<int64_t>(f) * p.n_bands + band) * NWARPS + warp] = key;
-    if (f == 0 && band == 0 && tid == 0) {
-      uint32_t *h = p.hint_hdr;
-      h[0] = HINT_MAGIC;
-      h[1] = static_cast<uint32_t>(p.batch);
-      h[2] = static_cast<uint32_t>(p.n_theta);
-      h[3] = static_cast<uint32_t>(p.n_rho);
-      h[4] = static_cast<uint32_t>(p.n_bands);
-      h[5] = NWARPS;
-    }
+    if (f == 0 && band == 0 && tid == 0) write_hint_header(p, NWARPS);
   }
-  if (tid == 0 && mid > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  if (tid == 0) bulk_wait_read();
 }
 
 int hough_plan_pairs(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *ppb, int *n_bands,
                      size_t *smem_bytes) {
-  const size_t fixed = sizeof(uint4) * HV_MAX_ROWS + 1024 + 16;
+  const size_t fixed = sizeof(uint4) * HV_MAX_ROWS + 1024 + 64;
   const int np = hough_pair_count(n_theta);
   const size_t pair = static_cast<size_t>(n_rho) * 8u;
   auto plan = [&](size_t limit, int *nb) {
@@ -444,31 +413,23 @@ int hough_plan_pairs(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *
   const int p1 = plan(smem_optin - fixed, &nb1);
   if (p1 < 1) return 0;
   const int p2 = plan(smem_optin / 2 - fixed, &nb2);
-  const char *env = getenv("LD_VOTE_CTAS");
-  const bool two = env ? (env[0] == '2' && p2 >= 1) : (p2 >= 4 && p1 >= 8);
+  const bool two = p2 >= 4 && p1 >= 8;
   *ctas = two ? 2 : 1;
   *ppb = two ? p2 : p1;
   *n_bands = two ? nb2 : nb1;
-  *smem_bytes = ((static_cast<size_t>(*ppb) * pair + 15) / 16) * 16 + 16;
+  // two blocks of ppb rows, each shifted by up to 3 words and rounded to 16
+  // bytes, + the scratch word (<= 52 bytes over 2 * ppb rows)
+  *smem_bytes = ((static_cast<size_t>(*ppb) * pair + 15) / 16) * 16 + 64;
   return 1;
 }
 
-static bool g_pairs_attr[64][3];
+static AttrOnce g_pairs_attr[3];
 
 cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int ctas,
                                size_t smem_bytes, cudaStream_t stream) {
-  int dev = 0;
-  cudaGetDevice(&dev);
   auto kern = ctas == 2 ? hough_vote_pairs_kernel<2> : hough_vote_pairs_kernel<1>;
-  if (!g_pairs_attr[dev & 63][ctas]) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024 / ctas - static_cast<int>(fa.sharedSizeBytes));
-    if (e != cudaSuccess) return e;
-    g_pairs_attr[dev & 63][ctas] = true;
-  }
+  cudaError_t e = ensure_smem_attr(g_pairs_attr[ctas], kern, -(227 * 1024 / ctas));
+  if (e != cudaSuccess) return e;
   dim3 grid(p.n_bands, p.batch);
   kern<<<grid, HV_THREADS / ctas, smem_bytes, stream>>>(p, trig);
   note_launch();
@@ -477,6 +438,8 @@ cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int 
 
 // ---------------------------------------------------------------------------
 // B5: red.shared.add.u32 throughput.  1024 threads per CTA, 48 K-word array.
+// The timed part is bracketed by clock64 in every CTA (cycles[] output), so
+// the rate per clock per SM excludes the prologue and the checksum.
 // ---------------------------------------------------------------------------
 constexpr int AB_WORDS = 49152;
 
@@ -486,6 +449,7 @@ __global__ void __launch_bounds__(1024, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < AB_WORDS; i += blockDim.x) buf[i] = 0u;
   __syncthreads();
+  const long long c0 = clock64();
   const uint32_t base = smem_u32(buf);
   if (mode == 0) {
     // conflict-free, issue-free: lane l -> bank l, 32 distinct rows per
@@ -511,26 +475,26 @@ __global__ void __launch_bounds__(1024, 1)
     for (int i = 0; i < iters; ++i) red_shared_add(base + (static_cast<uint32_t>(warp) << 7), 1u);
   }
   __syncthreads();
+  const long long c1 = clock64();
   if (tid < 32) {
     uint32_t s = 0;
     for (int i = tid; i < AB_WORDS; i += 32) s += buf[i];
-    out[blockIdx.x * 32 + tid] = s;
+    out[blockIdx.x * 34 + tid] = s;
+  }
+  if (tid == 0) {
+    const unsigned long long dc = static_cast<unsigned long long>(c1 - c0);
+    out[blockIdx.x * 34 + 32] = static_cast<uint32_t>(dc);
+    out[blockIdx.x * 34 + 33] = static_cast<uint32_t>(dc >> 32);
   }
 }
 
-static bool g_bench_attr[64];
+static AttrOnce g_bench_attr;
 
 cudaError_t launch_smem_atomic_bench(int mode, int iters, int grid, uint32_t *scratch,
                                      cudaStream_t stream) {
-  int dev = 0;
-  cudaGetDevice(&dev);
   const int smem = AB_WORDS * 4;
-  if (!g_bench_attr[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(smem_atomic_bench_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    g_bench_attr[dev & 63] = true;
-  }
+  cudaError_t e = ensure_smem_attr(g_bench_attr, smem_atomic_bench_kernel, smem);
+  if (e != cudaSuccess) return e;
   smem_atomic_bench_kernel<<<grid, 1024, smem, stream>>>(mode, iters, scratch);
   note_launch();
   return cudaGetLastError();

@@ -97,22 +97,13 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   }
 }
 
-static bool g_f64_attr[64][3];
+static AttrOnce g_f64_attr[3];
 
 cudaError_t launch_hough_f64(const HoughParams &p, const TrigTableF64 &trig, int ctas,
                              size_t smem_bytes, cudaStream_t stream) {
-  int dev = 0;
-  cudaGetDevice(&dev);
   auto kern = ctas == 2 ? hough_vote_f64_kernel<2> : hough_vote_f64_kernel<1>;
-  if (!g_f64_attr[dev & 63][ctas]) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024 / ctas - static_cast<int>(fa.sharedSizeBytes));
-    if (e != cudaSuccess) return e;
-    g_f64_attr[dev & 63][ctas] = true;
-  }
+  const cudaError_t e = ensure_smem_attr(g_f64_attr[ctas], kern, -(227 * 1024 / ctas));
+  if (e != cudaSuccess) return e;
   dim3 grid(p.n_bands, p.batch);
   kern<<<grid, HV_THREADS / ctas, smem_bytes, stream>>>(p, trig);
   note_launch();

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/ld.h"
 
 namespace ld {
@@ -69,20 +71,22 @@ struct HoughParams {
   int32_t n_theta, n_rho;
   int32_t rows_per_band, n_bands;  // paired kernel: pairs per band, bands
   int32_t n_pairs;                 // paired kernel (NEXT 2): theta pairs (t, n_theta - t)
-  uint32_t pair_delta;             // paired kernel: bytes from row t to its partner's row
-                                   // (= rows_per_band * n_rho * 4, a parameter so that it
-                                   // stays a uniform-register ATOMS offset)
   int32_t koff;  // 2^14 + (D << 15): rho_bin = (x*C + y*S + koff) >> 15
   uint32_t *acc;
   uint32_t *hint_hdr;            // nullable: peak-hint header (written by CTA (0, 0))
-  unsigned long long *hint_keys;  // [batch][n_bands][warps per CTA] range maxima
+  unsigned long long *hint_keys;  // [batch][n_bands][warps per CTA] per-warp maxima
+  uint32_t *segmax;              // [batch][n_theta][n_seg] 32-cell segment maxima
+  int32_t n_seg;                 // ceil(n_rho / 32)
 };
 
 // Peak-hint buffer layout (ld_hough_accumulate_hint / ld_hough_peaks_hinted):
-// a 64-byte header {magic, batch, n_theta, n_rho, n_bands, ranges per band,
-// 0...} then the range-maximum keys (one range per warp of the voting CTA).
-constexpr uint32_t HINT_MAGIC = 0x3148444Cu;  // "LDH1"
+// a 64-byte header {magic, batch, n_theta, n_rho, n_bands, keys per band,
+// n_seg, 0...}, the per-warp maximum keys ([batch][n_bands][keys per band],
+// capacity batch * n_theta * HINT_MAX_RANGES), then the segment maxima
+// [batch][n_theta][n_seg] (DESIGN R25, R30).
+constexpr uint32_t HINT_MAGIC = 0x3248444Cu;  // "LDH2"
 constexpr int HINT_HDR_BYTES = 64;
+constexpr int SEG_CELLS = 32;  // cells per segment maximum
 constexpr int HINT_MAX_KEYS = 1024;  // per frame, what the verifying kernel sorts (more are merged)
 constexpr int HINT_MAX_RANGES = 32;  // ranges per band (warps of a 1024-thread CTA)
 
@@ -134,12 +138,24 @@ struct PeaksParams {
   int32_t theta_offset;           // added to the row index in keys and reported theta bins
   const uint32_t *hint_hdr;       // nullable: peak hint (unrestricted searches only)
   const unsigned long long *hint_keys;
+  const uint32_t *segmax;         // hint's segment maxima [batch][n_theta][n_seg] (sparse path)
+  int32_t n_seg;
+  uint32_t *resolved;             // [batch] 1 = the sparse search wrote this frame's peaks
+  uint32_t *ncand;                // [batch] sparse-search candidates found
+  unsigned long long *cand;       // [batch][SP_CAP] sparse-search candidate keys
   ld_peak *peaks;
   int32_t *n_peaks;
 };
+constexpr int SP_CAP = 2048;      // sparse search: candidate keys per frame
 
+// Peaks workspace: byte offsets of its parts
+struct PeaksLayout {
+  size_t gtau, resolved, ncand, cand, keys, total;
+};
+PeaksLayout peaks_layout(int batch, int n_theta, int n_rho, int k);
 size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k);
-cudaError_t launch_peaks(const PeaksParams &p, cudaStream_t stream);
+// flags: LD_PEAKS_* of ld.h
+cudaError_t launch_peaks(const PeaksParams &p, uint32_t flags, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // NEXT 3: lanes module (ld_lanes.cu)
@@ -181,6 +197,20 @@ cudaError_t launch_extract_segments(const LanesParams &p, const TrigTable &trig,
                                     cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
+// Multi-GPU helpers (ld_dist.cu)
+// ---------------------------------------------------------------------------
+cudaError_t launch_edges_to_bitmask(const uint32_t *edges, const uint32_t *count, int width,
+                                    int row_begin, int rows, uint32_t *bits, int sm_count,
+                                    cudaStream_t stream);
+cudaError_t launch_bitmask_to_edges(const uint32_t *bits, int width, int n_blocks,
+                                    const int32_t *row_begin, const int32_t *rows,
+                                    int block_stride_rows, uint32_t *edges, int64_t capacity,
+                                    uint32_t *count, cudaStream_t stream);
+cudaError_t launch_merge_peak_lists(const ld_peak *peaks, const int32_t *n_peaks, int n_lists,
+                                    int k, int n_rho, ld_peak *out, int32_t *n_out,
+                                    cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
 // B5: shared-memory atomic microbenchmark (ld_hough.cu)
 // ---------------------------------------------------------------------------
 cudaError_t launch_smem_atomic_bench(int mode, int iters, int grid, uint32_t *scratch,
@@ -188,6 +218,36 @@ cudaError_t launch_smem_atomic_bench(int mode, int iters, int grid, uint32_t *sc
 
 // launch counter of the current host thread (ld_api.cu)
 void note_launch(int n = 1);
+
+// Per-device, per-kernel "max dynamic shared memory" attribute, set once:
+// std::call_once per (device, kernel) slot -- thread-safe, no racy flags.
+struct AttrOnce {
+  std::once_flag once[64];
+  cudaError_t err[64] = {};
+};
+
+// bytes >= 0: that many bytes; bytes < 0: -bytes minus the kernel's static
+// shared memory (the largest request a CTA of that kernel can make).
+template <typename K>
+static inline cudaError_t ensure_smem_attr(AttrOnce &a, K kern, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::call_once(a.once[dev & 63], [&]() {
+    int b = bytes;
+    if (b < 0) {
+      cudaFuncAttributes fa;
+      const cudaError_t r = cudaFuncGetAttributes(&fa, kern);
+      if (r != cudaSuccess) {
+        a.err[dev & 63] = r;
+        return;
+      }
+      b = -bytes - static_cast<int>(fa.sharedSizeBytes);
+    }
+    a.err[dev & 63] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  });
+  return a.err[dev & 63];
+}
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -239,11 +299,6 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
 
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
-// the counter 4 bytes above addr (an immediate offset of the ATOMS)
-__device__ __forceinline__ void red_shared_add_next(uint32_t addr, uint32_t v) {
-  asm volatile("red.shared.add.u32 [%0+4], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {

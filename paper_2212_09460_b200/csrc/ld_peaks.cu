@@ -23,6 +23,12 @@
 
 #include "ld_internal.cuh"
 
+// largest half_theta for which the streaming kernel loads 4 columns per thread
+// (else 2); a build option (-DLD_PS_CPT4_MAX_HT=...) for experiments
+#ifndef LD_PS_CPT4_MAX_HT
+#define LD_PS_CPT4_MAX_HT 6
+#endif
+
 namespace ld {
 
 typedef unsigned long long u64;
@@ -55,6 +61,12 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// The sparse search (peaks_sparse_finish_kernel) already wrote this frame's
+// peaks: the dense kernels skip it (uniform per CTA: f = blockIdx.y).
+__device__ __forceinline__ bool frame_resolved(const PeaksParams &p, int f) {
+  return p.resolved != nullptr && ld_relaxed_u32(p.resolved + f) != 0u;
 }
 
 // Sort a[0..n) descending (n a power of two); all threads participate.
@@ -117,6 +129,7 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
   __shared__ int s_nbuf, s_ntop;
 
   const int band = blockIdx.x, f = blockIdx.y;
+  if (frame_resolved(p, f)) return;
   const int t0 = p.cand_t0 + band * PK_ROWS;
   const int nr = min(PK_ROWS, p.cand_t1 - t0);
   const int ncell = nr * p.n_rho;
@@ -202,8 +215,13 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
   const bool match = h[0] == HINT_MAGIC && h[1] == static_cast<uint32_t>(p.batch) &&
                      h[2] == static_cast<uint32_t>(p.n_theta) &&
                      h[3] == static_cast<uint32_t>(p.n_rho) && h[5] >= 1 &&
-                     h[5] <= HINT_MAX_RANGES && h[4] >= 1 && h[4] <= static_cast<uint32_t>(p.n_theta);
+                     h[5] <= HINT_MAX_RANGES && h[4] >= 1 && h[4] <= static_cast<uint32_t>(p.n_theta) &&
+                     h[6] == static_cast<uint32_t>(p.n_seg);
   const int n_src = match ? static_cast<int>(h[4] * h[5]) : 0;
+  if (tid == 0 && p.ncand) {
+    p.ncand[f] = 0u;
+    p.resolved[f] = 0u;
+  }
   if (n_src <= 0) {
     if (tid == 0) p.gtau[f] = 0u;
     return;
@@ -300,11 +318,150 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
   if (tid == 0) p.gtau[f] = s_bound;
 }
 
+// ---------------------------------------------------------------------------
+// Sparse search (DESIGN R30): with a certified bound tau_f = gtau[f] > 0 (the
+// k-th verified hint key, R25) every top-k candidate has votes >= tau_f, and
+// every cell >= tau_f lies in a 32-cell segment whose maximum (recorded by the
+// voting kernel while the band was in shared memory) is >= tau_f.  So the
+// search reads the segment maxima (1/32 of the accumulator), tests only the
+// cells >= tau_f of those segments against the full candidate definition
+// (one warp per cell, exact window test as in the band kernel), and keeps the
+// keys of the candidates found.  peaks_sparse_finish_kernel then takes their
+// top k.  A frame whose bound is not certified, or whose candidate list
+// overflows SP_CAP, is left unresolved: the dense kernels (which skip
+// resolved frames) compute it.  The result is identical either way.
+// ---------------------------------------------------------------------------
+constexpr int SP_THREADS = 256;
+constexpr int SP_WARPS = SP_THREADS / 32;
+constexpr int SP_QUEUE = 1024;  // hot segments gathered per pass of a CTA
+constexpr int SP_CHUNK = 8192;  // segment maxima scanned per CTA
+
+// Exact candidate test of cell (t, r) with value v by one warp: every count in
+// the clipped window is <= v and an equal count sits at a higher cell index.
+// The +-1 row, +-15 column neighbourhood first (most non-maxima fail there),
+// then the whole window as one flat range, 8 loads in flight per lane.
+__device__ __forceinline__ bool warp_is_candidate(const uint32_t *A, int n_theta, int n_rho, int t,
+                                                  int r, uint32_t v, int ht, int hr, int lane) {
+  const uint32_t idx = static_cast<uint32_t>(t) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(r);
+  const int ta = max(t - ht, 0), tb = min(t + ht, n_theta - 1);
+  const int ra = max(r - hr, 0), rb = min(r + hr, n_rho - 1);
+  bool bad = false;
+  {
+    const int dr = lane - 15;  // lanes 0..30: columns r-15 .. r+15
+    if (lane < 31 && r + dr >= ra && r + dr <= rb) {
+      for (int tt = max(t - 1, ta); tt <= min(t + 1, tb); ++tt) {
+        const uint32_t ci = static_cast<uint32_t>(tt) * static_cast<uint32_t>(n_rho) +
+                            static_cast<uint32_t>(r + dr);
+        const uint32_t w = __ldg(A + ci);
+        bad = bad || w > v || (w == v && ci < idx);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) return false;
+  const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
+  for (int c0 = 0; c0 < cells; c0 += 32 * 8) {
+    uint32_t w[8], ci[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + 32 * u + lane;
+      const int tt = ta + c / wc, rr = ra + c % wc;
+      ci[u] = static_cast<uint32_t>(tt) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(rr);
+      w[u] = c < cells ? __ldg(A + ci[u]) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bad = bad || w[u] > v || (w[u] == v && ci[u] < idx);
+    if (__any_sync(0xffffffffu, bad)) return false;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(SP_THREADS) peaks_sparse_kernel(const PeaksParams p) {
+  __shared__ int s_q[SP_QUEUE];
+  __shared__ int s_nq;
+  const int f = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t g = p.gtau[f];
+  if (g == 0u) return;  // no certified bound: the dense search handles this frame
+  const uint32_t tau = g > p.floor_votes ? g : p.floor_votes;
+  const int nseg = p.n_seg, n_rho = p.n_rho, n_theta = p.n_theta;
+  const int total = n_theta * nseg;
+  const uint32_t *S = p.segmax + static_cast<int64_t>(f) * total;
+  const uint32_t *A = p.acc + static_cast<int64_t>(f) * n_theta * n_rho;
+  const int c0 = blockIdx.x * SP_CHUNK, c1 = min(total, c0 + SP_CHUNK);
+  for (int base = c0; base < c1; base += SP_QUEUE) {
+    if (tid == 0) s_nq = 0;
+    __syncthreads();
+    const int end = min(c1, base + SP_QUEUE);
+    for (int i = base + tid; i < end; i += SP_THREADS)
+      if (S[i] >= tau) s_q[atomicAdd(&s_nq, 1)] = i;
+    __syncthreads();
+    const int nq = s_nq;
+    for (int q = warp; q < nq; q += SP_WARPS) {
+      const int u = s_q[q];
+      const int t = u / nseg, s = u - t * nseg;
+      const int r = s * 32 + lane;
+      const uint32_t v = r < n_rho ? __ldg(A + static_cast<int64_t>(t) * n_rho + r) : 0u;
+      uint32_t m = __ballot_sync(0xffffffffu, r < n_rho && v >= tau);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t cv = __shfl_sync(0xffffffffu, v, b);
+        if (warp_is_candidate(A, n_theta, n_rho, t, s * 32 + b, cv, p.half_theta, p.half_rho,
+                              lane) &&
+            lane == 0) {
+          const uint32_t slot = atomicAdd(p.ncand + f, 1u);
+          if (slot < static_cast<uint32_t>(SP_CAP))
+            p.cand[static_cast<int64_t>(f) * SP_CAP + slot] =
+                mk_key(cv, static_cast<uint32_t>(t * n_rho + s * 32 + b));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// One CTA per frame: the top k of the sparse candidates (a bitonic sort of at
+// most SP_CAP keys) -> peaks, n_peaks, resolved = 1; or nothing (resolved = 0)
+// when the frame had no certified bound or overflowed the list.
+__global__ void __launch_bounds__(PK_THREADS) peaks_sparse_finish_kernel(const PeaksParams p) {
+  __shared__ u64 keys[SP_CAP];
+  const int f = blockIdx.x;
+  const uint32_t n = p.ncand[f];
+  if (p.gtau[f] == 0u || n > static_cast<uint32_t>(SP_CAP)) return;  // resolved stays 0
+  int n2 = 1;
+  while (n2 < static_cast<int>(n)) n2 <<= 1;
+  const u64 *in = p.cand + static_cast<int64_t>(f) * SP_CAP;
+  for (int i = threadIdx.x; i < n2; i += PK_THREADS) keys[i] = i < static_cast<int>(n) ? in[i] : 0ull;
+  __syncthreads();
+  bitonic_desc(keys, n2);
+  const int keep = min(static_cast<int>(n), p.k);
+  ld_peak *out = p.peaks + static_cast<int64_t>(f) * p.k;
+  for (int i = threadIdx.x; i < p.k; i += PK_THREADS) {
+    ld_peak pk;
+    if (i < keep) {
+      const u64 key = keys[i];
+      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+      pk.theta_bin = static_cast<int32_t>(idx / static_cast<uint32_t>(p.n_rho));
+      pk.rho_bin = static_cast<int32_t>(idx % static_cast<uint32_t>(p.n_rho));
+      pk.votes = static_cast<uint32_t>(key >> 32);
+    } else {
+      pk.theta_bin = -1;
+      pk.rho_bin = -1;
+      pk.votes = 0u;
+    }
+    out[i] = pk;
+  }
+  if (threadIdx.x == 0) {
+    p.n_peaks[f] = keep;
+    p.resolved[f] = 1u;
+  }
+}
+
 __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksParams p) {
   __shared__ u64 buf[PK_BUF];
   __shared__ u64 top[LD_MAX_K];
   __shared__ int s_ntop;
   const int f = blockIdx.x;
+  if (frame_resolved(p, f)) return;
   const u64 *in = p.band_keys + static_cast<int64_t>(f) * p.n_units * p.k;
   const int n_in = p.n_units * p.k;
   __shared__ int s_nbuf;
@@ -391,6 +548,7 @@ __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksP
   __shared__ int s_nbuf, s_nsurv;
 
   const int tile = blockIdx.x, f = blockIdx.y;
+  if (frame_resolved(p, f)) return;
   const int tt = tile / p.tiles_r, tr = tile - tt * p.tiles_r;
   const int t0 = tt * PT_TR;
   const int hr = p.half_rho;
@@ -550,6 +708,7 @@ __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
   __shared__ uint32_t s_tau;
 
   const int unit = blockIdx.x, f = blockIdx.y;
+  if (frame_resolved(p, f)) return;
   const int strip = unit / p.st_chunks, chunk = unit - strip * p.st_chunks;
   const int hr = p.half_rho, n_rho = p.n_rho, n_theta = p.n_theta;
   const int cbase = strip * p.st_sw - hr;  // global column of loaded column 0
@@ -822,8 +981,7 @@ static size_t stream_smem_bytes(int width, int sw, int ht, int hr, int k) {
 static bool peaks_stream_plan(int batch, int n_theta, int n_rho, int half_theta, int half_rho,
                               int k, int sm_count, PeaksParams *p, int *cpt_out, size_t *smem) {
   if (half_theta > PT_MAX_HT) return false;
-  const char *env_cpt = getenv("LD_PEAKS_CPT");
-  int cpt = (half_theta <= 6 && !(env_cpt && env_cpt[0] == '2')) ? 4 : 2;
+  int cpt = half_theta <= LD_PS_CPT4_MAX_HT ? 4 : 2;
   if (n_rho < cpt) cpt = 2;      // the clamped row pointer needs n_rho >= CPT
   if (n_rho < cpt) return false;  // (n_rho = 2D + 1 >= 3 for every image)
   int best_s = 0, best_nt = 0;
@@ -1023,6 +1181,7 @@ __global__ void __launch_bounds__(32 * PW_W, LD_PW_MINB) peaks_warp_kernel(const
   extern __shared__ __align__(16) unsigned char psm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x * PW_W + warp, f = blockIdx.y;
+  if (frame_resolved(p, f)) return;
   if (unit >= p.n_units) return;  // whole warp; no CTA-wide synchronisation below
   PwSmem &S = reinterpret_cast<PwSmem *>(psm)[warp];
   constexpr int NV = PW_G + 2 * HT;  // rows one group reads
@@ -1158,8 +1317,6 @@ static size_t warp_smem_bytes(int) { return PW_W * sizeof(PwSmem); }
 // Warp-strip geometry; false when the window or k do not fit the kernel.
 static bool peaks_warp_plan(int batch, int n_theta, int n_rho, int half_theta, int half_rho, int k,
                             int sm_count, PeaksParams *p, size_t *smem) {
-  const char *env = getenv("LD_PEAKS_KERNEL");
-  if (env && env[0] == 's') return false;  // force the CTA streaming kernel
   if (half_theta > 3 || half_rho < 4 || half_rho > 64 || k > PW_KMAX || n_rho < PW_CPT)
     return false;
   const int sw = PW_COLS - 2 * half_rho;
@@ -1260,30 +1417,41 @@ extern "C" int ld_debug_error_line(void) {
 }
 #endif
 
-size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k) {
-  // per-frame thresholds (256-B padded), then the per-unit top-k keys: worst
-  // case over the kernels (tiles/units of >= 16 rows x >= 32 columns, or
-  // bands of PK_ROWS rows)
+PeaksLayout peaks_layout(int batch, int n_theta, int n_rho, int k) {
+  // per-frame thresholds, resolved flags and sparse candidate counts (each
+  // 256-B padded), the sparse candidate keys, then the per-unit top-k keys:
+  // worst case over the dense kernels (tiles/units of >= 16 rows x >= 32
+  // columns, or bands of PK_ROWS rows)
   const size_t tiles = static_cast<size_t>((n_theta + PT_TR - 1) / PT_TR) * ((n_rho + 31) / 32);
   const size_t bands = static_cast<size_t>((n_theta + PK_ROWS - 1) / PK_ROWS);
   const size_t head = (sizeof(uint32_t) * static_cast<size_t>(batch) + 255) / 256 * 256;
-  return head + static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
+  PeaksLayout L;
+  L.gtau = 0;
+  L.resolved = head;
+  L.ncand = 2 * head;
+  L.cand = 3 * head;
+  L.keys = L.cand + sizeof(u64) * static_cast<size_t>(batch) * SP_CAP;
+  L.total = L.keys + static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
+  return L;
 }
 
-static bool g_tile_attr[64][PT_MAX_HT + 1];
+size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k) {
+  return peaks_layout(batch, n_theta, n_rho, k).total;
+}
 
-static bool g_stream_attr[64][2][PT_MAX_HT + 1];
-static bool g_warp_attr[64][4];
+static AttrOnce g_tile_attr[PT_MAX_HT + 1];
+static AttrOnce g_stream_attr[2][PT_MAX_HT + 1];
+static AttrOnce g_warp_attr[4];
 
-// Per-frame starting thresholds of the streaming kernels: the verified peak
-// hint when one is given for an unrestricted search, else 0.
-// (p.hint_hdr is cleared when the hint is not used, which the warp kernel reads)
-static cudaError_t init_gtau(PeaksParams &p, bool restricted, cudaStream_t stream) {
-  if (getenv("LD_PEAKS_GTAU_KEEP")) return cudaSuccess;  // experiments (tools/exp_tau_oracle.py)
-  // the hint pays when its verification is cheap next to the search it
-  // shortens: a window of at most 64 K cells in total over k keys
+// Per-frame starting thresholds: the verified peak hint (R25) when one is
+// given for an unrestricted search and its verification is cheap next to the
+// search it shortens (a window of at most 64 K cells in total over k keys),
+// else 0.  Returns whether the hint is used (p.hint_hdr is cleared if not,
+// which the warp kernel reads).
+static cudaError_t init_gtau(PeaksParams &p, bool restricted, cudaStream_t stream, bool *hinted) {
   const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
-  if (p.hint_hdr && !restricted && wcells * p.k <= 65536) {
+  *hinted = p.hint_hdr && !restricted && wcells * p.k <= 65536;
+  if (*hinted) {
     peaks_hint_kernel<<<p.batch, PH_THREADS, 0, stream>>>(p);
     note_launch();
     return cudaGetLastError();
@@ -1293,12 +1461,27 @@ static cudaError_t init_gtau(PeaksParams &p, bool restricted, cudaStream_t strea
   return cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
 }
 
-cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
+// The sparse search (R30) over the frames whose bound the hint certified;
+// the dense kernels launched after it skip the frames it resolved.
+static cudaError_t launch_sparse(const PeaksParams &p, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(p.n_theta) * p.n_seg;
+  dim3 g1(static_cast<unsigned>((total + SP_CHUNK - 1) / SP_CHUNK), p.batch);
+  peaks_sparse_kernel<<<g1, SP_THREADS, 0, stream>>>(p);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  peaks_sparse_finish_kernel<<<p.batch, PK_THREADS, 0, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t stream) {
   PeaksParams p = p_in;
   size_t smem = 0;
-  const char *env = getenv("LD_PEAKS_KERNEL");
-  const bool force_band = env && env[0] == 'b';
-  const bool force_tile = env && env[0] == 't';
+  const bool force_band = (flags & LD_PEAKS_FORCE_BAND) != 0;
+  const bool force_tile = (flags & LD_PEAKS_FORCE_TILE) != 0;
+  const bool force_stream = (flags & LD_PEAKS_FORCE_STREAM) != 0;
+  const bool dense_only = (flags & LD_PEAKS_DENSE) != 0;
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = 148;
@@ -1308,49 +1491,51 @@ cudaError_t launch_peaks(const PeaksParams &p_in, cudaStream_t stream) {
   // the tiled kernel has no row restriction and is skipped when one is set
   const int n_cand = p.cand_t1 - p.cand_t0;
   const bool restricted = p.cand_t0 != 0 || p.cand_t1 != p.n_theta || p.theta_offset != 0;
+  p.resolved = nullptr;
   if (n_cand <= 0) {  // no candidate rows: the merge writes sentinels and 0 peaks
     p.n_units = 0;
     peaks_merge_kernel<<<p.batch, PK_THREADS, 0, stream>>>(p);
     note_launch();
     return cudaGetLastError();
   }
-  if (!force_band && !force_tile &&
-      peaks_warp_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem)) {
-    cudaError_t em = init_gtau(p, restricted, stream);
+  const bool dense_cheap = !force_band && !force_tile && !force_stream &&
+      peaks_warp_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem);
+  const bool dense_stream = !dense_cheap && !force_band && !force_tile &&
+      peaks_stream_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
+                        &smem);
+  if (dense_cheap || dense_stream) {
+    // the hint (and with it the sparse search) serves the warp and streaming kernels
+    PeaksParams ps = p;
+    ps.ncand = (ps.hint_hdr && ps.segmax && !dense_only) ? p_in.ncand : nullptr;
+    bool hinted = false;
+    cudaError_t em = init_gtau(ps, restricted, stream, &hinted);
     if (em != cudaSuccess) return em;
-    WarpKernel kern = warp_kernel(p.half_theta);
-    if (!g_warp_attr[dev & 63][p.half_theta]) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      g_warp_attr[dev & 63][p.half_theta] = true;
+    p.hint_hdr = ps.hint_hdr;
+    p.hint_keys = ps.hint_keys;
+    if (hinted && ps.ncand) {
+      ps.resolved = p_in.resolved;
+      em = launch_sparse(ps, stream);
+      if (em != cudaSuccess) return em;
+      p.resolved = p_in.resolved;
     }
+  }
+  if (dense_cheap) {
+    WarpKernel kern = warp_kernel(p.half_theta);
+    cudaError_t e = ensure_smem_attr(g_warp_attr[p.half_theta], kern, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
     dim3 g1((p.n_units + PW_W - 1) / PW_W, p.batch);
     kern<<<g1, 32 * PW_W, smem, stream>>>(p);
-  } else if (!force_band && !force_tile &&
-      peaks_stream_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &cpt,
-                        &smem)) {
-    cudaError_t em = init_gtau(p, restricted, stream);
-    if (em != cudaSuccess) return em;
+  } else if (dense_stream) {
     StreamKernel kern = stream_kernel(p.half_theta, cpt);
-    bool &attr = g_stream_attr[dev & 63][cpt == 4][p.half_theta];
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           220 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    cudaError_t e = ensure_smem_attr(g_stream_attr[cpt == 4][p.half_theta], kern, 220 * 1024);
+    if (e != cudaSuccess) return e;
     dim3 g1(p.n_units, p.batch);
     kern<<<g1, p.st_nt, smem, stream>>>(p);
   } else if (!force_band && !restricted &&
              peaks_tile_plan(p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, &p, &smem)) {
     TileKernel kern = tile_kernel(p.half_theta);
-    if (!g_tile_attr[dev & 63][p.half_theta]) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           200 * 1024);
-      if (e != cudaSuccess) return e;
-      g_tile_attr[dev & 63][p.half_theta] = true;
-    }
+    cudaError_t e = ensure_smem_attr(g_tile_attr[p.half_theta], kern, 200 * 1024);
+    if (e != cudaSuccess) return e;
     dim3 g1(p.n_units, p.batch);
     kern<<<g1, p.tch, smem, stream>>>(p);
   } else {

@@ -3,8 +3,10 @@
 One process per GPU, ``torch.distributed`` for the plumbing.  Two partitions:
 
 * **frame shards** (cfg3, cfg4): a batch of independent frames splits into
-  contiguous per-rank ranges; every rank runs the whole path on its frames with
-  no data-path collective (weak scaling).
+  contiguous per-rank ranges (BASELINE.json: the batch "sharded across
+  1/2/4/8 GPUs", i.e. strong scaling of a fixed batch; bench.py --scaling weak
+  gives every rank a whole batch instead); every rank runs the whole path on
+  its frames with no data-path collective.
 * **row bands** (cfg5): one large image splits into bands of rows.  Each rank
   runs the fused Sobel + binarize + compaction on its band (1-row halo, global
   border semantics via ``ld_image.row_begin/row_end``), votes its global-y
@@ -12,6 +14,10 @@ One process per GPU, ``torch.distributed`` for the plumbing.  Two partitions:
   summed with one ``all_reduce(SUM)`` -- the only exchange step of the method
   (the Hough transform is additive over edge sets, SURVEY §8(c) pins).  Peaks
   then run on every rank and are identical.
+* **theta shards** (cfg5, NEXT 1): row bands for Sobel, the band edge sets
+  exchanged as fixed-size bitmaps (all_gather, no host synchronisation), each
+  rank votes all edges into its own theta rows (+ halo) and the per-rank top-k
+  lists are all-gathered and merged on the device.
 
 The accumulator is ``uint32`` (DESIGN R12) held in an ``int32`` tensor; the SUM
 is exact because every count is at most W*H < 2^31.  All arithmetic of the
@@ -84,9 +90,12 @@ class BandedDetector:
     """Row-band detector of one large image on this rank (cfg5).
 
     ``load(gray)`` copies this rank's band (with halo) of a full uint8 [H][W]
-    image to the device once; ``__call__`` then runs, on ``stream``:
-    ld_sobel_binarize(band) -> ld_hough_accumulate(full-size partial acc) ->
-    all_reduce(SUM) -> ld_hough_peaks, and returns (peaks, n_peaks, acc, count).
+    image to the device once; ``__call__`` then runs, on the current stream
+    (or ``stream``): ld_sobel_binarize(band) -> ld_hough_accumulate(full-size
+    partial acc) -> all_reduce(SUM) -> ld_hough_peaks, and returns (peaks,
+    n_peaks, acc, count).  ``mark(j)``, if given, is called at the stage
+    boundaries j = 0 (start), 1 (after Sobel), 2 (after voting), 3 (after the
+    all_reduce), 4 (after peaks) -- bench.py records CUDA events there.
     """
 
     def __init__(self, width, height, n_theta, cos_q15, sin_q15, threshold, k, half_theta,
@@ -134,41 +143,45 @@ class BandedDetector:
             band = torch.from_numpy(band.copy())
         self.gray[:, :self.w].copy_(band)
 
-    def __call__(self, stream=None):
-        import torch
-        if stream is not None and not isinstance(stream, int):
-            with torch.cuda.stream(stream):  # the collective orders on torch's current stream
-                return self._run(None)
-        return self._run(stream)
+    @property
+    def result(self):
+        return self.peaks, self.n_peaks
 
-    def _run(self, stream):
+    def __call__(self, stream=None, mark=None):
+        import torch
+        if isinstance(stream, int):  # a raw cudaStream_t handle
+            stream = torch.cuda.ExternalStream(stream, device=self.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        # one stream for the kernels AND the collective (NCCL orders on torch's
+        # current stream), so the all_reduce sums finished partials
+        with torch.cuda.device(self.device), torch.cuda.stream(stream):
+            return self._run(stream, mark or (lambda j: None))
+
+    def _run(self, stream, mark):
         ld = self.ld
         self.launches = 0
+        mark(0)
         if self.plan.rows > 0:
             ld.ld_sobel_binarize(self.gray, self.img, self.threshold, None, self.edges,
                                  self.edge_stride, self.count, stream)
             self.launches += ld.ld_last_launch_count()
         else:
             self.count.zero_()
-        if self.hint is not None:
-            ld.ld_hough_accumulate_hint(self.edges, self.count, self.edge_stride, 1, self.w,
-                                        self.h, self.n_theta, self.cos, self.sin, self.acc,
-                                        self.hint, self.hint_bytes, stream)
-        else:
-            ld.ld_hough_accumulate(self.edges, self.count, self.edge_stride, 1, self.w, self.h,
-                                   self.n_theta, self.cos, self.sin, self.acc, stream)
+        mark(1)
+        ld.ld_hough_accumulate_opt(self.edges, self.count, self.edge_stride, 1, self.w, self.h,
+                                   self.n_theta, self.cos, self.sin, 0, self.acc, self.hint,
+                                   self.hint_bytes, stream)
         self.launches += ld.ld_last_launch_count()
+        mark(2)
         allreduce_accumulator(self.acc, self.group)
-        if self.hint is not None:
-            ld.ld_hough_peaks_hinted(self.acc, 1, self.n_theta, self.n_rho, self.half_theta,
-                                     self.half_rho, self.min_votes, self.k, self.hint,
-                                     self.hint_bytes, self.peaks, self.n_peaks, self.ws,
-                                     self.ws_bytes, stream)
-        else:
-            ld.ld_hough_peaks(self.acc, 1, self.n_theta, self.n_rho, self.half_theta,
-                              self.half_rho, self.min_votes, self.k, self.peaks, self.n_peaks,
-                              self.ws, self.ws_bytes, stream)
+        mark(3)
+        ld.ld_hough_peaks_opt(self.acc, 1, self.n_theta, self.n_rho, self.half_theta,
+                              self.half_rho, self.min_votes, self.k, 0, self.n_theta, 0,
+                              self.hint, self.hint_bytes, 0, self.peaks, self.n_peaks, self.ws,
+                              self.ws_bytes, stream)
         self.launches += ld.ld_last_launch_count()
+        mark(4)
         return self.peaks, self.n_peaks, self.acc, self.count
 
 
@@ -186,46 +199,36 @@ def theta_slice(n_theta: int, half_theta: int, t0: int, t1: int) -> tuple[int, i
     return max(t0 - half_theta, 0), min(t1 + half_theta, n_theta)
 
 
-def merge_peak_lists(peaks, n_peaks, n_rho: int, k: int):
-    """Merge per-shard top-k lists (global theta bins) into the global top-k.
-
-    peaks: int32 [S][k][3] (theta_bin, rho_bin, votes as uint32 bits), n_peaks
-    int32 [S].  Keys are (votes, -theta, -rho) (DESIGN R14) as one int64
-    votes * 2^32 + (2^32 - 1 - (theta * n_rho + rho)); runs on the tensors'
-    device (no host synchronisation).  Returns (peaks [k][3], n_peaks [1])."""
+def merge_peak_lists(peaks, n_peaks, n_rho: int, k: int, stream=None):
+    """Merge per-shard top-k lists (global theta bins) into the global top-k
+    on the device (libld ld_merge_peak_lists, key (votes, -theta, -rho), DESIGN
+    R14; no host synchronisation).  peaks: int32 [S][k][3], n_peaks int32 [S].
+    Returns (peaks [k][3], n_peaks [1])."""
     import torch
-    s, kk, _ = peaks.shape
-    p = peaks.reshape(s * kk, 3).to(torch.int64)
-    valid = (torch.arange(kk, device=peaks.device)[None, :] < n_peaks[:, None].to(torch.int64))
-    valid = valid.reshape(-1)
-    votes = p[:, 2] & 0xFFFFFFFF
-    idx = p[:, 0] * n_rho + p[:, 1]
-    key = votes * (1 << 32) + (0xFFFFFFFF - idx)
-    key = torch.where(valid, key, torch.full_like(key, -1))
-    top = torch.topk(key, min(k, key.numel())).values
-    ok = top >= 0
-    idx_out = 0xFFFFFFFF - (top & 0xFFFFFFFF)
-    out = torch.full((k, 3), -1, dtype=torch.int64, device=peaks.device)
-    out[:, 2] = 0
-    n = top.numel()
-    out[:n, 0] = torch.where(ok, idx_out // n_rho, torch.full_like(top, -1))
-    out[:n, 1] = torch.where(ok, idx_out % n_rho, torch.full_like(top, -1))
-    out[:n, 2] = torch.where(ok, top >> 32, torch.zeros_like(top))
-    cnt = ok.sum().to(torch.int32).reshape(1)
-    return out.to(torch.int32), cnt
+    from . import ld
+    s = peaks.shape[0]
+    out = torch.empty((k, 3), dtype=torch.int32, device=peaks.device)
+    n = torch.empty((1,), dtype=torch.int32, device=peaks.device)
+    ld.ld_merge_peak_lists(peaks.contiguous(), n_peaks.contiguous(), s, k, n_rho, out, n, stream)
+    return out, n
 
 
 class ThetaShardedDetector:
     """Theta-sharded detection of one large image (cfg5, NEXT 1).
 
     Sobel + binarize + compaction run on this rank's row band (as in
-    BandedDetector); the band edge lists are all-gathered (4 B per edge), every
-    rank votes ALL edges into only its theta shard plus half_theta halo rows
-    (ld_hough_accumulate on a slice of the trig table), finds the candidates of
-    its own rows (ld_hough_peaks_ex with global theta bins), and the per-rank
-    top-k lists are all-gathered (12 B x k per rank) and merged.  Compared with
-    the row-band all_reduce of the 4 n_theta n_rho-byte accumulator this
-    exchanges ~4 E bytes, and voting and peaks both scale with the rank count.
+    BandedDetector); the band's edge set is turned into a fixed-size bitmap
+    (ld_edges_to_bitmask, 1 bit per band pixel) and the bitmaps are
+    all-gathered -- fixed-size, so no host-known sizes and no host
+    synchronisation -- and expanded back into one edge list of the whole image
+    on every rank (ld_bitmask_to_edges).  Every rank then votes ALL edges into
+    only its theta shard plus half_theta halo rows (ld_hough_accumulate on a
+    slice of the trig table), finds the candidates of its own rows
+    (ld_hough_peaks_ex with global theta bins), and the per-rank top-k lists
+    are all-gathered (12 B x k per rank) and merged on the device
+    (ld_merge_peak_lists).  Compared with the row-band all_reduce of the
+    4 n_theta n_rho-byte accumulator (47.5 MB for cfg5) this exchanges W*H/8
+    bytes (2.1 MB), and voting and peaks both scale with the rank count.
     Results are bit-identical to the single-GPU path and the oracle.
     """
 
@@ -246,14 +249,15 @@ class ThetaShardedDetector:
         c = ld._host_i32(cos_q15)
         s = ld._host_i32(sin_q15)
         self.cos_s, self.sin_s = c[self.g0:self.g1].copy(), s[self.g0:self.g1].copy()
-        # gathered edge lists: every rank's band holds at most rows * (W - 2) edges
-        self.max_band_edges = max(BandPlan.make(width, height, r, world).max_edges
-                                  for r in range(world))
-        self.gathered = torch.empty((world, max(self.max_band_edges, 1)), dtype=torch.int32,
-                                    device=self.device)
-        self.send = torch.zeros((max(self.max_band_edges, 1),), dtype=torch.int32,
-                                device=self.device)
-        self.all_stride = ld._round_up(max(world * self.max_band_edges, 1), 4)
+        # band bitmaps: every rank's block has the largest band's row count
+        plans = [BandPlan.make(width, height, r, world) for r in range(world)]
+        self.block_rows = [p.rows for p in plans]
+        self.block_begin = [p.row_begin for p in plans]
+        self.stride_rows = max(max(self.block_rows), 1)
+        self.words = ld.ld_edge_bitmask_words(width, self.stride_rows)
+        self.bits = torch.zeros((self.words,), dtype=torch.int32, device=self.device)
+        self.all_bits = torch.zeros((world * self.words,), dtype=torch.int32, device=self.device)
+        self.all_stride = ld._round_up(max(height * width, 1), 4)
         self.all_edges = torch.zeros((self.all_stride,), dtype=torch.int32, device=self.device)
         self.total = torch.zeros((1,), dtype=torch.int32, device=self.device)
         ns = max(self.g1 - self.g0, 1)
@@ -262,60 +266,67 @@ class ThetaShardedDetector:
         self.ws = torch.empty((max(self.ws_bytes, 16),), dtype=torch.uint8, device=self.device)
         self.peaks = torch.empty((1, k, 3), dtype=torch.int32, device=self.device)
         self.n_peaks = torch.empty((1,), dtype=torch.int32, device=self.device)
+        self.allp = torch.empty((world, k, 3), dtype=torch.int32, device=self.device)
+        self.alln = torch.empty((world,), dtype=torch.int32, device=self.device)
+        self.out_peaks = torch.empty((k, 3), dtype=torch.int32, device=self.device)
+        self.out_n = torch.empty((1,), dtype=torch.int32, device=self.device)
         self.launches = 0
 
     def load(self, gray_full):
         self.band.load(gray_full)
 
+    @property
+    def result(self):
+        """(peaks [k][3], n_peaks [1]) of the last call, identical on every rank."""
+        return self.out_peaks, self.out_n
+
     def __call__(self, mark=None):
-        """Returns (peaks [1][k][3], n_peaks [1]) on every rank.  `mark(j)`, if
-        given, is called at the stage boundaries j = 0 (start), 1 (after
-        Sobel), 2 (after the edge exchange), 3 (after voting), 4 (after
-        peaks), 5 (after the top-k exchange and merge) -- bench.py records
-        CUDA events there."""
+        """Returns (peaks [k][3], n_peaks [1]) on every rank, on the current
+        stream.  `mark(j)`, if given, is called at the stage boundaries j = 0
+        (start), 1 (after Sobel), 2 (after the edge exchange), 3 (after
+        voting), 4 (after peaks), 5 (after the top-k exchange and merge) --
+        bench.py records CUDA events there."""
         import torch
         import torch.distributed as dist
         ld, b = self.ld, self.band
         mark = mark or (lambda j: None)
         self.launches = 0
-        mark(0)
-        if b.plan.rows > 0:
-            ld.ld_sobel_binarize(b.gray, b.img, b.threshold, None, b.edges, b.edge_stride,
-                                 b.count, None)
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            mark(0)
+            if b.plan.rows > 0:
+                ld.ld_sobel_binarize(b.gray, b.img, b.threshold, None, b.edges, b.edge_stride,
+                                     b.count, stream)
+                self.launches += ld.ld_last_launch_count()
+            else:
+                b.count.zero_()
+            mark(1)
+            multi = dist.is_initialized() and self.world > 1
+            if multi:
+                ld.ld_edges_to_bitmask(b.edges, b.count, self.w, b.plan.row_begin,
+                                       self.stride_rows, self.bits, stream)
+                self.launches += ld.ld_last_launch_count()
+                dist.all_gather_into_tensor(self.all_bits, self.bits, group=self.group)
+                ld.ld_bitmask_to_edges(self.all_bits, self.w, self.block_begin, self.block_rows,
+                                       self.stride_rows, self.all_edges, self.all_stride,
+                                       self.total, stream)
+                self.launches += ld.ld_last_launch_count()
+                edges, count, stride = self.all_edges, self.total, self.all_stride
+            else:
+                edges, count, stride = b.edges, b.count, b.edge_stride
+            mark(2)
+            self.vote_and_peaks(edges, count, stride, mark)
+            if multi:
+                dist.all_gather_into_tensor(self.allp, self.peaks, group=self.group)
+                dist.all_gather_into_tensor(self.alln, self.n_peaks, group=self.group)
+                ld.ld_merge_peak_lists(self.allp, self.alln, self.world, self.k, self.n_rho,
+                                       self.out_peaks, self.out_n, stream)
+            else:
+                ld.ld_merge_peak_lists(self.peaks, self.n_peaks, 1, self.k, self.n_rho,
+                                       self.out_peaks, self.out_n, stream)
             self.launches += ld.ld_last_launch_count()
-        else:
-            b.count.zero_()
-        mark(1)
-        multi = dist.is_initialized() and self.world > 1
-        if multi:
-            counts = torch.empty((self.world,), dtype=torch.int32, device=self.device)
-            dist.all_gather_into_tensor(counts, b.count, group=self.group)
-            cl = counts.tolist()  # host sizes for the variable-length gather
-            m = max(max(cl), 1)
-            mine = cl[self.rank]
-            if mine:
-                self.send[:mine].copy_(b.edges[:mine])
-            dist.all_gather_into_tensor(self._gbuf(m), self.send[:m], group=self.group)
-            parts = [self._gview(m)[r, :cl[r]] for r in range(self.world)]
-            n = sum(cl)
-            if n:
-                torch.cat(parts, out=self.all_edges[:n])
-            self.total.fill_(n)
-            edges, count, stride = self.all_edges, self.total, self.all_stride
-        else:
-            edges, count, stride = b.edges, b.count, b.edge_stride
-        mark(2)
-        self.vote_and_peaks(edges, count, stride, mark)
-        if not multi:
             mark(5)
-            return self.peaks, self.n_peaks
-        allp = torch.empty((self.world, self.k, 3), dtype=torch.int32, device=self.device)
-        alln = torch.empty((self.world,), dtype=torch.int32, device=self.device)
-        dist.all_gather_into_tensor(allp, self.peaks, group=self.group)
-        dist.all_gather_into_tensor(alln, self.n_peaks, group=self.group)
-        p, n = merge_peak_lists(allp, alln, self.n_rho, self.k)
-        mark(5)
-        return p[None], n
+        return self.out_peaks, self.out_n
 
     def vote_and_peaks(self, edges, count, stride, mark=None):
         """This rank's theta shard: vote every edge of the image (device list
@@ -335,10 +346,3 @@ class ThetaShardedDetector:
         self.launches += ld.ld_last_launch_count()
         if mark:
             mark(4)
-
-    def _gbuf(self, m):
-        self._gflat = self.gathered.reshape(-1)[: self.world * m]
-        return self._gflat
-
-    def _gview(self, m):
-        return self._gflat.reshape(self.world, m)

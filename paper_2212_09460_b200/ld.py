@@ -51,10 +51,14 @@ class ld_peak(ctypes.Structure):
 PEAK_DTYPE = np.dtype([("theta_bin", "<i4"), ("rho_bin", "<i4"), ("votes", "<u4")])
 
 LD_FLAG_ZERO_PAD, LD_FLAG_CLAMP_255 = 1, 2
+LD_VOTE_PLAIN = 1
+LD_PEAKS_DENSE, LD_PEAKS_FORCE_STREAM, LD_PEAKS_FORCE_TILE, LD_PEAKS_FORCE_BAND = 1, 2, 4, 8
 
 EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",
            "ld_hough_hint_bytes", "ld_hough_accumulate_hint", "ld_hough_peaks_hinted",
-           "ld_hough_accumulate_f64",
+           "ld_hough_accumulate_f64", "ld_hough_accumulate_opt", "ld_hough_peaks_opt",
+           "ld_edge_bitmask_words", "ld_edges_to_bitmask", "ld_bitmask_to_edges",
+           "ld_merge_peak_lists",
            "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_hough_peaks_ex",
            "ld_hough_peaks_nms_workspace_bytes", "ld_hough_peaks_nms", "ld_peak_lines",
            "ld_extract_segments",
@@ -93,6 +97,10 @@ def lib():
                                ctypes.c_int),
             "ld_hough_peaks_ex": ([P, i32, i32, i32, i32, i32, u32, i32, i32, i32, i32, P, P, P,
                                    sz, P], ctypes.c_int),
+            "ld_hough_accumulate_opt": ([P, P, i64, i32, i32, i32, i32, P, P, u32, P, P, sz, P],
+                                        ctypes.c_int),
+            "ld_hough_peaks_opt": ([P, i32, i32, i32, i32, i32, u32, i32, i32, i32, i32, P, sz,
+                                    u32, P, P, P, sz, P], ctypes.c_int),
             "ld_hough_peaks_nms_workspace_bytes": ([i32, i32, i32], sz),
             "ld_hough_peaks_nms": ([P, i32, i32, i32, i32, i32, u32, u32, u32, i32, P, P, P, sz,
                                     P], ctypes.c_int),
@@ -109,6 +117,10 @@ def lib():
                                       sz, P], ctypes.c_int),
             "ld_bench_smem_atomics": ([i32, i32, i32, ctypes.POINTER(ctypes.c_uint64), P, P],
                                       ctypes.c_int),
+            "ld_edge_bitmask_words": ([i32, i32], i64),
+            "ld_edges_to_bitmask": ([P, P, i32, i32, i32, P, P], ctypes.c_int),
+            "ld_bitmask_to_edges": ([P, i32, i32, P, P, i32, P, i64, P, P], ctypes.c_int),
+            "ld_merge_peak_lists": ([P, P, i32, i32, i32, P, P, P], ctypes.c_int),
             "ld_device_sm_count": ([], i32),
             "ld_device_l2_bytes": ([], i64),
             "ld_status_string": ([ctypes.c_int], ctypes.c_char_p),
@@ -197,6 +209,15 @@ def ld_hough_accumulate(edge_xy, edge_count, edge_stride, batch, width, height, 
                                      _addr(c), _addr(s), _addr(acc), _stream(stream)))
 
 
+def ld_hough_accumulate_opt(edge_xy, edge_count, edge_stride, batch, width, height, n_theta,
+                            cos_q15, sin_q15, flags, acc, hint=None, hint_bytes=0, stream=None):
+    c, s = _host_i32(cos_q15), _host_i32(sin_q15)
+    _check(lib().ld_hough_accumulate_opt(_addr(edge_xy), _addr(edge_count), int(edge_stride),
+                                         int(batch), int(width), int(height), int(n_theta),
+                                         _addr(c), _addr(s), int(flags), _addr(acc), _addr(hint),
+                                         int(hint_bytes), _stream(stream)))
+
+
 def ld_hough_accumulate_f64(edge_xy, edge_count, edge_stride, batch, width, height, n_theta,
                             cos_f64, sin_f64, acc, stream=None):
     c = np.ascontiguousarray(np.asarray(cos_f64, dtype=np.float64))
@@ -261,6 +282,17 @@ def ld_hough_peaks_ex(acc, batch, n_theta, n_rho, half_theta, half_rho, min_vote
                                    int(cand_row_begin), int(cand_row_end), int(theta_offset),
                                    _addr(peaks), _addr(n_peaks), _addr(workspace),
                                    int(workspace_bytes), _stream(stream)))
+
+
+def ld_hough_peaks_opt(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k,
+                       cand_row_begin, cand_row_end, theta_offset, hint, hint_bytes, flags, peaks,
+                       n_peaks, workspace, workspace_bytes, stream=None):
+    _check(lib().ld_hough_peaks_opt(_addr(acc), int(batch), int(n_theta), int(n_rho),
+                                    int(half_theta), int(half_rho), int(min_votes), int(k),
+                                    int(cand_row_begin), int(cand_row_end), int(theta_offset),
+                                    _addr(hint), int(hint_bytes), int(flags), _addr(peaks),
+                                    _addr(n_peaks), _addr(workspace), int(workspace_bytes),
+                                    _stream(stream)))
 
 
 def ld_hough_peaks_nms_workspace_bytes(batch, n_theta, n_rho) -> int:
@@ -343,6 +375,28 @@ def ld_bench_smem_atomics(mode, iters, blocks_per_sm, scratch, stream=None) -> i
     return int(n.value)
 
 
+def ld_edge_bitmask_words(width, rows) -> int:
+    return int(lib().ld_edge_bitmask_words(int(width), int(rows)))
+
+
+def ld_edges_to_bitmask(edge_xy, edge_count, width, row_begin, rows, bits, stream=None):
+    _check(lib().ld_edges_to_bitmask(_addr(edge_xy), _addr(edge_count), int(width),
+                                     int(row_begin), int(rows), _addr(bits), _stream(stream)))
+
+
+def ld_bitmask_to_edges(bits, width, block_row_begin, block_rows, block_stride_rows, edge_xy,
+                        edge_capacity, edge_count, stream=None):
+    rb, rr = _host_i32(block_row_begin), _host_i32(block_rows)
+    _check(lib().ld_bitmask_to_edges(_addr(bits), int(width), int(len(rb)), _addr(rb),
+                                     _addr(rr), int(block_stride_rows), _addr(edge_xy),
+                                     int(edge_capacity), _addr(edge_count), _stream(stream)))
+
+
+def ld_merge_peak_lists(peaks, n_peaks, n_lists, k, n_rho, out, n_out, stream=None):
+    _check(lib().ld_merge_peak_lists(_addr(peaks), _addr(n_peaks), int(n_lists), int(k),
+                                     int(n_rho), _addr(out), _addr(n_out), _stream(stream)))
+
+
 def ld_device_sm_count() -> int:
     return int(lib().ld_device_sm_count())
 
@@ -395,37 +449,41 @@ def sobel_binarize(gray, threshold: int, want_binary=True, want_edges=True, stre
 
 
 def hough_accumulate(edges, counts, edge_stride, width, height, cos_q15, sin_q15, stream=None,
-                     want_hint=False):
-    """Returns acc, or (acc, hint) with want_hint (ld_hough_accumulate_hint)."""
+                     want_hint=False, flags=0):
+    """Returns acc, or (acc, hint) with want_hint (ld_hough_accumulate_hint).
+    flags: LD_VOTE_PLAIN (ld_hough_accumulate_opt)."""
     import torch
     b = counts.shape[0]
     n_theta = len(cos_q15)
     n_rho = 2 * ld_rho_offset(width, height) + 1
     acc = torch.empty((b, n_theta, n_rho), dtype=torch.int32, device=counts.device)
-    if not want_hint:
-        ld_hough_accumulate(edges, counts, edge_stride, b, width, height, n_theta, cos_q15,
-                            sin_q15, acc, stream)
-        return acc
-    hb = ld_hough_hint_bytes(b, width, height, n_theta)
-    hint = torch.empty((hb,), dtype=torch.uint8, device=counts.device)
-    ld_hough_accumulate_hint(edges, counts, edge_stride, b, width, height, n_theta, cos_q15,
-                             sin_q15, acc, hint, hb, stream)
-    return acc, hint
+    hint, hb = None, 0
+    if want_hint:
+        hb = ld_hough_hint_bytes(b, width, height, n_theta)
+        hint = torch.empty((hb,), dtype=torch.uint8, device=counts.device)
+    ld_hough_accumulate_opt(edges, counts, edge_stride, b, width, height, n_theta, cos_q15,
+                            sin_q15, flags, acc, hint, hb, stream)
+    return (acc, hint) if want_hint else acc
 
 
 def hough_peaks(acc, half_theta, half_rho, min_votes, k, stream=None, cand_rows=None,
-                theta_offset=0, hint=None):
+                theta_offset=0, hint=None, flags=0):
     """acc: int32 CUDA [B][n_theta][n_rho] (uint32 bits).  cand_rows=(begin, end)
     and theta_offset select ld_hough_peaks_ex (a theta slice of a larger
     accumulator); hint (from hough_accumulate(want_hint=True)) selects
-    ld_hough_peaks_hinted."""
+    ld_hough_peaks_hinted; flags (LD_PEAKS_*) select ld_hough_peaks_opt."""
     import torch
     b, n_theta, n_rho = acc.shape
     ws_bytes = ld_hough_peaks_workspace_bytes(b, n_theta, n_rho, k)
     ws = torch.empty((max(ws_bytes, 16),), dtype=torch.uint8, device=acc.device)
     peaks = torch.empty((b, k, 3), dtype=torch.int32, device=acc.device)
     n_peaks = torch.empty((b,), dtype=torch.int32, device=acc.device)
-    if hint is not None:
+    if flags:
+        c0, c1 = cand_rows if cand_rows is not None else (0, n_theta)
+        ld_hough_peaks_opt(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, c0, c1,
+                           theta_offset, hint, 0 if hint is None else hint.numel(), flags, peaks,
+                           n_peaks, ws, ws_bytes, stream)
+    elif hint is not None:
         ld_hough_peaks_hinted(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, hint,
                               hint.numel(), peaks, n_peaks, ws, ws_bytes, stream)
     elif cand_rows is None and theta_offset == 0:
@@ -463,11 +521,17 @@ class Detector:
                                 device=self.device) if export_acc else None)
 
     def __call__(self, gray, stream=None):
-        """gray: uint8 CUDA [B][H][pitch] with pitch = round_up(W, 16)."""
-        ld_detect_batch_ex(gray, self.img, self.threshold, self.flags, self.n_theta, self.cos,
-                           self.sin, self.half_theta, self.half_rho, self.min_votes, self.k,
-                           self.peaks, self.n_peaks, self.counts, self.acc, self.ws,
-                           self.ws_bytes, stream)
+        """gray: uint8 CUDA [B][H][pitch] with pitch = round_up(W, 16).  Runs on
+        the detector's device (the C ABI uses the current device), on `stream`
+        or that device's current stream."""
+        import torch
+        with torch.cuda.device(self.device):
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            ld_detect_batch_ex(gray, self.img, self.threshold, self.flags, self.n_theta,
+                               self.cos, self.sin, self.half_theta, self.half_rho,
+                               self.min_votes, self.k, self.peaks, self.n_peaks, self.counts,
+                               self.acc, self.ws, self.ws_bytes, stream)
         return self.peaks, self.n_peaks, self.counts, self.acc
 
 
@@ -499,6 +563,9 @@ class PipelinedDetector:
         det, st = self.slots[self.next]
         self.next = (self.next + 1) % len(self.slots)
         st.wait_stream(torch.cuda.current_stream(det.device))
+        # the caller may drop `gray` right away: keep the caching allocator
+        # from handing its memory to another stream while `st` still reads it
+        gray.record_stream(st)
         det(gray, st)
         ev = torch.cuda.Event()
         ev.record(st)

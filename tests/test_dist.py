@@ -117,8 +117,8 @@ def test_band_accumulators_sum_to_whole_without_collective(oracle):
 
 
 # ----------------------------------------------------------------------------
-# theta-sharded detection (NEXT 1): partition, halo slices and the device-side
-# merge of per-shard top-k lists, through a real gloo process group
+# theta-sharded detection (NEXT 1): partition, halo slices and the exchange of
+# per-shard top-k lists through a real gloo process group
 # ----------------------------------------------------------------------------
 def test_theta_slices_cover_with_halo():
     for nt, ht in [(180, 2), (1024, 10), (7, 3), (3, 0)]:
@@ -145,6 +145,18 @@ def _shard_peaks(oracle, big, t0, t1, ht, hr, k):
     return out, len(own)
 
 
+def _merge_by_key(peaks, n_peaks, n_rho, k):
+    """Top k of the per-shard lists by (votes, -theta, -rho) (DESIGN R14)."""
+    keys = [(int(v), -(int(t) * n_rho + int(r)), int(t), int(r))
+            for lst, n in zip(peaks, n_peaks) for (t, r, v) in lst[:int(n)]]
+    keys.sort(reverse=True)
+    out = np.full((k, 3), -1, np.int32)
+    out[:, 2] = 0
+    for i, (v, _, t, r) in enumerate(keys[:k]):
+        out[i] = (t, r, v)
+    return out, min(k, len(keys))
+
+
 def _theta_worker(rank, world, port, outdir):
     import torch
     import torch.distributed as dist
@@ -163,9 +175,12 @@ def _theta_worker(rank, world, port, outdir):
         alln = [torch.zeros((1,), dtype=torch.int32) for _ in range(world)]
         dist.all_gather(allp, torch.from_numpy(p))
         dist.all_gather(alln, torch.tensor([n], dtype=torch.int32))
-        mp, mn = pdist.merge_peak_lists(torch.stack(allp), torch.cat(alln), big.shape[1], 6)
-        np.save(os.path.join(outdir, "tp%d.npy" % rank), mp.numpy())
-        np.save(os.path.join(outdir, "tn%d.npy" % rank), mn.numpy())
+        # the merge itself is libld's ld_merge_peak_lists (GPU, test_gpu_parity);
+        # here the gathered lists merge by the same key in plain Python
+        mp, mn = _merge_by_key(torch.stack(allp).numpy(), torch.cat(alln).numpy(),
+                               big.shape[1], 6)
+        np.save(os.path.join(outdir, "tp%d.npy" % rank), mp)
+        np.save(os.path.join(outdir, "tn%d.npy" % rank), np.array([mn], np.int32))
     finally:
         dist.destroy_process_group()
 

@@ -163,3 +163,87 @@ def test_cfg5_decompositions_whole_image(ld, oracle, world, shard):
         got = [(int(a), int(b), int(np.uint32(np.int32(v))))
                for a, b, v in p.cpu().numpy().reshape(-1, 3)[: int(n.reshape(-1)[0])]]
     assert got == wp
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_band_bitmaps_round_trip_cfg5(ld, oracle, world):
+    """The theta-shard exchange: each band's edge list ->
+    ld_edges_to_bitmask; the bitmaps laid out as an all_gather would
+    ([world][stride_rows][words]) -> ld_bitmask_to_edges == the whole image's
+    oracle edge set."""
+    from paper_2212_09460_b200 import dist as pdist
+    cfg = synth.CONFIGS["cfg5"]
+    img = synth.gen_frame("cfg5", 0)
+    W, H = cfg.width, cfg.height
+    want = oracle.compact(oracle.sobel_binarize(img, cfg.threshold))
+    plans = [pdist.BandPlan.make(W, H, r, world) for r in range(world)]
+    stride_rows = max(p.rows for p in plans)
+    words = ld.ld_edge_bitmask_words(W, stride_rows)
+    allbits = torch.zeros((world * words,), dtype=torch.int32, device="cuda")
+    for r, p in enumerate(plans):
+        det = pdist.BandedDetector(W, H, cfg.n_theta, *synth.q15_table(cfg.n_theta),
+                                   cfg.threshold, cfg.k, cfg.half_theta, cfg.half_rho, 1, r, world)
+        det.load(img)
+        ld.ld_sobel_binarize(det.gray, det.img, cfg.threshold, None, det.edges, det.edge_stride,
+                             det.count)
+        ld.ld_edges_to_bitmask(det.edges, det.count, W, p.row_begin, stride_rows,
+                               allbits[r * words:(r + 1) * words])
+    cap = ld._round_up(W * H, 4)
+    edges = torch.zeros((cap,), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    ld.ld_bitmask_to_edges(allbits, W, [p.row_begin for p in plans], [p.rows for p in plans],
+                           stride_rows, edges, cap, cnt)
+    torch.cuda.synchronize()
+    n = int(cnt.item())
+    got = np.sort(edges[:n].cpu().numpy().view(np.uint32))
+    assert n == len(want) and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("k", [1, 4, 64])
+def test_merge_peak_lists_kernel(ld, k):
+    """ld_merge_peak_lists == the top k by (votes, -theta, -rho) of the union,
+    with ties in votes, short lists and empty lists."""
+    from paper_2212_09460_b200 import dist as pdist
+    rng = np.random.default_rng(k)
+    n_rho, S = 2001, 5
+    lists = np.full((S, k, 3), -1, np.int32)
+    lists[:, :, 2] = 0
+    ns = np.array([k, k // 2, 0, k, 1], np.int32)
+    cells = rng.choice(900 * n_rho, size=S * k, replace=False)
+    i = 0
+    for sidx in range(S):
+        for j in range(ns[sidx]):
+            t, r = divmod(int(cells[i]), n_rho)
+            lists[sidx, j] = (t, r, int(rng.integers(1, 6)))  # many equal votes
+            i += 1
+    out, n = pdist.merge_peak_lists(torch.from_numpy(lists).cuda(), torch.from_numpy(ns).cuda(),
+                                    n_rho, k)
+    torch.cuda.synchronize()
+    keys = sorted(((int(v), -(int(t) * n_rho + int(r)), int(t), int(r))
+                   for sidx in range(S) for (t, r, v) in lists[sidx, :ns[sidx]]), reverse=True)
+    want = [(t, r, v) for v, _, t, r in keys[:k]]
+    got = [tuple(int(x) for x in p) for p in out.cpu().numpy()]
+    assert int(n[0]) == len(want) and got[:len(want)] == want
+    assert all(p == (-1, -1, 0) for p in got[len(want):])
+
+
+def test_bench_two_ranks_gloo_one_command(tmp_path):
+    """`bench.py --gpus 2` launches its own two ranks (here the gloo backend on
+    one GPU: a plumbing check) and prints one line: the BASELINE batch of 256
+    frames split 128 + 128."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--dist-backend", "gloo", "--workload", "cfg3", "--steps", "2",
+                        "--warmup", "1", "--no-e2e", "--no-parity"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 256
+    assert d["config"]["frames_per_gpu"] == 128 and d["scaling"] == "strong"
+    assert d["gpu_launches"] > 0 and d["value"] > 0

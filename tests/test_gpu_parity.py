@@ -131,7 +131,7 @@ def test_sobel_bands_match_whole(ld, oracle):
 # ----------------------------------------------------------------------------
 # Stage 3: voting
 # ----------------------------------------------------------------------------
-def gpu_vote_list(ld, edge_lists, w, h, n_theta):
+def gpu_vote_list(ld, edge_lists, w, h, n_theta, flags=0):
     c, s = synth.q15_table(n_theta)
     b = len(edge_lists)
     stride = ld._round_up(max(max(len(e) for e in edge_lists), 1), 4)
@@ -139,23 +139,21 @@ def gpu_vote_list(ld, edge_lists, w, h, n_theta):
     for i, e in enumerate(edge_lists):
         el[i, :len(e)] = e
     counts = cuda(np.array([len(e) for e in edge_lists], np.int32))
-    acc = ld.hough_accumulate(cuda(el.view(np.int32)), counts, stride, w, h, c, s)
+    acc = ld.hough_accumulate(cuda(el.view(np.int32)), counts, stride, w, h, c, s, flags=flags)
     torch.cuda.synchronize()
     return acc.cpu().numpy().view(np.uint32)
 
 
-# LD_VOTE_PAIRED=0 forces the plain kernel; unset, a symmetric table (every
+# LD_VOTE_PLAIN forces the plain kernel; without it a symmetric table (every
 # synth.q15_table) selects the half-angle paired kernel (NEXT 2)
 VOTE_MODES = ["paired", "plain"]
 
 
 @pytest.fixture(params=VOTE_MODES)
-def vote_mode(request, monkeypatch):
-    if request.param == "plain":
-        monkeypatch.setenv("LD_VOTE_PAIRED", "0")
-    else:
-        monkeypatch.delenv("LD_VOTE_PAIRED", raising=False)
-    return request.param
+def vote_mode(request):
+    """ld_hough_accumulate_opt flags of the mode."""
+    from paper_2212_09460_b200 import ld as _ld
+    return _ld.LD_VOTE_PLAIN if request.param == "plain" else 0
 
 
 @pytest.mark.parametrize("n_theta", [1, 2, 3, 4, 5, 180, 181, 720, 1024, 2048])
@@ -167,7 +165,7 @@ def test_vote_random_lists(ld, oracle, n_theta, vote_mode):
     for n in (0, 1, 5, 4099):
         xs, ys = rng.integers(0, w, n), rng.integers(0, h, n)
         lists.append(((ys.astype(np.uint32) << 16) | xs.astype(np.uint32)))
-    got = gpu_vote_list(ld, lists, w, h, n_theta)
+    got = gpu_vote_list(ld, lists, w, h, n_theta, vote_mode)
     for i, e in enumerate(lists):
         assert np.array_equal(got[i], oracle.hough_accumulate(e, w, h, c, s)), (n_theta, len(e))
 
@@ -177,7 +175,7 @@ def test_vote_extreme_corners_and_tiny(ld, oracle, vote_mode):
         c, s = synth.q15_table(64)
         corners = sorted({(0, 0), (w - 1, 0), (0, h - 1), (w - 1, h - 1)})
         e = np.array([(y << 16) | x for x, y in corners], np.uint32)
-        got = gpu_vote_list(ld, [e], w, h, 64)
+        got = gpu_vote_list(ld, [e], w, h, 64, vote_mode)
         assert np.array_equal(got[0], oracle.hough_accumulate(e, w, h, c, s)), (w, h)
 
 
@@ -185,7 +183,7 @@ def test_vote_collinear_hotspot(ld, oracle, vote_mode):
     # thousands of votes into the same bin (same-address atomics)
     c, s = synth.q15_table(180)
     e = np.array([(100 << 16) | x for x in range(1000)] * 3, np.uint32)
-    got = gpu_vote_list(ld, [e], 1000, 200, 180)
+    got = gpu_vote_list(ld, [e], 1000, 200, 180, vote_mode)
     want = oracle.hough_accumulate(e, 1000, 200, c, s)
     assert np.array_equal(got[0], want) and want.max() == 3000
 
@@ -207,15 +205,18 @@ def test_vote_asymmetric_table_uses_plain_path(ld, oracle):
                           oracle.hough_accumulate(e, w, h, c, s))
 
 
-def test_vote_paired_equals_plain_on_frames(ld, monkeypatch):
+def test_vote_paired_equals_plain_on_frames(ld):
     cfg = synth.CONFIGS["cfg3"]
     c, s = synth.q15_table(cfg.n_theta)
     _, edges, counts, stride = ld.sobel_binarize(cuda(synth.gen_batch("cfg3", 0, 4)), cfg.threshold,
                                                  want_binary=False)
     a1, h1 = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s, want_hint=True)
-    monkeypatch.setenv("LD_VOTE_PAIRED", "0")
-    a0, h0 = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s, want_hint=True)
+    a0, h0 = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s, want_hint=True,
+                                 flags=ld.LD_VOTE_PLAIN)
     assert torch.equal(a0, a1)
+    # both kernels write the same segment maxima (the sparse peak search's input)
+    assert torch.equal(h0[-a0.shape[0] * 180 * ((a0.shape[2] + 31) // 32) * 4:],
+                       h1[-a1.shape[0] * 180 * ((a1.shape[2] + 31) // 32) * 4:])
     p0, n0 = ld.hough_peaks(a0, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=h0)
     p1, n1 = ld.hough_peaks(a1, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=h1)
     assert torch.equal(p0, p1) and torch.equal(n0, n1)
@@ -240,6 +241,9 @@ def gpu_vote_list_raw(ld, c, s):
 # ----------------------------------------------------------------------------
 # Stage 4: peaks
 # ----------------------------------------------------------------------------
+# ld_hough_peaks_opt flags forcing each search kernel
+PEAK_KERNEL_FLAGS = {"auto": 0, "stream": 2, "tile": 4, "band": 8}
+
 def test_peaks_random_small(ld, oracle):
     rng = np.random.default_rng(9)
     for trial in range(40):
@@ -372,18 +376,17 @@ def test_banded_accumulators_sum_to_whole(ld, oracle):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "stream", "tile", "band"])
-def test_peaks_all_kernels_windows(ld, oracle, kernel, monkeypatch):
+def test_peaks_all_kernels_windows(ld, oracle, kernel):
     # the default choice (warp-strip kernel for narrow windows, else the CTA
     # streaming kernel), the forced CTA streaming kernel, the tiled kernel and
     # the generic band kernel all agree with the oracle
-    if kernel != "auto":
-        monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
+    flags = PEAK_KERNEL_FLAGS[kernel]
     rng = np.random.default_rng(31)
     for trial, (ht, hr) in enumerate([(0, 0), (0, 5), (1, 1), (2, 29), (7, 44), (10, 116),
                                       (12, 3), (13, 2), (3, 240), (20, 300)]):
         acc = rng.integers(0, 6, size=(2, 61, 1201)).astype(np.uint32)
         acc[1, 30, 600] = 50      # one dominant peak
-        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, 16)
+        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, 16, flags=flags)
         torch.cuda.synchronize()
         for f in range(2):
             want, wn = oracle.hough_peaks(acc[f], ht, hr, 1, 16)
@@ -444,12 +447,11 @@ def test_banded_detector_more_ranks_than_rows(ld, oracle):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "stream", "band"])
-def test_peaks_ties_and_plateaus(ld, oracle, kernel, monkeypatch):
+def test_peaks_ties_and_plateaus(ld, oracle, kernel):
     # equal maxima inside one window (plateaus, equal values left/right/above/
     # below) exercise the exact (theta, rho) tie-break; small value range makes
     # ties everywhere
-    if kernel != "auto":
-        monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
+    flags = PEAK_KERNEL_FLAGS[kernel]
     rng = np.random.default_rng(77)
     for trial, (ht, hr, k) in enumerate([(2, 29, 4), (1, 3, 64), (0, 0, 1024), (7, 44, 8),
                                          (10, 116, 64), (12, 5, 16), (3, 0, 32), (3, 4, 64),
@@ -458,7 +460,7 @@ def test_peaks_ties_and_plateaus(ld, oracle, kernel, monkeypatch):
         acc[0, 40:43, 700:705] = 9                    # plateau
         acc[1, 10, 100] = acc[1, 10, 103] = acc[1, 12, 101] = 7
         acc[2, :, 1499] = 5                           # column of equal values at the edge
-        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, k)
+        peaks, npk = ld.hough_peaks(cuda(acc.view(np.int32)), ht, hr, 1, k, flags=flags)
         torch.cuda.synchronize()
         for f in range(3):
             want, wn = oracle.hough_peaks(acc[f], ht, hr, 1, k)
@@ -587,9 +589,8 @@ def oracle_slice_peaks(cands, t0, t1, k):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "stream", "band"])
-def test_peaks_ex_theta_slices(ld, oracle, kernel, monkeypatch):
-    if kernel != "auto":
-        monkeypatch.setenv("LD_PEAKS_KERNEL", kernel)
+def test_peaks_ex_theta_slices(ld, oracle, kernel):
+    flags = PEAK_KERNEL_FLAGS[kernel]
     rng = np.random.default_rng(123)
     for trial, (nt, ht, hr, k) in enumerate([(180, 2, 29, 4), (1024, 10, 116, 64),
                                               (97, 3, 5, 16), (60, 0, 0, 8), (33, 7, 44, 8)]):
@@ -602,7 +603,8 @@ def test_peaks_ex_theta_slices(ld, oracle, kernel, monkeypatch):
             # (the ABI requires n_theta >= 1); its candidate range is empty
             sl = np.ascontiguousarray(big[g0:max(g1, g0 + 1)])[None]
             peaks, npk = ld.hough_peaks(cuda(sl.view(np.int32)), ht, hr, 1, k,
-                                        cand_rows=(t0 - g0, t1 - g0), theta_offset=g0)
+                                        cand_rows=(t0 - g0, t1 - g0), theta_offset=g0,
+                                        flags=flags)
             torch.cuda.synchronize()
             want = oracle_slice_peaks(cands, t0, t1, k)
             assert int(npk[0]) == len(want), (kernel, trial, t0, t1)
@@ -662,6 +664,10 @@ def _hint_case(ld, oracle, frames, cfg, kernel=None, monkeypatch=None, check_ora
     torch.cuda.synchronize()
     assert torch.equal(n0, n1) and torch.equal(p0, p1)
     gtau = ws[:4 * b].view(torch.int32).cpu().numpy().view(np.uint32)
+    # the hinted search without the sparse stage (R30) gives the same peaks
+    p2, n2 = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k, hint=hint,
+                            flags=ld.LD_PEAKS_DENSE)
+    assert torch.equal(n0, n2) and torch.equal(p0, p2)
     n1c, p1c = n1.cpu().numpy(), p1.cpu().numpy()
     for f in range(b):
         if n1c[f] == cfg.k:
