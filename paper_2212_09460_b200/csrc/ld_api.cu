@@ -235,11 +235,13 @@ static size_t hint_keys_bytes(int32_t batch, int32_t n_theta) {
   return sizeof(unsigned long long) * static_cast<size_t>(batch) * n_theta * HINT_MAX_RANGES;
 }
 
-static int32_t n_seg_of(int32_t n_rho) { return (n_rho + SEG_CELLS - 1) / SEG_CELLS; }
+static int32_t n_seg_of(int32_t n_theta, int32_t n_rho) {
+  return seg_count(static_cast<int64_t>(n_theta) * n_rho);
+}
 
 static size_t hint_bytes(int32_t batch, int32_t n_theta, int32_t n_rho) {
   return HINT_HDR_BYTES + hint_keys_bytes(batch, n_theta) +
-         sizeof(uint32_t) * static_cast<size_t>(batch) * n_theta * n_seg_of(n_rho);
+         sizeof(uint32_t) * static_cast<size_t>(batch) * n_seg_of(n_theta, n_rho);
 }
 
 static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64_t edge_stride,
@@ -281,7 +283,7 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   p.segmax = hint ? reinterpret_cast<uint32_t *>(static_cast<char *>(hint) + HINT_HDR_BYTES +
                                                  hint_keys_bytes(batch, n_theta))
                   : nullptr;
-  p.n_seg = n_seg_of(n_rho);
+  p.n_seg = n_seg_of(n_theta, n_rho);
   p.n_pairs = paired ? hough_pair_count(n_theta) : 0;
   cudaError_t e = paired ? launch_hough_pairs(p, trig, ctas, smem, stream)
                          : launch_hough(p, trig, ctas, smem, stream);
@@ -314,7 +316,7 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   p.segmax = hint ? reinterpret_cast<const uint32_t *>(static_cast<const char *>(hint) +
                                                        HINT_HDR_BYTES + hint_keys_bytes(batch, n_theta))
                   : nullptr;
-  p.n_seg = n_seg_of(n_rho);
+  p.n_seg = n_seg_of(n_theta, n_rho);
   const PeaksLayout W = peaks_layout(batch, n_theta, n_rho, k);
   char *ws = static_cast<char *>(workspace);
   p.gtau = reinterpret_cast<uint32_t *>(ws + W.gtau);

@@ -26,7 +26,7 @@
 //
 // While a band is in shared memory the kernel also writes, for the peak
 // search (DESIGN R25, R30), (a) per warp the largest count it saw and its
-// cell, and (b) the maximum of every 32-cell segment of every row.
+// cell, and (b) the maximum of every 1 KB chunk of the accumulator.
 #include <cstdlib>
 
 #include "ld_internal.cuh"
@@ -71,49 +71,67 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
-// Running per-warp best of the summaries: the largest segment maximum seen
-// and where (a shared-memory pointer to the segment, its global row and
-// segment index).  Segments are visited in increasing cell order per warp, so
-// the strict '>' keeps the first (lowest-index) segment among equal maxima.
+// Running per-warp best of the summaries: the largest chunk maximum seen and
+// the chunk (its shared-memory words and their global address).  Chunks are
+// visited in increasing address order per warp, so the strict '>' keeps the
+// first (lowest-address) chunk among equal maxima.
 struct SegBest {
   uint32_t v = 0;
-  int row = 0, seg = 0;
-  const uint32_t *ptr = nullptr;
+  const uint32_t *sm = nullptr;  // shared-memory copy of the chunk's first word
+  const uint32_t *gl = nullptr;  // its global address
 };
 
-// Segment maxima of rows [0, nrows) of a shared-memory block (row j at
-// rows + j*n_rho, global row g0 + j): warp `wi` of `nw` takes segments
-// wi, wi+nw, ... of every row; one LDS + REDUX.MAX per segment of 32 cells.
-__device__ __forceinline__ void summarize_rows(const uint32_t *rows, int nrows, int g0, int n_rho,
-                                               int nseg, uint32_t *segmax_frame, int wi, int nw,
-                                               int lane, SegBest &best) {
-  for (int j = 0; j < nrows; ++j) {
-    const uint32_t *row = rows + j * n_rho;
-    uint32_t *out = segmax_frame + static_cast<int64_t>(g0 + j) * nseg;
-    for (int s = wi; s < nseg; s += nw) {
-      const int c = s * 32 + lane;
-      const uint32_t v = c < n_rho ? row[c] : 0u;
-      const uint32_t m = __reduce_max_sync(0xffffffffu, v);
-      if (lane == 0) out[s] = m;
+// Summaries of one block of counters on its way out: dst[0 .. ncell) in
+// global memory, src the shared-memory copy (congruent modulo 16 bytes).  The
+// accumulator is cut into SEG_BYTES-aligned chunks of GLOBAL memory (DESIGN
+// R30); for every chunk that lies wholly inside the block its maximum goes to
+// segmax[chunk - first chunk of the frame], a chunk only partly inside gets
+// 0xFFFFFFFF ("must be examined": its other part belongs to another CTA or
+// frame, and every writer of it writes the same value).  Warp `wi` of `nw`
+// takes chunks wi, wi+nw, ...: two 16-byte shared loads per lane (256 words
+// = 32 lanes x 8), a 3-input max tree and one REDUX.MAX.
+__device__ __forceinline__ void summarize_block(const uint32_t *dst, const uint32_t *src,
+                                                int ncell, uintptr_t frame_chunk0,
+                                                uint32_t *segmax_frame, int wi, int nw, int lane,
+                                                SegBest &best) {
+  if (ncell <= 0) return;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(dst + ncell);
+  const uintptr_t q0 = a0 / SEG_BYTES, q1 = (a1 - 1) / SEG_BYTES;
+  for (uintptr_t q = q0 + wi; q <= q1; q += nw) {
+    const uintptr_t c0 = q * SEG_BYTES;
+    uint32_t m = 0xFFFFFFFFu;
+    if (c0 >= a0 && c0 + SEG_BYTES <= a1) {
+      const uint32_t *sc = src + (c0 - a0) / 4;  // 16-byte aligned (congruent copies)
+      const uint4 u = reinterpret_cast<const uint4 *>(sc)[lane];
+      const uint4 w = reinterpret_cast<const uint4 *>(sc)[32 + lane];
+      const uint32_t v = max(max(max(u.x, u.y), max(u.z, u.w)), max(max(w.x, w.y), max(w.z, w.w)));
+      m = __reduce_max_sync(0xffffffffu, v);
       if (m > best.v) {
         best.v = m;
-        best.row = g0 + j;
-        best.seg = s;
-        best.ptr = row + s * 32;
+        best.sm = sc;
+        best.gl = reinterpret_cast<const uint32_t *>(c0);
       }
     }
+    if (lane == 0) segmax_frame[q - frame_chunk0] = m;
   }
 }
 
-// The warp's hint key (value << 32 | ~cell index) from its best segment: the
-// first lane holding the maximum.  0 when the warp saw only zeros.
-__device__ __forceinline__ unsigned long long seg_best_key(const SegBest &b, int n_rho, int lane) {
+// The warp's hint key (value << 32 | ~cell index) from its best chunk: the
+// first word holding the maximum.  0 when the warp saw only zeros.
+__device__ __forceinline__ unsigned long long seg_best_key(const SegBest &b,
+                                                           const uint32_t *frame, int lane) {
   if (b.v == 0u) return 0ull;
-  const int c = b.seg * 32 + lane;
-  const uint32_t v = c < n_rho ? b.ptr[lane] : 0u;
-  const uint32_t hit = __ballot_sync(0xffffffffu, v == b.v);
-  const uint32_t idx = static_cast<uint32_t>(b.row) * static_cast<uint32_t>(n_rho) +
-                       static_cast<uint32_t>(b.seg * 32 + __ffs(hit) - 1);
+  // lane l's words: 4l .. 4l+3 and 128+4l .. 128+4l+3
+  const uint4 u = reinterpret_cast<const uint4 *>(b.sm)[lane];
+  const uint4 w = reinterpret_cast<const uint4 *>(b.sm)[32 + lane];
+  const int lo = u.x == b.v ? 0 : u.y == b.v ? 1 : u.z == b.v ? 2 : u.w == b.v ? 3 : 99;
+  const int hi = w.x == b.v ? 0 : w.y == b.v ? 1 : w.z == b.v ? 2 : w.w == b.v ? 3 : 99;
+  const uint32_t bl = __ballot_sync(0xffffffffu, lo < 99), bh = __ballot_sync(0xffffffffu, hi < 99);
+  const int src_lane = bl ? __ffs(bl) - 1 : __ffs(bh) - 1;
+  const int sub = __shfl_sync(0xffffffffu, bl ? lo : hi, src_lane);
+  const int word = (bl ? 0 : 128) + 4 * src_lane + sub;
+  const uint32_t idx = static_cast<uint32_t>((b.gl + word) - frame);
   return (static_cast<unsigned long long>(b.v) << 32) | (0xFFFFFFFFu - idx);
 }
 
@@ -126,6 +144,9 @@ __device__ __forceinline__ void write_hint_header(const HoughParams &p, int nwar
   h[4] = static_cast<uint32_t>(p.n_bands);
   h[5] = static_cast<uint32_t>(nwarps);
   h[6] = static_cast<uint32_t>(p.n_seg);
+  const uint64_t a = reinterpret_cast<uintptr_t>(p.acc);  // segmax is tied to this address
+  h[7] = static_cast<uint32_t>(a);
+  h[8] = static_cast<uint32_t>(a >> 32);
 }
 
 // ---------------------------------------------------------------------------
@@ -219,9 +240,10 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   bulk_rows_out(dst, slice, ncell, tid, NT);
   if (p.hint_keys) {
     SegBest best;
-    uint32_t *segmax = p.segmax + static_cast<int64_t>(f) * p.n_theta * p.n_seg;
-    summarize_rows(slice, nr, t0, p.n_rho, p.n_seg, segmax, warp, NWARPS, lane, best);
-    const unsigned long long key = seg_best_key(best, p.n_rho, lane);
+    const uint32_t *frame = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
+    summarize_block(dst, slice, ncell, reinterpret_cast<uintptr_t>(frame) / SEG_BYTES,
+                    p.segmax + static_cast<int64_t>(f) * p.n_seg, warp, NWARPS, lane, best);
+    const unsigned long long key = seg_best_key(best, frame, lane);
     if (lane == 0) p.hint_keys[(static_cast<int64_t>(f) * p.n_bands + band) * NWARPS + warp] = key;
     if (f == 0 && band == 0 && tid == 0) write_hint_header(p, NWARPS);
   }
@@ -385,12 +407,13 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   if (j1 > j0) bulk_rows_out(dst2 + j0 * n_rho, blk2 + j0 * n_rho, (j1 - j0) * n_rho, tid, NT);
   if (p.hint_keys) {
     SegBest best;
-    uint32_t *segmax = p.segmax + static_cast<int64_t>(f) * n_theta * p.n_seg;
-    summarize_rows(blk1, np, p0, n_rho, p.n_seg, segmax, warp, NWARPS, lane, best);
+    const uintptr_t fc0 = reinterpret_cast<uintptr_t>(frame) / SEG_BYTES;
+    uint32_t *segmax = p.segmax + static_cast<int64_t>(f) * p.n_seg;
+    summarize_block(dst1, blk1, ncell, fc0, segmax, warp, NWARPS, lane, best);
     if (j1 > j0)
-      summarize_rows(blk2 + j0 * n_rho, j1 - j0, g2 + j0, n_rho, p.n_seg, segmax, warp, NWARPS,
-                     lane, best);
-    const unsigned long long key = seg_best_key(best, n_rho, lane);
+      summarize_block(dst2 + j0 * n_rho, blk2 + j0 * n_rho, (j1 - j0) * n_rho, fc0, segmax, warp,
+                      NWARPS, lane, best);
+    const unsigned long long key = seg_best_key(best, frame, lane);
     if (lane == 0) p.hint_keys[(static_cast<int64_t>(f) * p.n_bands + band) * NWARPS + warp] = key;
     if (f == 0 && band == 0 && tid == 0) write_hint_header(p, NWARPS);
   }

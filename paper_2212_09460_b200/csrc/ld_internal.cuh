@@ -75,18 +75,25 @@ struct HoughParams {
   uint32_t *acc;
   uint32_t *hint_hdr;            // nullable: peak-hint header (written by CTA (0, 0))
   unsigned long long *hint_keys;  // [batch][n_bands][warps per CTA] per-warp maxima
-  uint32_t *segmax;              // [batch][n_theta][n_seg] 32-cell segment maxima
-  int32_t n_seg;                 // ceil(n_rho / 32)
+  uint32_t *segmax;              // [batch][n_seg] maxima of the accumulator's 1 KB chunks
+  int32_t n_seg;                 // chunks per frame (seg_count)
 };
 
 // Peak-hint buffer layout (ld_hough_accumulate_hint / ld_hough_peaks_hinted):
 // a 64-byte header {magic, batch, n_theta, n_rho, n_bands, keys per band,
-// n_seg, 0...}, the per-warp maximum keys ([batch][n_bands][keys per band],
-// capacity batch * n_theta * HINT_MAX_RANGES), then the segment maxima
-// [batch][n_theta][n_seg] (DESIGN R25, R30).
+// n_seg, acc address lo, hi, 0...}, the per-warp maximum keys
+// ([batch][n_bands][keys per band], capacity batch * n_theta *
+// HINT_MAX_RANGES), then the chunk maxima [batch][n_seg] (DESIGN R25, R30):
+// chunk q of frame f covers the SEG_BYTES-aligned global bytes
+// [(c0 + q) * SEG_BYTES, +SEG_BYTES), c0 = (frame start address) / SEG_BYTES;
+// 0xFFFFFFFF marks a chunk only partly inside the frame or a voting block.
 constexpr uint32_t HINT_MAGIC = 0x3248444Cu;  // "LDH2"
 constexpr int HINT_HDR_BYTES = 64;
-constexpr int SEG_CELLS = 32;  // cells per segment maximum
+constexpr int SEG_BYTES = 1024;  // accumulator bytes per chunk maximum (256 counters)
+// chunks a frame of n_cells counters can touch at any 4-byte-aligned start
+__host__ __device__ constexpr int seg_count(int64_t n_cells) {
+  return static_cast<int>((n_cells * 4 + SEG_BYTES - 1) / SEG_BYTES) + 1;
+}
 constexpr int HINT_MAX_KEYS = 1024;  // per frame, what the verifying kernel sorts (more are merged)
 constexpr int HINT_MAX_RANGES = 32;  // ranges per band (warps of a 1024-thread CTA)
 
@@ -138,7 +145,7 @@ struct PeaksParams {
   int32_t theta_offset;           // added to the row index in keys and reported theta bins
   const uint32_t *hint_hdr;       // nullable: peak hint (unrestricted searches only)
   const unsigned long long *hint_keys;
-  const uint32_t *segmax;         // hint's segment maxima [batch][n_theta][n_seg] (sparse path)
+  const uint32_t *segmax;         // hint's chunk maxima [batch][n_seg] (sparse path)
   int32_t n_seg;
   uint32_t *resolved;             // [batch] 1 = the sparse search wrote this frame's peaks
   uint32_t *ncand;                // [batch] sparse-search candidates found

@@ -217,9 +217,16 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
                      h[3] == static_cast<uint32_t>(p.n_rho) && h[5] >= 1 &&
                      h[5] <= HINT_MAX_RANGES && h[4] >= 1 && h[4] <= static_cast<uint32_t>(p.n_theta) &&
                      h[6] == static_cast<uint32_t>(p.n_seg);
+  // the chunk maxima describe the accumulator at the address voting wrote it
+  // to: a copy elsewhere keeps the (verified) keys but not the sparse search
+  const uint64_t acc_addr = reinterpret_cast<uintptr_t>(p.acc);
+  const bool same_acc = h[7] == static_cast<uint32_t>(acc_addr) &&
+                        h[8] == static_cast<uint32_t>(acc_addr >> 32);
   const int n_src = match ? static_cast<int>(h[4] * h[5]) : 0;
   if (tid == 0 && p.ncand) {
-    p.ncand[f] = 0u;
+    // ncand = SP_CAP + 1 (an "overflow") keeps the sparse search off this
+    // frame when the chunk maxima do not belong to this accumulator
+    p.ncand[f] = (match && same_acc) ? 0u : static_cast<uint32_t>(SP_CAP + 1);
     p.resolved[f] = 0u;
   }
   if (n_src <= 0) {
@@ -321,10 +328,11 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
 // ---------------------------------------------------------------------------
 // Sparse search (DESIGN R30): with a certified bound tau_f = gtau[f] > 0 (the
 // k-th verified hint key, R25) every top-k candidate has votes >= tau_f, and
-// every cell >= tau_f lies in a 32-cell segment whose maximum (recorded by the
-// voting kernel while the band was in shared memory) is >= tau_f.  So the
-// search reads the segment maxima (1/32 of the accumulator), tests only the
-// cells >= tau_f of those segments against the full candidate definition
+// every cell >= tau_f lies in a 1 KB chunk of the accumulator whose maximum
+// (recorded by the voting kernel while the band was in shared memory; a chunk
+// split between two voting blocks is marked 0xFFFFFFFF) is >= tau_f.  So the
+// search reads the chunk maxima (1/256 of the accumulator), tests only the
+// cells >= tau_f of those chunks against the full candidate definition
 // (one warp per cell, exact window test as in the band kernel), and keeps the
 // keys of the candidates found.  peaks_sparse_finish_kernel then takes their
 // top k.  A frame whose bound is not certified, or whose candidate list
@@ -334,7 +342,7 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
 constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
 constexpr int SP_QUEUE = 1024;  // hot segments gathered per pass of a CTA
-constexpr int SP_CHUNK = 8192;  // segment maxima scanned per CTA
+constexpr int SP_CHUNK = 2048;  // chunk maxima scanned per CTA
 
 // Exact candidate test of cell (t, r) with value v by one warp: every count in
 // the clipped window is <= v and an equal count sits at a higher cell index.
@@ -380,38 +388,47 @@ __global__ void __launch_bounds__(SP_THREADS) peaks_sparse_kernel(const PeaksPar
   __shared__ int s_nq;
   const int f = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t g = p.gtau[f];
-  if (g == 0u) return;  // no certified bound: the dense search handles this frame
+  // no certified bound, or chunk maxima of another accumulator (ncand set
+  // past SP_CAP by the hint kernel): the dense search handles this frame
+  if (g == 0u || p.ncand[f] > static_cast<uint32_t>(SP_CAP)) return;
   const uint32_t tau = g > p.floor_votes ? g : p.floor_votes;
-  const int nseg = p.n_seg, n_rho = p.n_rho, n_theta = p.n_theta;
-  const int total = n_theta * nseg;
-  const uint32_t *S = p.segmax + static_cast<int64_t>(f) * total;
-  const uint32_t *A = p.acc + static_cast<int64_t>(f) * n_theta * n_rho;
-  const int c0 = blockIdx.x * SP_CHUNK, c1 = min(total, c0 + SP_CHUNK);
-  for (int base = c0; base < c1; base += SP_QUEUE) {
+  const int n_rho = p.n_rho, n_theta = p.n_theta;
+  const int64_t ncells = static_cast<int64_t>(n_theta) * n_rho;
+  const uint32_t *S = p.segmax + static_cast<int64_t>(f) * p.n_seg;
+  const uint32_t *A = p.acc + static_cast<int64_t>(f) * ncells;
+  const uintptr_t c0 = reinterpret_cast<uintptr_t>(A) / SEG_BYTES;
+  const int q_begin = blockIdx.x * SP_CHUNK, q_end = min(p.n_seg, q_begin + SP_CHUNK);
+  for (int base = q_begin; base < q_end; base += SP_QUEUE) {
     if (tid == 0) s_nq = 0;
     __syncthreads();
-    const int end = min(c1, base + SP_QUEUE);
+    const int end = min(q_end, base + SP_QUEUE);
     for (int i = base + tid; i < end; i += SP_THREADS)
       if (S[i] >= tau) s_q[atomicAdd(&s_nq, 1)] = i;
     __syncthreads();
     const int nq = s_nq;
     for (int q = warp; q < nq; q += SP_WARPS) {
-      const int u = s_q[q];
-      const int t = u / nseg, s = u - t * nseg;
-      const int r = s * 32 + lane;
-      const uint32_t v = r < n_rho ? __ldg(A + static_cast<int64_t>(t) * n_rho + r) : 0u;
-      uint32_t m = __ballot_sync(0xffffffffu, r < n_rho && v >= tau);
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t cv = __shfl_sync(0xffffffffu, v, b);
-        if (warp_is_candidate(A, n_theta, n_rho, t, s * 32 + b, cv, p.half_theta, p.half_rho,
-                              lane) &&
-            lane == 0) {
-          const uint32_t slot = atomicAdd(p.ncand + f, 1u);
-          if (slot < static_cast<uint32_t>(SP_CAP))
-            p.cand[static_cast<int64_t>(f) * SP_CAP + slot] =
-                mk_key(cv, static_cast<uint32_t>(t * n_rho + s * 32 + b));
+      // the chunk's 256 words, 32 consecutive per step; words outside the
+      // frame are not read
+      const int64_t w0 = static_cast<int64_t>((c0 + s_q[q]) * SEG_BYTES -
+                                              reinterpret_cast<uintptr_t>(A)) / 4;
+      for (int step = 0; step < SEG_BYTES / 128; ++step) {
+        const int64_t c = w0 + step * 32 + lane;
+        const bool in = c >= 0 && c < ncells;
+        const uint32_t v = in ? __ldg(A + c) : 0u;
+        uint32_t m = __ballot_sync(0xffffffffu, in && v >= tau);
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t cv = __shfl_sync(0xffffffffu, v, b);
+          const int64_t cell = w0 + step * 32 + b;
+          const int t = static_cast<int>(cell / n_rho), r = static_cast<int>(cell - static_cast<int64_t>(t) * n_rho);
+          if (warp_is_candidate(A, n_theta, n_rho, t, r, cv, p.half_theta, p.half_rho, lane) &&
+              lane == 0) {
+            const uint32_t slot = atomicAdd(p.ncand + f, 1u);
+            if (slot < static_cast<uint32_t>(SP_CAP))
+              p.cand[static_cast<int64_t>(f) * SP_CAP + slot] =
+                  mk_key(cv, static_cast<uint32_t>(cell));
+          }
         }
       }
     }
@@ -1464,8 +1481,7 @@ static cudaError_t init_gtau(PeaksParams &p, bool restricted, cudaStream_t strea
 // The sparse search (R30) over the frames whose bound the hint certified;
 // the dense kernels launched after it skip the frames it resolved.
 static cudaError_t launch_sparse(const PeaksParams &p, cudaStream_t stream) {
-  const int64_t total = static_cast<int64_t>(p.n_theta) * p.n_seg;
-  dim3 g1(static_cast<unsigned>((total + SP_CHUNK - 1) / SP_CHUNK), p.batch);
+  dim3 g1(static_cast<unsigned>((p.n_seg + SP_CHUNK - 1) / SP_CHUNK), p.batch);
   peaks_sparse_kernel<<<g1, SP_THREADS, 0, stream>>>(p);
   note_launch();
   cudaError_t e = cudaGetLastError();
@@ -1506,14 +1522,15 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
   if (dense_cheap || dense_stream) {
     // the hint (and with it the sparse search) serves the warp and streaming kernels
     PeaksParams ps = p;
-    ps.ncand = (ps.hint_hdr && ps.segmax && !dense_only) ? p_in.ncand : nullptr;
+    const bool sparse_ok = ps.hint_hdr && ps.segmax && !dense_only;
+    ps.ncand = sparse_ok ? p_in.ncand : nullptr;
+    ps.resolved = sparse_ok ? p_in.resolved : nullptr;  // the hint kernel clears both
     bool hinted = false;
     cudaError_t em = init_gtau(ps, restricted, stream, &hinted);
     if (em != cudaSuccess) return em;
     p.hint_hdr = ps.hint_hdr;
     p.hint_keys = ps.hint_keys;
     if (hinted && ps.ncand) {
-      ps.resolved = p_in.resolved;
       em = launch_sparse(ps, stream);
       if (em != cudaSuccess) return em;
       p.resolved = p_in.resolved;

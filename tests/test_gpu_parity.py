@@ -214,12 +214,39 @@ def test_vote_paired_equals_plain_on_frames(ld):
     a0, h0 = ld.hough_accumulate(edges, counts, stride, 1280, 720, c, s, want_hint=True,
                                  flags=ld.LD_VOTE_PLAIN)
     assert torch.equal(a0, a1)
-    # both kernels write the same segment maxima (the sparse peak search's input)
-    assert torch.equal(h0[-a0.shape[0] * 180 * ((a0.shape[2] + 31) // 32) * 4:],
-                       h1[-a1.shape[0] * 180 * ((a1.shape[2] + 31) // 32) * 4:])
+    # both kernels' chunk maxima (the sparse peak search's input, R30) are
+    # exact or the "examine" marker
+    check_chunk_maxima(a0, h0)
+    check_chunk_maxima(a1, h1)
     p0, n0 = ld.hough_peaks(a0, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=h0)
     p1, n1 = ld.hough_peaks(a1, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=h1)
     assert torch.equal(p0, p1) and torch.equal(n0, n1)
+
+
+def check_chunk_maxima(acc, hint):
+    """The hint's chunk maxima (DESIGN R30): chunk q of frame f covers the
+    1 KB-aligned bytes [(c0 + q) * 1024, +1024) of the accumulator, c0 = frame
+    start // 1024; its entry is the maximum of the frame's counters in it, or
+    0xFFFFFFFF (a chunk split between voting blocks).  Every chunk holding a
+    cell is covered."""
+    b, nt, nr = acc.shape
+    ncells = nt * nr
+    n_seg = (ncells * 4 + 1023) // 1024 + 1
+    seg = hint[-b * n_seg * 4:].view(torch.int32).cpu().numpy().view(np.uint32).reshape(b, n_seg)
+    A = acc.cpu().numpy().view(np.uint32).reshape(b, ncells)
+    base = acc.data_ptr()
+    for f in range(b):
+        start = base + f * ncells * 4
+        c0 = start // 1024
+        first = (start - c0 * 1024) // 4  # counters of chunk 0 before the frame
+        padded = np.zeros(n_seg * 256, np.uint32)
+        padded[first:first + ncells] = A[f]
+        true = padded.reshape(n_seg, 256).max(axis=1)
+        used = (start + ncells * 4 - 1) // 1024 - c0 + 1
+        s_ = seg[f, :used]
+        ok = (s_ == true[:used]) | (s_ == 0xFFFFFFFF)
+        assert ok.all(), (f, np.flatnonzero(~ok)[:5])
+        assert (s_ == 0xFFFFFFFF).mean() < 0.2
 
 
 def test_vote_range_error(ld):
@@ -653,7 +680,13 @@ def _hint_case(ld, oracle, frames, cfg, kernel=None, monkeypatch=None, check_ora
     acc0 = ld.hough_accumulate(edges, counts, stride, w, h, c, s)
     acc, hint = ld.hough_accumulate(edges, counts, stride, w, h, c, s, want_hint=True)
     assert torch.equal(acc0, acc)
+    check_chunk_maxima(acc, hint)
     p0, n0 = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+    # a copy of the accumulator at another address: the chunk maxima do not
+    # describe it, so the search falls back to dense -- same peaks
+    pc, nc = ld.hough_peaks(acc.clone(), cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k,
+                            hint=hint)
+    assert torch.equal(p0, pc) and torch.equal(n0, nc)
     _, nt, nr = acc.shape
     wsb = ld.ld_hough_peaks_workspace_bytes(b, nt, nr, cfg.k)
     ws = torch.zeros((wsb,), dtype=torch.uint8, device="cuda")
