@@ -2,6 +2,7 @@
 """Summarise an ncu report (``--set full``) and a launch list into markdown.
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep [gpurun_out/launches.csv] > profiles/x.md
+    python tools/ncu_summary.py --traffic WORKLOAD gpurun_out/prof.ncu-rep   # -> profiles/ncu_traffic.json
 
 Reads the report with ``ncu -i ... --page raw --csv`` (no GPU needed) and
 prints, per profiled kernel, the counters the roofline of DESIGN.md section 7
@@ -48,7 +49,34 @@ def raw(report: str):
     return hdr, units, rows[2:]
 
 
+def traffic(workload: str, report: str, out="profiles/ncu_traffic.json"):
+    """DRAM bytes (read + write) per launch of each kernel of the capture,
+    merged into profiles/ncu_traffic.json under `workload` (bench.py reports it
+    as roofline.traffic)."""
+    import json
+    import os
+    hdr, units, rows = raw(report)
+    ki = hdr.index("Kernel Name")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rec = {}
+    for r in rows:
+        tot = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(key)
+            tot += float(r[i].replace(",", "")) * scale.get(units[i], 1)
+        name = r[ki].split("(")[0].replace("void ", "").replace("ld::", "")
+        rec.setdefault(name, []).append(tot)
+    data = json.load(open(out)) if os.path.exists(out) else {}
+    data[workload] = {k: sum(v) / len(v) for k, v in rec.items()}
+    data.setdefault("_source", {})[workload] = report
+    json.dump(data, open(out, "w"), indent=1, sort_keys=True)
+    print(json.dumps(data[workload], indent=1))
+
+
 def main():
+    if sys.argv[1] == "--traffic":
+        traffic(sys.argv[2], sys.argv[3])
+        return
     report = sys.argv[1]
     hdr, units, rows = raw(report)
     print("## ncu --set full: %s\n" % report)

@@ -1,24 +1,36 @@
 #!/usr/bin/env bash
 # Standard measurement of one round, run on the GPU box from the repo root:
-#   /usr/local/graft/bin/gpurun --timeout 2700 -- 'bash tools/profile_round.sh rNN'
+#   /usr/local/graft/bin/gpurun --timeout 2700 -- 'bash tools/profile_round.sh r02x'
 # Writes gpurun_out/<tag>_*: smoke, GPU tests, default bench line, reference
-# arm, cfg4/cfg5 lines, a full ncu capture of one serialised cfg3 step (the
-# five kernels) and its launch list.  Summarise afterwards (no GPU needed):
+# arm, cfg4/cfg5 lines, a full ncu capture of one serialised step per config
+# (cfg3, cfg4) and the cfg3 launch list, and an ncu capture of the B5 kernel.
+# Summarise afterwards (no GPU needed):
 #   python tools/ncu_summary.py gpurun_out/<tag>_prof.ncu-rep gpurun_out/<tag>_launches.csv
+#   python tools/ncu_summary.py --traffic cfg3 gpurun_out/<tag>_prof.ncu-rep
 set -u
 tag=${1:-run}
+skip_tests=${2:-}
 out=gpurun_out
 mkdir -p $out
+nproc > $out/${tag}_host.txt
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $out/${tag}_smoke.log 2>&1; echo smoke=$?
-timeout 900 python -m pytest tests -m gpu -q > $out/${tag}_pytest_gpu.log 2>&1; echo pytest=$?
-timeout 600 python bench.py > $out/${tag}_bench.jsonl 2>&1; echo bench=$?
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $out/${tag}_reference.jsonl 2>&1; echo ref=$?
-for w in cfg4 cfg5; do
-  timeout 300 python bench.py --workload $w --steps 10 --warmup 3 > $out/${tag}_bench_$w.jsonl 2>&1; echo $w=$?
+if [ -z "$skip_tests" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q > $out/${tag}_pytest_gpu.log 2>&1; echo pytest=$?
+fi
+timeout 900 python bench.py > $out/${tag}_bench.jsonl 2> $out/${tag}_bench.err; echo bench=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/${tag}_reference.jsonl 2>&1; echo ref=$?
+timeout 600 python bench.py --workload cfg4 --steps 10 --warmup 3 > $out/${tag}_bench_cfg4.jsonl 2> $out/${tag}_bench_cfg4.err; echo cfg4=$?
+for sh in band theta; do
+  timeout 300 python bench.py --workload cfg5 --shard $sh --steps 10 --warmup 3 > $out/${tag}_bench_cfg5_$sh.jsonl 2> $out/${tag}_bench_cfg5_$sh.err; echo cfg5_$sh=$?
 done
+timeout 300 python bench.py --workload cfg2 --steps 20 --warmup 5 --no-e2e > $out/${tag}_bench_cfg2.jsonl 2> $out/${tag}_bench_cfg2.err; echo cfg2=$?
 # ncu only after the same command exited 0 above (bench.py --profile: one stream, no extras)
-timeout 300 python bench.py --profile --steps 2 --warmup 3 > /dev/null 2>&1 && \
-timeout 900 ncu --set full --import-source on --clock-control none -s 15 -c 5 \
-    -o $out/${tag}_prof -f python bench.py --profile --steps 2 --warmup 3 > $out/${tag}_ncu.log 2>&1; echo ncu=$?
+for w in cfg3 cfg4; do
+  timeout 300 python bench.py --workload $w --profile --steps 1 --warmup 3 > /dev/null 2>&1 && \
+  timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:ld:: -s 28 -c 10 \
+      -o $out/${tag}_prof_$w -f python bench.py --workload $w --profile --steps 1 --warmup 3 > $out/${tag}_ncu_$w.log 2>&1; echo ncu_$w=$?
+done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $out/${tag}_launches.csv python bench.py --profile --steps 2 --warmup 3 > /dev/null 2>&1; echo launches=$?
+timeout 300 ncu --set full --clock-control none -k regex:smem_atomic -o $out/${tag}_b5 -f \
+    python tools/b5_probe.py > $out/${tag}_b5.log 2>&1; echo b5=$?
