@@ -285,6 +285,11 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
                   : nullptr;
   p.n_seg = n_seg_of(n_theta, n_rho);
   p.n_pairs = paired ? hough_pair_count(n_theta) : 0;
+  if (p.segmax) {  // shared chunks are combined with atomicMax (ld_hough.cu summarize_block)
+    cudaError_t e = cudaMemsetAsync(p.segmax, 0, sizeof(uint32_t) * static_cast<size_t>(batch) * p.n_seg,
+                                    stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(segmax)");
+  }
   cudaError_t e = paired ? launch_hough_pairs(p, trig, ctas, smem, stream)
                          : launch_hough(p, trig, ctas, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");

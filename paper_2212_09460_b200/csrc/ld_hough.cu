@@ -84,12 +84,13 @@ struct SegBest {
 // Summaries of one block of counters on its way out: dst[0 .. ncell) in
 // global memory, src the shared-memory copy (congruent modulo 16 bytes).  The
 // accumulator is cut into SEG_BYTES-aligned chunks of GLOBAL memory (DESIGN
-// R30); for every chunk that lies wholly inside the block its maximum goes to
-// segmax[chunk - first chunk of the frame], a chunk only partly inside gets
-// 0xFFFFFFFF ("must be examined": its other part belongs to another CTA or
-// frame, and every writer of it writes the same value).  Warp `wi` of `nw`
-// takes chunks wi, wi+nw, ...: two 16-byte shared loads per lane (256 words
-// = 32 lanes x 8), a 3-input max tree and one REDUX.MAX.
+// R30); the maximum of the block's counters in each chunk goes to
+// segmax[chunk - first chunk of the frame]: a plain store for a chunk wholly
+// inside the block, an atomicMax for a chunk the block shares with a
+// neighbouring block or frame (at most two per block; the host zeroes segmax
+// before the launch).  Warp `wi` of `nw` takes chunks wi, wi+nw, ...: two
+// 16-byte shared loads per lane (256 words = 32 lanes x 8), a max tree and
+// one REDUX.MAX.
 __device__ __forceinline__ void summarize_block(const uint32_t *dst, const uint32_t *src,
                                                 int ncell, uintptr_t frame_chunk0,
                                                 uint32_t *segmax_frame, int wi, int nw, int lane,
@@ -100,20 +101,27 @@ __device__ __forceinline__ void summarize_block(const uint32_t *dst, const uint3
   const uintptr_t q0 = a0 / SEG_BYTES, q1 = (a1 - 1) / SEG_BYTES;
   for (uintptr_t q = q0 + wi; q <= q1; q += nw) {
     const uintptr_t c0 = q * SEG_BYTES;
-    uint32_t m = 0xFFFFFFFFu;
     if (c0 >= a0 && c0 + SEG_BYTES <= a1) {
       const uint32_t *sc = src + (c0 - a0) / 4;  // 16-byte aligned (congruent copies)
       const uint4 u = reinterpret_cast<const uint4 *>(sc)[lane];
       const uint4 w = reinterpret_cast<const uint4 *>(sc)[32 + lane];
       const uint32_t v = max(max(max(u.x, u.y), max(u.z, u.w)), max(max(w.x, w.y), max(w.z, w.w)));
-      m = __reduce_max_sync(0xffffffffu, v);
+      const uint32_t m = __reduce_max_sync(0xffffffffu, v);
       if (m > best.v) {
         best.v = m;
         best.sm = sc;
         best.gl = reinterpret_cast<const uint32_t *>(c0);
       }
+      if (lane == 0) segmax_frame[q - frame_chunk0] = m;
+    } else {  // the block's part of a shared chunk, word by word
+      uint32_t v = 0u;
+      for (int i = lane; i < SEG_BYTES / 4; i += 32) {
+        const uintptr_t a = c0 + 4u * i;
+        if (a >= a0 && a < a1) v = max(v, src[(a - a0) / 4]);
+      }
+      const uint32_t m = __reduce_max_sync(0xffffffffu, v);
+      if (lane == 0 && m) atomicMax(segmax_frame + (q - frame_chunk0), m);
     }
-    if (lane == 0) segmax_frame[q - frame_chunk0] = m;
   }
 }
 

@@ -86,7 +86,7 @@ struct HoughParams {
 // HINT_MAX_RANGES), then the chunk maxima [batch][n_seg] (DESIGN R25, R30):
 // chunk q of frame f covers the SEG_BYTES-aligned global bytes
 // [(c0 + q) * SEG_BYTES, +SEG_BYTES), c0 = (frame start address) / SEG_BYTES;
-// 0xFFFFFFFF marks a chunk only partly inside the frame or a voting block.
+// the entry is the maximum of the frame's counters in the chunk (0 if none).
 constexpr uint32_t HINT_MAGIC = 0x3248444Cu;  // "LDH2"
 constexpr int HINT_HDR_BYTES = 64;
 constexpr int SEG_BYTES = 1024;  // accumulator bytes per chunk maximum (256 counters)

@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
 // k-th verified hint key, R25) every top-k candidate has votes >= tau_f, and
 // every cell >= tau_f lies in a 1 KB chunk of the accumulator whose maximum
 // (recorded by the voting kernel while the band was in shared memory; a chunk
-// split between two voting blocks is marked 0xFFFFFFFF) is >= tau_f.  So the
+// shared by two voting blocks combines their parts) is >= tau_f.  So the
 // search reads the chunk maxima (1/256 of the accumulator), tests only the
 // cells >= tau_f of those chunks against the full candidate definition
 // (one warp per cell, exact window test as in the band kernel), and keeps the
@@ -341,8 +341,8 @@ __global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParam
 // ---------------------------------------------------------------------------
 constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
-constexpr int SP_QUEUE = 1024;  // hot segments gathered per pass of a CTA
-constexpr int SP_CHUNK = 2048;  // chunk maxima scanned per CTA
+constexpr int SP_QUEUE = 256;   // hot chunks gathered per pass of a CTA
+constexpr int SP_CHUNK = 256;   // chunk maxima scanned per CTA
 
 // Exact candidate test of cell (t, r) with value v by one warp: every count in
 // the clipped window is <= v and an equal count sits at a higher cell index.
@@ -355,15 +355,17 @@ __device__ __forceinline__ bool warp_is_candidate(const uint32_t *A, int n_theta
   const int ra = max(r - hr, 0), rb = min(r + hr, n_rho - 1);
   bool bad = false;
   {
-    const int dr = lane - 15;  // lanes 0..30: columns r-15 .. r+15
-    if (lane < 31 && r + dr >= ra && r + dr <= rb) {
-      for (int tt = max(t - 1, ta); tt <= min(t + 1, tb); ++tt) {
-        const uint32_t ci = static_cast<uint32_t>(tt) * static_cast<uint32_t>(n_rho) +
-                            static_cast<uint32_t>(r + dr);
-        const uint32_t w = __ldg(A + ci);
-        bad = bad || w > v || (w == v && ci < idx);
-      }
+    const int dr = lane - 15;  // lanes 0..30: columns r-15 .. r+15, rows t-1 .. t+1
+    const bool col = lane < 31 && r + dr >= ra && r + dr <= rb;
+    uint32_t w[3], ci[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int tt = t - 1 + d;
+      ci[d] = static_cast<uint32_t>(tt) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(r + dr);
+      w[d] = (col && tt >= ta && tt <= tb) ? __ldg(A + ci[d]) : 0u;
     }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) bad = bad || w[d] > v || (w[d] == v && ci[d] < idx);
   }
   if (__any_sync(0xffffffffu, bad)) return false;
   const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
@@ -407,15 +409,21 @@ __global__ void __launch_bounds__(SP_THREADS) peaks_sparse_kernel(const PeaksPar
     __syncthreads();
     const int nq = s_nq;
     for (int q = warp; q < nq; q += SP_WARPS) {
-      // the chunk's 256 words, 32 consecutive per step; words outside the
-      // frame are not read
+      // the chunk's 256 words, 32 consecutive per step, all 8 loads in
+      // flight at once; words outside the frame are not read
       const int64_t w0 = static_cast<int64_t>((c0 + s_q[q]) * SEG_BYTES -
                                               reinterpret_cast<uintptr_t>(A)) / 4;
-      for (int step = 0; step < SEG_BYTES / 128; ++step) {
+      constexpr int STEPS = SEG_BYTES / 128;
+      uint32_t vv[STEPS];
+#pragma unroll
+      for (int step = 0; step < STEPS; ++step) {
         const int64_t c = w0 + step * 32 + lane;
-        const bool in = c >= 0 && c < ncells;
-        const uint32_t v = in ? __ldg(A + c) : 0u;
-        uint32_t m = __ballot_sync(0xffffffffu, in && v >= tau);
+        vv[step] = (c >= 0 && c < ncells) ? __ldg(A + c) : 0u;
+      }
+#pragma unroll
+      for (int step = 0; step < STEPS; ++step) {
+        const uint32_t v = vv[step];
+        uint32_t m = __ballot_sync(0xffffffffu, v >= tau);
         while (m) {
           const int b = __ffs(m) - 1;
           m &= m - 1;
@@ -1467,7 +1475,7 @@ static AttrOnce g_warp_attr[4];
 // which the warp kernel reads).
 static cudaError_t init_gtau(PeaksParams &p, bool restricted, cudaStream_t stream, bool *hinted) {
   const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
-  *hinted = p.hint_hdr && !restricted && wcells * p.k <= 65536;
+  *hinted = p.hint_hdr && !restricted && wcells * p.k <= (1 << 20);
   if (*hinted) {
     peaks_hint_kernel<<<p.batch, PH_THREADS, 0, stream>>>(p);
     note_launch();
