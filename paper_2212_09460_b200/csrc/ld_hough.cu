@@ -36,6 +36,12 @@ namespace ld {
 #ifndef LD_HV_UNROLL
 #define LD_HV_UNROLL 4  // band rows per unrolled step (plain kernel)
 #endif
+#ifndef LD_HV_ADDR_MODE
+#define LD_HV_ADDR_MODE 0
+#endif
+#ifndef LD_HV_PAIR_UNROLL
+#define LD_HV_PAIR_UNROLL 2  // pairs per unrolled step (paired kernel)
+#endif
 
 // ---------------------------------------------------------------------------
 // Shared pieces
@@ -61,14 +67,6 @@ __device__ __forceinline__ void bulk_rows_out(uint32_t *dst, const uint32_t *src
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
-}
-
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // Running per-warp best of the summaries: the largest chunk maximum seen and
@@ -321,28 +319,44 @@ int hough_pair_count(int n_theta) { return n_theta / 2 + 1; }
 template <int EPL, bool FULL>
 __device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t blk, uint32_t end,
                                                  int lane, int np, const uint4 *rowk,
-                                                 uint32_t delta0, uint32_t row_bytes2,
+                                                 uint32_t row_bytes, uint32_t delta0,
                                                  uint32_t scratch) {
+  // one 32-bit load per entry: the kernel is bound by the L1 data pipe
+  // (shared-memory atomics + these loads, one wavefront per clock per SM),
+  // so the unpacking ALU instructions are cheaper than a second 16-bit load
+  const uint32_t *pe = el + blk + lane;
   uint32_t xs[EPL], ys[EPL];
   bool ok[EPL];
 #pragma unroll
   for (int j = 0; j < EPL; ++j) {
-    const uint32_t e = blk + 32u * j + lane;
-    ok[j] = FULL || e < end;
-    const uint32_t q = ok[j] ? __ldg(el + e) : 0u;
+    ok[j] = FULL || blk + 32u * j + lane < end;
+    const uint32_t q = ok[j] ? __ldg(pe + 32 * j) : 0u;
     xs[j] = q & 0xFFFFu;
     ys[j] = q >> 16;
   }
-#pragma unroll 2
+  constexpr int PAIR_UNROLL = LD_HV_PAIR_UNROLL;
+#pragma unroll PAIR_UNROLL
   for (int r = 0; r < np; ++r) {
-    const uint4 k = rowk[r];  // C, S, K, -2C
-    const uint32_t delta = delta0 - static_cast<uint32_t>(r) * row_bytes2;  // uniform
+    const uint4 k = rowk[r];  // C, S, K, -2C (one broadcast shared load per pair)
+    const uint32_t delta = delta0 - static_cast<uint32_t>(r) * 2u * row_bytes;  // uniform
 #pragma unroll
     for (int j = 0; j < EPL; ++j) {
       const uint32_t v1 = xs[j] * k.x + (ys[j] * k.y + k.z);
       const uint32_t v2 = xs[j] * k.w + v1;
+      // address = ((v >> 13) & ~3) (+ delta) = 4 * hi32(v * 2^17) (+ delta):
+      // shift + mask on the ALU pipe, or IMAD.HI + LEA, moving half the work
+      // to the FMA pipe (LD_HV_ADDR_MODE: 0 both shift/mask, 1 partner via
+      // IMAD.HI, 2 both via IMAD.HI)
+#if LD_HV_ADDR_MODE >= 2
+      red_shared_add(FULL || ok[j] ? __umulhi(v1, 1u << 17) * 4u : scratch, 1u);
+#else
       red_shared_add(FULL || ok[j] ? (v1 >> 13) & ~3u : scratch, 1u);
+#endif
+#if LD_HV_ADDR_MODE >= 1
+      red_shared_add(FULL || ok[j] ? __umulhi(v2, 1u << 17) * 4u + delta : scratch, 1u);
+#else
       red_shared_add((FULL || ok[j] ? (v2 >> 13) & ~3u : scratch - delta) + delta, 1u);
+#endif
     }
   }
 }
@@ -393,16 +407,15 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
 
   const uint32_t n_edges = p.counts[f];
   const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
-  const uint32_t rb2 = 2u * row_bytes;
   uint32_t base = 0;
   for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
-    vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, delta0, rb2,
-                               scratch);
+    vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, row_bytes,
+                               delta0, scratch);
   uint32_t blk = base + static_cast<uint32_t>(warp) * (32u * 8u);
   for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
-    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, delta0, rb2, scratch);
+    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, row_bytes, delta0, scratch);
   if (blk < n_edges)
-    vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, delta0, rb2, scratch);
+    vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, row_bytes, delta0, scratch);
   fence_proxy_async_smem();
   __syncthreads();
 
