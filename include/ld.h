@@ -162,12 +162,20 @@ int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
                             const double *sin_f64, uint32_t *acc, void *stream);
 
 /* ld_hough_accumulate / ld_hough_accumulate_hint (below) with options:
- *  flags : 0, or LD_VOTE_PLAIN -- use the unpaired voting kernel even for a
- *          symmetric table (the half-angle pairing of Eq. 4-5 is otherwise
- *          chosen automatically; both give identical accumulators).  Any other
- *          bit: LD_ERR_INVALID_ARG.
+ *  flags : 0 or any of
+ *          LD_VOTE_PLAIN      -- the unpaired voting kernel even for a
+ *                                symmetric table (the half-angle pairing of
+ *                                Eq. 4-5 is otherwise chosen automatically);
+ *          LD_VOTE_NO_CLUSTER -- no thread-block clusters (for launches too
+ *                                small to fill the GPU, e.g. one frame, the
+ *                                edges of a band are otherwise split over a
+ *                                cluster of CTAs whose shared-memory copies
+ *                                are summed over distributed shared memory).
+ *          Every choice gives the identical accumulator.  Any other bit:
+ *          LD_ERR_INVALID_ARG.
  *  hint  : nullable; as ld_hough_accumulate_hint when given. */
 #define LD_VOTE_PLAIN 1u
+#define LD_VOTE_NO_CLUSTER 2u
 int ld_hough_accumulate_opt(const uint32_t *edge_xy, const uint32_t *edge_count,
                             int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
                             int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,

@@ -290,7 +290,9 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
                                     stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(segmax)");
   }
-  cudaError_t e = paired ? launch_hough_pairs(p, trig, ctas, smem, stream)
+  const int cluster = paired && !(flags & LD_VOTE_NO_CLUSTER)
+                          ? hough_cluster_size(batch, n_bands, ctas, dev.sm_count) : 1;
+  cudaError_t e = paired ? launch_hough_pairs(p, trig, ctas, smem, stream, cluster)
                          : launch_hough(p, trig, ctas, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "hough_vote_kernel launch");
   return LD_OK;
@@ -457,7 +459,7 @@ int ld_hough_accumulate_opt(const uint32_t *edge_xy, const uint32_t *edge_count,
   g_launches = 0;
   int rc = check_vote_args(edge_xy, edge_count, acc, edge_stride, batch, width, height);
   if (rc) return rc;
-  if (flags & ~static_cast<uint32_t>(LD_VOTE_PLAIN))
+  if (flags & ~static_cast<uint32_t>(LD_VOTE_PLAIN | LD_VOTE_NO_CLUSTER))
     return fail(LD_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
   if (n_theta < 1 || n_theta > LD_MAX_THETA)
     return fail(LD_ERR_INVALID_ARG, "n_theta %d outside [1, %d]", n_theta, LD_MAX_THETA);

@@ -27,6 +27,7 @@
 // While a band is in shared memory the kernel also writes, for the peak
 // search (DESIGN R25, R30), (a) per warp the largest count it saw and its
 // cell, and (b) the maximum of every 1 KB chunk of the accumulator.
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "ld_internal.cuh"
@@ -35,9 +36,6 @@ namespace ld {
 
 #ifndef LD_HV_UNROLL
 #define LD_HV_UNROLL 4  // band rows per unrolled step (plain kernel)
-#endif
-#ifndef LD_HV_ADDR_MODE
-#define LD_HV_ADDR_MODE 0
 #endif
 #ifndef LD_HV_PAIR_UNROLL
 #define LD_HV_PAIR_UNROLL 2  // pairs per unrolled step (paired kernel)
@@ -320,7 +318,7 @@ template <int EPL, bool FULL>
 __device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t blk, uint32_t end,
                                                  int lane, int np, const uint4 *rowk,
                                                  uint32_t row_bytes, uint32_t delta0,
-                                                 uint32_t scratch) {
+                                                 uint32_t scratch, uint32_t win) {
   // one 32-bit load per entry: the kernel is bound by the L1 data pipe
   // (shared-memory atomics + these loads, one wavefront per clock per SM),
   // so the unpacking ALU instructions are cheaper than a second 16-bit load
@@ -343,25 +341,62 @@ __device__ __forceinline__ void vote_block_pairs(const uint32_t *el, uint32_t bl
     for (int j = 0; j < EPL; ++j) {
       const uint32_t v1 = xs[j] * k.x + (ys[j] * k.y + k.z);
       const uint32_t v2 = xs[j] * k.w + v1;
-      // address = ((v >> 13) & ~3) (+ delta) = 4 * hi32(v * 2^17) (+ delta):
-      // shift + mask on the ALU pipe, or IMAD.HI + LEA, moving half the work
-      // to the FMA pipe (LD_HV_ADDR_MODE: 0 both shift/mask, 1 partner via
-      // IMAD.HI, 2 both via IMAD.HI)
-#if LD_HV_ADDR_MODE >= 2
-      red_shared_add(FULL || ok[j] ? __umulhi(v1, 1u << 17) * 4u : scratch, 1u);
-#else
-      red_shared_add(FULL || ok[j] ? (v1 >> 13) & ~3u : scratch, 1u);
-#endif
-#if LD_HV_ADDR_MODE >= 1
-      red_shared_add(FULL || ok[j] ? __umulhi(v2, 1u << 17) * 4u + delta : scratch, 1u);
-#else
-      red_shared_add((FULL || ok[j] ? (v2 >> 13) & ~3u : scratch - delta) + delta, 1u);
-#endif
+      // shift + mask (the IMAD.HI form 4 * hi32(v * 2^17), on the FMA pipe,
+      // measured slower); win = the CTA's shared window (its cluster rank
+      // bits), added as a uniform-register offset of the ATOMS
+      red_shared_add((FULL || ok[j] ? (v1 >> 13) & ~3u : scratch) + win, 1u);
+      red_shared_add((FULL || ok[j] ? (v2 >> 13) & ~3u : scratch - delta) + (delta + win), 1u);
     }
   }
 }
 
-template <int CTAS>
+// Cluster epilogue (G > 1: a band's edges are split over the G CTAs of a
+// thread-block cluster, each voting into its own shared-memory copy of the
+// band -- for single frames, whose bands alone would leave most SMs idle,
+// DESIGN 6.2).  The copies are summed over distributed shared memory: the
+// band's global chunks (SEG_BYTES-aligned, as the summaries) are dealt to the
+// cluster's CTAs and their warps; each lane adds the G copies of its words,
+// stores the sums and folds them into the chunk maximum (atomicMax: a chunk
+// can also belong to a neighbouring band's cluster) and into its best cell
+// (the CTA's hint key).
+template <int G, int NWARPS>
+__device__ __forceinline__ void cluster_reduce_out(const HoughParams &p, uint32_t *dst,
+                                                   int smem_off, int ncell,
+                                                   uint32_t *const *copies, uintptr_t fc0,
+                                                   const uint32_t *frame, int rank, int warp,
+                                                   int lane, unsigned long long &best) {
+  if (ncell <= 0) return;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(dst + ncell);
+  const uintptr_t q0 = a0 / SEG_BYTES, q1 = (a1 - 1) / SEG_BYTES;
+  uint32_t *segmax = p.hint_keys ? p.segmax + static_cast<int64_t>(blockIdx.y) * p.n_seg : nullptr;
+  for (uintptr_t q = q0 + rank + static_cast<uintptr_t>(G) * warp; q <= q1;
+       q += static_cast<uintptr_t>(G) * NWARPS) {
+    uint32_t m = 0u;
+#pragma unroll
+    for (int i = 0; i < SEG_BYTES / 128; ++i) {
+      const uintptr_t a = q * SEG_BYTES + 4u * (32u * i + lane);
+      if (a >= a0 && a < a1) {
+        const int li = static_cast<int>((a - a0) / 4);
+        uint32_t v = 0u;
+#pragma unroll
+        for (int c = 0; c < G; ++c) v += copies[c][smem_off + li];
+        dst[li] = v;
+        m = max(m, v);
+        const unsigned long long key =
+            (static_cast<unsigned long long>(v) << 32) |
+            (0xFFFFFFFFu - static_cast<uint32_t>((dst + li) - frame));
+        if (v && key > best) best = key;
+      }
+    }
+    if (segmax) {
+      m = __reduce_max_sync(0xffffffffu, m);
+      if (lane == 0 && m) atomicMax(segmax + (q - fc0), m);
+    }
+  }
+}
+
+template <int CTAS, int G>
 __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
     hough_vote_pairs_kernel(const HoughParams p, const __grid_constant__ TrigTable trig) {
   constexpr int NT = HV_THREADS / CTAS;
@@ -370,7 +405,8 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   __shared__ uint4 rowk[HV_MAX_ROWS];  // per pair: C, S, K = koff + (row t address << 13), -2C
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int band = blockIdx.x;
+  const int band = blockIdx.x / G;
+  const int rank = G > 1 ? static_cast<int>(blockIdx.x % G) : 0;  // rank in the cluster
   const int f = blockIdx.y;
   const int n_rho = p.n_rho, n_theta = p.n_theta;
   const int p0 = band * p.rows_per_band;
@@ -388,14 +424,18 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   uint32_t *blk1 = slice_raw + mw1;
   uint32_t *blk2 = slice_raw + h2 + mw2;
   const uint32_t row_bytes = static_cast<uint32_t>(n_rho) * 4u;
+  // Shared addresses are the CTA's window (bits 24+: its rank in a cluster,
+  // 0 otherwise) plus an offset < 2^18; only offsets are folded into K (the
+  // << 13 must not overflow 32 bits), the window goes into the ATOMS.
+  const uint32_t win = smem_u32(slice_raw) & 0xFF000000u;
   // partner distance of slot i: delta0 - i * 2 row_bytes
   const uint32_t delta0 = smem_u32(blk2) - smem_u32(blk1) + static_cast<uint32_t>(np - 1) * row_bytes;
-  const uint32_t scratch = smem_u32(blk2 + ncell);  // inside the allocation, never written out
+  const uint32_t scratch = smem_u32(blk2 + ncell) - win;  // inside the allocation, never written out
   {
     uint4 *s4 = reinterpret_cast<uint4 *>(slice_raw);
     const int n4 = (h2 + mw2 + ncell + 1 + 3) >> 2;
     for (int i = tid; i < n4; i += NT) s4[i] = make_uint4(0u, 0u, 0u, 0u);
-    const uint32_t sbase = smem_u32(blk1);
+    const uint32_t sbase = smem_u32(blk1) - win;
     for (int i = tid; i < np; i += NT) {
       const int t = p0 + i;
       rowk[i] = make_uint4(static_cast<uint32_t>(trig.c[t]), static_cast<uint32_t>(trig.s[t]),
@@ -405,17 +445,24 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   }
   __syncthreads();
 
-  const uint32_t n_edges = p.counts[f];
-  const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride;
+  // this CTA's part of the frame's list: all of it, or (cluster) the rank-th
+  // of G parts, cut at multiples of 32 entries
+  const uint32_t n_all = p.counts[f];
+  const uint32_t e_lo = G > 1 ? ((n_all / 32u) * rank / G) * 32u : 0u;
+  const uint32_t e_hi = G > 1 ? (rank == G - 1 ? n_all : ((n_all / 32u) * (rank + 1) / G) * 32u)
+                              : n_all;
+  const uint32_t n_edges = e_hi - e_lo;
+  const uint32_t *el = p.edges + static_cast<int64_t>(f) * p.edge_stride + e_lo;
   uint32_t base = 0;
   for (; base + NWARPS * 32u * 16u <= n_edges; base += NWARPS * 32u * 16u)
     vote_block_pairs<16, true>(el, base + warp * 32u * 16u, n_edges, lane, np, rowk, row_bytes,
-                               delta0, scratch);
+                               delta0, scratch, win);
   uint32_t blk = base + static_cast<uint32_t>(warp) * (32u * 8u);
   for (; blk + 32u * 8u <= n_edges; blk += NWARPS * 32u * 8u)
-    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, row_bytes, delta0, scratch);
+    vote_block_pairs<8, true>(el, blk, n_edges, lane, np, rowk, row_bytes, delta0, scratch, win);
   if (blk < n_edges)
-    vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, row_bytes, delta0, scratch);
+    vote_block_pairs<8, false>(el, blk, n_edges, lane, np, rowk, row_bytes, delta0, scratch,
+                               win);
   fence_proxy_async_smem();
   __syncthreads();
 
@@ -424,6 +471,38 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   // n/2 of an even n, the last pair: block-2 row 0)
   const int j0 = (n_theta % 2 == 0 && p0 + np - 1 == n_theta / 2) ? 1 : 0;
   const int j1 = p0 == 0 ? np - 1 : np;
+  if constexpr (G > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // every copy of the band complete and visible cluster-wide
+    uint32_t *copies[G];
+#pragma unroll
+    for (int c = 0; c < G; ++c) copies[c] = cl.map_shared_rank(slice_raw, c);
+    unsigned long long best = 0ull;
+    const uintptr_t fc0 = reinterpret_cast<uintptr_t>(frame) / SEG_BYTES;
+    cluster_reduce_out<G, NWARPS>(p, dst1, mw1, ncell, copies, fc0, frame, rank, warp, lane,
+                                  best);
+    if (j1 > j0)
+      cluster_reduce_out<G, NWARPS>(p, dst2 + j0 * n_rho, h2 + mw2 + j0 * n_rho,
+                                    (j1 - j0) * n_rho, copies, fc0, frame, rank, warp, lane,
+                                    best);
+    if (p.hint_keys) {  // one key per CTA: the best cell it summed
+      __shared__ unsigned long long s_best;
+      if (tid == 0) s_best = 0ull;
+      __syncthreads();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other > best ? other : best;
+      }
+      if (lane == 0 && best) atomicMax(&s_best, best);
+      __syncthreads();
+      if (tid == 0) p.hint_keys[(static_cast<int64_t>(f) * p.n_bands + band) * G + rank] = s_best;
+      if (f == 0 && band == 0 && tid == 0) write_hint_header(p, G);
+    }
+    cl.sync();  // no CTA leaves while another still reads its copy
+    return;
+  }
   bulk_rows_out(dst1, blk1, ncell, tid, NT);
   if (j1 > j0) bulk_rows_out(dst2 + j0 * n_rho, blk2 + j0 * n_rho, (j1 - j0) * n_rho, tid, NT);
   if (p.hint_keys) {
@@ -468,10 +547,59 @@ int hough_plan_pairs(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *
 }
 
 static AttrOnce g_pairs_attr[3];
+static AttrOnce g_pairs_cl_attr[3][4];
+
+// Thread-block clusters of G CTAs per band when one launch would otherwise
+// occupy fewer than half the SMs (single frames): G = 8, 4 or 2, the largest
+// that keeps the launch within one wave of the plan's CTA slots.
+int hough_cluster_size(int batch, int n_bands, int ctas, int sm_count) {
+  const int64_t ctas_total = static_cast<int64_t>(batch) * n_bands;
+  const int64_t slots = static_cast<int64_t>(sm_count) * ctas;
+  if (2 * ctas_total > static_cast<int64_t>(sm_count)) return 1;
+  for (int g = 8; g >= 2; g >>= 1)
+    if (ctas_total * g <= slots) return g;
+  return 1;
+}
+
+template <int CTAS, int G>
+static cudaError_t launch_pairs_cluster(const HoughParams &p, const TrigTable &trig,
+                                        size_t smem_bytes, cudaStream_t stream, AttrOnce &attr) {
+  auto kern = hough_vote_pairs_kernel<CTAS, G>;
+  cudaError_t e = ensure_smem_attr(attr, kern, -(227 * 1024 / CTAS));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_bands * G, p.batch);
+  cfg.blockDim = dim3(HV_THREADS / CTAS);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, p, trig);
+  note_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int ctas,
-                               size_t smem_bytes, cudaStream_t stream) {
-  auto kern = ctas == 2 ? hough_vote_pairs_kernel<2> : hough_vote_pairs_kernel<1>;
+                               size_t smem_bytes, cudaStream_t stream, int cluster) {
+  if (cluster > 1) {
+    const int gi = cluster == 8 ? 3 : cluster == 4 ? 2 : 1;
+    AttrOnce &a = g_pairs_cl_attr[ctas][gi];
+    if (ctas == 2) {
+      if (cluster == 8) return launch_pairs_cluster<2, 8>(p, trig, smem_bytes, stream, a);
+      if (cluster == 4) return launch_pairs_cluster<2, 4>(p, trig, smem_bytes, stream, a);
+      return launch_pairs_cluster<2, 2>(p, trig, smem_bytes, stream, a);
+    }
+    if (cluster == 8) return launch_pairs_cluster<1, 8>(p, trig, smem_bytes, stream, a);
+    if (cluster == 4) return launch_pairs_cluster<1, 4>(p, trig, smem_bytes, stream, a);
+    return launch_pairs_cluster<1, 2>(p, trig, smem_bytes, stream, a);
+  }
+  auto kern = ctas == 2 ? hough_vote_pairs_kernel<2, 1> : hough_vote_pairs_kernel<1, 1>;
   cudaError_t e = ensure_smem_attr(g_pairs_attr[ctas], kern, -(227 * 1024 / ctas));
   if (e != cudaSuccess) return e;
   dim3 grid(p.n_bands, p.batch);

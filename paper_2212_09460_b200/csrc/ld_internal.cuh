@@ -118,8 +118,12 @@ cudaError_t launch_hough_f64(const HoughParams &p, const TrigTableF64 &trig, int
 int hough_pair_count(int n_theta);
 int hough_plan_pairs(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *pairs_per_band,
                      int *n_bands, size_t *smem_bytes);
+// cluster > 1: the band's edges split over a thread-block cluster of that many
+// CTAs whose shared-memory copies are summed over DSMEM (single frames);
+// hough_cluster_size picks it (1 = no cluster).
+int hough_cluster_size(int batch, int n_bands, int ctas, int sm_count);
 cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int ctas,
-                               size_t smem_bytes, cudaStream_t stream);
+                               size_t smem_bytes, cudaStream_t stream, int cluster = 1);
 
 // ---------------------------------------------------------------------------
 // B4: peaks (ld_peaks.cu)

@@ -51,7 +51,7 @@ class ld_peak(ctypes.Structure):
 PEAK_DTYPE = np.dtype([("theta_bin", "<i4"), ("rho_bin", "<i4"), ("votes", "<u4")])
 
 LD_FLAG_ZERO_PAD, LD_FLAG_CLAMP_255 = 1, 2
-LD_VOTE_PLAIN = 1
+LD_VOTE_PLAIN, LD_VOTE_NO_CLUSTER = 1, 2
 LD_PEAKS_DENSE, LD_PEAKS_FORCE_STREAM, LD_PEAKS_FORCE_TILE, LD_PEAKS_FORCE_BAND = 1, 2, 4, 8
 
 EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",

@@ -1014,3 +1014,29 @@ def test_detect_is_cuda_graph_capturable(ld):
     torch.cuda.synchronize()
     assert torch.equal(det.peaks, ref[0]) and torch.equal(det.n_peaks, ref[1])
     assert torch.equal(det.counts, ref[2])
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_vote_cluster_split_equals_single_cta(ld, oracle, name):
+    """Single frames vote through thread-block clusters (a band's edges split
+    over the cluster's CTAs, copies summed over distributed shared memory):
+    the accumulator, the chunk maxima and the hinted peaks equal the one-CTA-
+    per-band path and the oracle."""
+    cfg = synth.CONFIGS[name]
+    c, s = synth.q15_table(cfg.n_theta)
+    img = synth.gen_frame(name, 0)
+    _, edges, counts, stride = ld.sobel_binarize(cuda(img[None]), cfg.threshold,
+                                                 want_binary=False)
+    h, w = img.shape
+    a_cl, h_cl = ld.hough_accumulate(edges, counts, stride, w, h, c, s, want_hint=True)
+    a_1, h_1 = ld.hough_accumulate(edges, counts, stride, w, h, c, s, want_hint=True,
+                                   flags=ld.LD_VOTE_NO_CLUSTER)
+    torch.cuda.synchronize()
+    assert torch.equal(a_cl, a_1)
+    want = oracle.hough_accumulate(oracle.compact(oracle.sobel_binarize(img, cfg.threshold)),
+                                   w, h, c, s)
+    assert np.array_equal(a_cl.cpu().numpy().view(np.uint32)[0], want)
+    check_chunk_maxima(a_cl, h_cl)
+    p0, n0 = ld.hough_peaks(a_cl, cfg.half_theta, cfg.half_rho, 1, cfg.k)
+    p1, n1 = ld.hough_peaks(a_cl, cfg.half_theta, cfg.half_rho, 1, cfg.k, hint=h_cl)
+    assert torch.equal(p0, p1) and torch.equal(n0, n1)
