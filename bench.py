@@ -706,6 +706,13 @@ def run_cfg5(args, rank, world, dist):
         dist.all_reduce(ecount)
     edges_total = int(ecount.item())
     votes = edges_total * cfg.n_theta
+    if args.profile:
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "votes": votes}), flush=True)
+        return
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nmarks)]
            for _ in range(args.steps)]
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None

@@ -43,7 +43,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libld.so")
-    with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
+    # the ptxas resource report (registers, spills, shared memory per kernel)
+    # goes next to the other build artefacts, out of the source tree
+    os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    with open(os.path.join(ROOT, "build", "ptxas_info.txt"), "w") as f:
         f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)

@@ -234,6 +234,12 @@ __global__ void extract_segments_kernel(const LanesParams p, const __grid_consta
     return;
   }
   const ld_peak pk = p.peaks[static_cast<int64_t>(f) * p.k + i];
+  // a peak from another table size (or a sentinel inside n_peaks) has no line
+  // here: no segments, and no read outside the table
+  if (pk.theta_bin < 0 || pk.theta_bin >= p.n_theta) {
+    if (lane == 0) *nseg = 0;
+    return;
+  }
   const int32_t ci = trig.c[pk.theta_bin], si = trig.s[pk.theta_bin];
   if (ci == 0 && si == 0) {
     if (lane == 0) *nseg = 0;

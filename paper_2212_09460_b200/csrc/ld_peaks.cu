@@ -25,6 +25,11 @@
 
 // largest half_theta for which the streaming kernel loads 4 columns per thread
 // (else 2); a build option (-DLD_PS_CPT4_MAX_HT=...) for experiments
+// the round-2 split hinted search (hint, sparse and finish kernels) instead of
+// the fused one, for A/B timing (-DLD_PEAKS_SPLIT=1)
+#ifndef LD_PEAKS_SPLIT
+#define LD_PEAKS_SPLIT 0
+#endif
 #ifndef LD_PS_CPT4_MAX_HT
 #define LD_PS_CPT4_MAX_HT 6
 #endif
@@ -477,6 +482,484 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_sparse_finish_kernel(const P
   }
   if (threadIdx.x == 0) {
     p.n_peaks[f] = keep;
+    p.resolved[f] = 1u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused hinted search (DESIGN R25 + R30, one CTA per frame, one launch): the
+// bound, the sparse search and its top k without a global round trip or a
+// launch between them -- what bounds a single frame's latency.
+//   1. bound: the voting kernel's range maxima are sorted (bitonic: shuffles
+//      for partners inside a warp, shared memory across warps) and verified
+//      32 at a time, one warp per key, against the full candidate definition;
+//      the value of the k-th verified key in key order bounds the frame's
+//      k-th best candidate from below (tau_f; 0 if fewer than k verify or a
+//      key below the floor ends the list first);
+//   2. sparse: every cell >= tau_f lies in a 1 KB chunk whose recorded maximum
+//      is >= tau_f; the verified keys >= tau_f are candidates already; the
+//      chunks are read one per warp and their other cells >= tau_f checked
+//      lane-parallel against their (up to 8) neighbours inside the window (a
+//      necessary condition); the survivors, pooled, are dealt to the warps for
+//      the exact test (the +-1-row, +-15-column neighbourhood first, where
+//      most of them fail, then the whole window);
+//   3. the candidates (all >= tau_f, at least the k verified ones) are sorted
+//      and the best k written: peaks, n_peaks, resolved = 1.
+// A frame it cannot finish (no or mismatched hint, chunk maxima of another
+// accumulator, fewer than k verified, queue or list overflow) keeps
+// resolved = 0 and gets gtau = tau_f (possibly 0): the dense kernels launched
+// after it start from that bound.  Without p.resolved (dense-only searches)
+// only the bound is computed.
+// ---------------------------------------------------------------------------
+// -DLD_PF_STATS=1 (experiments): per-frame phase clocks and counts into the
+// sparse candidate area of the workspace (cand[f][0..8])
+#ifndef LD_PF_STATS
+#define LD_PF_STATS 0
+#endif
+constexpr int PF_KEYS = 2048;   // range maxima sorted per frame (more are combined)
+constexpr int PF_QUEUE = 2048;  // hot chunks per pass
+constexpr int PF_SURV = 2048;   // prefilter survivors per pass
+static_assert(SP_CAP == 2048, "candidate list size");
+// dynamic shared memory: keys, candidates, survivors (u64) + queue (int)
+constexpr size_t PF_SMEM = sizeof(u64) * (PF_KEYS + SP_CAP + PF_SURV) + sizeof(int) * PF_QUEUE;
+
+// Exact window test of cell idx = (t, r), value v, by one warp: A[idx] == v,
+// every count of the clipped window is <= v and an equal one sits at a higher
+// index.  NEAR: the +-1-row, +-15-column neighbourhood first (one load per
+// lane and row).  The window is then one flat range of cells, U loads in
+// flight per lane; (row, column) advance incrementally (no division per cell).
+template <int U, bool NEAR>
+__device__ __forceinline__ bool warp_window_max(const uint32_t *A, int n_theta, int n_rho, int t,
+                                                int r, uint32_t v, int ht, int hr, int lane) {
+  const uint32_t idx = static_cast<uint32_t>(t) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(r);
+  const int ta = max(t - ht, 0), tb = min(t + ht, n_theta - 1);
+  const int ra = max(r - hr, 0), rb = min(r + hr, n_rho - 1);
+  bool bad = false;
+  if (NEAR) {
+    const int dr = lane - 15;  // lanes 0..30: columns r-15 .. r+15
+    const bool col = lane < 31 && r + dr >= ra && r + dr <= rb;
+    uint32_t w[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int tt = t - 1 + d;
+      w[d] = (col && tt >= ta && tt <= tb) ? __ldg(A + (idx + (d - 1) * n_rho + dr)) : 0u;
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      bad = bad || w[d] > v || (w[d] == v && (d < 1 || (d == 1 && dr < 0))) ||
+            (d == 1 && dr == 0 && w[d] != v);
+    if (__any_sync(0xffffffffu, bad)) return false;
+  }
+  const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
+  int q = lane / wc, m = lane - q * wc;  // lane's first cell: row ta + q, column ra + m
+  const int dq = 32 / wc, dm = 32 - dq * wc;  // advance by 32 cells
+  for (int c0 = 0; c0 < cells; c0 += 32 * U) {
+    uint32_t w[U], ci[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ci[u] = static_cast<uint32_t>(ta + q) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(ra + m);
+      w[u] = c0 + 32 * u + lane < cells ? __ldg(A + ci[u]) : 0u;
+      q += dq;
+      m += dm;
+      if (m >= wc) {
+        m -= wc;
+        ++q;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      bad = bad || w[u] > v || (w[u] == v && ci[u] < idx) ||
+            (ci[u] == idx && w[u] != v && c0 + 32 * u + lane < cells);
+    if (__any_sync(0xffffffffu, bad)) return false;
+  }
+  return true;
+}
+
+// Necessary condition for cell idx = (t, r) with value v: it beats its
+// neighbours at distance 1 that lie inside its window (dt within ht, dr within
+// hr) and inside the accumulator -- by value, or by index on a tie.  One
+// lane, all loads independent.
+__device__ __forceinline__ bool beats_neighbours(const uint32_t *A, int n_theta, int n_rho, int t,
+                                                 int r, uint32_t v, int ht, int hr) {
+  const int64_t idx = static_cast<int64_t>(t) * n_rho + r;
+  uint32_t w[8];
+  bool in[8];
+  int j = 0;
+#pragma unroll
+  for (int dt = -1; dt <= 1; ++dt) {
+#pragma unroll
+    for (int dr = -1; dr <= 1; ++dr) {
+      if (dt == 0 && dr == 0) continue;
+      in[j] = (dt == 0 || ht > 0) && (dr == 0 || hr > 0) && t + dt >= 0 && t + dt < n_theta &&
+              r + dr >= 0 && r + dr < n_rho;
+      w[j] = in[j] ? __ldg(A + idx + dt * n_rho + dr) : 0u;
+      ++j;
+    }
+  }
+  bool ok = true;
+  j = 0;
+#pragma unroll
+  for (int dt = -1; dt <= 1; ++dt) {
+#pragma unroll
+    for (int dr = -1; dr <= 1; ++dr) {
+      if (dt == 0 && dr == 0) continue;
+      const bool lower = dt < 0 || (dt == 0 && dr < 0);  // neighbour index below idx
+      ok = ok && !(in[j] && (w[j] > v || (w[j] == v && lower)));
+      ++j;
+    }
+  }
+  return ok;
+}
+
+// Sort a[0..n2) descending, n2 a power of two in [32, NT * S]: element e lives
+// in register x[e / NT] of thread e % NT; compare-exchange partners inside a
+// warp go through shuffles, across warps through shared memory (a), across
+// register slots in place.  Returns with a[] holding the sorted keys.
+template <int NT, int S>
+__device__ __forceinline__ void block_sort_desc(u64 *a, int n2, u64 (&x)[S]) {
+  const int tid = threadIdx.x;
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= NT) {  // partner in another slot of this thread (S <= 4: slot distance 1 or 2)
+        auto cx = [&](u64 &a, u64 &b, int s) {
+          const int e = s * NT + tid;
+          if (e < n2) {
+            const bool desc = (e & k) == 0;
+            const u64 hi = a > b ? a : b, lo = a > b ? b : a;
+            a = desc ? hi : lo;
+            b = desc ? lo : hi;
+          }
+        };
+        static_assert(S <= 4, "at most 4 slots");
+        if (j == NT) {
+          if (S > 1) cx(x[0], x[1 % S], 0);
+          if (S > 3) cx(x[2 % S], x[3 % S], 2);
+        } else if (S > 3) {
+          cx(x[0], x[2 % S], 0);
+          cx(x[1 % S], x[3 % S], 1);
+        }
+      } else if (j >= 32) {  // partner in another warp
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          if (s * NT + tid < n2) a[s * NT + tid] = x[s];
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const int e = s * NT + tid;
+          if (e < n2) {
+            const u64 o = a[e ^ j];
+            const bool desc = (e & k) == 0, lower = (e & j) == 0;
+            const u64 hi = x[s] > o ? x[s] : o, lo = x[s] > o ? o : x[s];
+            x[s] = (desc == lower) ? hi : lo;
+          }
+        }
+        __syncthreads();
+      } else {  // partner in this warp: all lanes of a warp share the slot's validity
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const int e = s * NT + tid;
+          if (s * NT + (tid & ~31) < n2) {
+            const u64 o = __shfl_xor_sync(0xffffffffu, x[s], j);
+            const bool desc = (e & k) == 0, lower = (e & j) == 0;
+            const u64 hi = x[s] > o ? x[s] : o, lo = x[s] > o ? o : x[s];
+            x[s] = (desc == lower) ? hi : lo;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (s * NT + tid < n2) a[s * NT + tid] = x[s];
+  __syncthreads();
+}
+
+// position of key in a[0..n) sorted descending (distinct keys), or -1
+__device__ __forceinline__ int find_desc(const u64 *a, int n, u64 key) {
+  int lo = 0, hi = n;  // a[lo-1] > key >= a[hi]... invariant: answer in [lo, hi)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] > key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < n && a[lo] == key ? lo : -1;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksParams p) {
+  constexpr int NW = NT / 32;
+  constexpr int S = PF_KEYS / NT;
+  extern __shared__ __align__(16) unsigned char pf_smem[];
+  u64 *keys = reinterpret_cast<u64 *>(pf_smem);  // sorted range maxima
+  u64 *cand = keys + PF_KEYS;                     // candidate keys
+  u64 *surv = cand + SP_CAP;                      // prefilter survivors
+  int *queue = reinterpret_cast<int *>(surv + PF_SURV);
+  __shared__ uint32_t s_vbits[PF_KEYS / 32];      // verified keys (by sorted position)
+  __shared__ int s_ok[NW];
+  __shared__ int s_state, s_found, s_nq, s_ncand, s_nsurv, s_last;
+  __shared__ uint32_t s_tau;
+  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_theta = p.n_theta, n_rho = p.n_rho;
+  const uint32_t *h = p.hint_hdr;
+  const bool match = h[0] == HINT_MAGIC && h[1] == static_cast<uint32_t>(p.batch) &&
+                     h[2] == static_cast<uint32_t>(n_theta) &&
+                     h[3] == static_cast<uint32_t>(n_rho) && h[5] >= 1 &&
+                     h[5] <= HINT_MAX_RANGES && h[4] >= 1 && h[4] <= static_cast<uint32_t>(n_theta) &&
+                     h[6] == static_cast<uint32_t>(p.n_seg);
+  // the chunk maxima describe the accumulator at the address voting wrote it
+  // to: a copy elsewhere keeps the (verified) bound but not the sparse search
+  const uint64_t acc_addr = reinterpret_cast<uintptr_t>(p.acc);
+  const bool sparse = match && p.resolved != nullptr && p.segmax != nullptr &&
+                      h[7] == static_cast<uint32_t>(acc_addr) &&
+                      h[8] == static_cast<uint32_t>(acc_addr >> 32);
+  const int n_src = match ? static_cast<int>(h[4] * h[5]) : 0;
+  const int64_t ncells = static_cast<int64_t>(n_theta) * n_rho;
+  const uint32_t *A = p.acc + static_cast<int64_t>(f) * ncells;
+  const int ht = p.half_theta, hr = p.half_rho;
+#if LD_PF_STATS
+  long long st_t0 = clock64(), st_t1 = 0, st_t2 = 0, st_t3 = 0, st_tl = 0;
+  __shared__ int st_hot, st_surv, st_rounds;
+  if (tid == 0) st_hot = st_surv = st_rounds = 0;
+#endif
+
+  // ---- 1. the bound
+  // more keys than the sort holds: combine g consecutive ranges (the maximum
+  // of a union of ranges is a cell of the accumulator all the same)
+  const int g = (n_src + PF_KEYS - 1) / PF_KEYS;
+  const int n = n_src > 0 ? (n_src + g - 1) / g : 0;
+  int n2 = 32;
+  while (n2 < n) n2 <<= 1;
+  {
+    const u64 *src = p.hint_keys + static_cast<int64_t>(f) * n_src;
+    u64 x[S];
+    if (g == 1) {  // every slot's load in flight at once
+#pragma unroll
+      for (int s = 0; s < S; ++s) x[s] = s * NT + tid < n ? __ldg(src + s * NT + tid) : 0ull;
+    } else {
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = s * NT + tid;
+        u64 m = 0ull;
+        if (i < n)
+          for (int j = i * g; j < min(i * g + g, n_src); ++j) m = src[j] > m ? src[j] : m;
+        x[s] = m;
+      }
+    }
+#if LD_PF_STATS
+    st_tl = clock64();
+#endif
+    if (tid < PF_KEYS / 32) s_vbits[tid] = 0u;
+    if (tid == 0) {
+      s_state = n > 0 ? 0 : 2;
+      s_found = 0;
+      s_tau = 0u;
+      s_nq = 0;
+      s_ncand = 0;
+      s_nsurv = 0;
+      s_last = 0;
+    }
+    block_sort_desc<NT, S>(keys, n2, x);  // ends synchronised
+  }
+#if LD_PF_STATS
+  st_t1 = clock64();
+#endif
+  for (int r0 = 0; s_state == 0; r0 += NW) {
+#if LD_PF_STATS
+    if (tid == 0) ++st_rounds;
+#endif
+    const int j = r0 + warp;
+    const u64 key = j < n2 ? keys[j] : 0ull;
+    const uint32_t v = static_cast<uint32_t>(key >> 32);
+    int ok = -1;  // below the floor or exhausted: this and every later key end the search
+    if (key != 0ull && v >= p.floor_votes) {
+      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+      const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
+      const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
+      ok = (t < n_theta && warp_window_max<16, false>(A, n_theta, n_rho, t, r, v, ht, hr, lane))
+               ? 1 : 0;
+    }
+    if (lane == 0) s_ok[warp] = ok;
+    __syncthreads();
+    if (warp == 0) {
+      const int o = lane < NW ? s_ok[lane] : 0;  // lanes past the round's keys: neutral
+      const uint32_t endm = __ballot_sync(0xffffffffu, o < 0);
+      uint32_t okm = __ballot_sync(0xffffffffu, o > 0);
+      if (endm) okm &= (1u << (__ffs(endm) - 1)) - 1u;  // verified keys before the end
+      const int need = p.k - s_found;
+      const int c = __popc(okm);
+      if (c >= need) {  // the need-th verified key of this round sets the bound
+        const bool me = ((okm >> lane) & 1u) && __popc(okm & ((2u << lane) - 1u)) == need;
+        const uint32_t who = __ballot_sync(0xffffffffu, me);
+        okm &= (2u << (__ffs(who) - 1)) - 1u;  // up to and including it
+        if (lane == 0) {
+          s_tau = static_cast<uint32_t>(keys[r0 + __ffs(who) - 1] >> 32);
+          s_state = 1;
+        }
+      } else if (lane == 0) {
+        s_found += c;
+        if (endm || r0 + NW >= n2) s_state = 2;
+      }
+      if (lane == 0) {
+        s_vbits[r0 >> 5] |= okm << (r0 & 31);  // NW <= 32 keys per round, r0 % NW == 0
+        s_last = r0 + NW;
+      }
+    }
+    __syncthreads();
+  }
+  const uint32_t tau_f = s_tau;  // 0 = no bound
+#if LD_PF_STATS
+  st_t2 = clock64();
+#endif
+  if (tau_f == 0u || !sparse) {
+    if (tid == 0) {
+      p.gtau[f] = tau_f;
+      if (p.resolved) p.resolved[f] = 0u;
+    }
+    return;
+  }
+
+  // ---- 2. the sparse search over the chunks whose maximum reaches tau
+  const uint32_t tau = tau_f > p.floor_votes ? tau_f : p.floor_votes;
+  const int nv = min(s_last, n2);
+  // the verified keys (all >= tau: verified in key order up to the k-th) are
+  // candidates; the chunk scan skips them
+  for (int i = tid; i < nv; i += NT)
+    if ((s_vbits[i >> 5] >> (i & 31)) & 1u) cand[atomicAdd(&s_ncand, 1)] = keys[i];
+  const uint32_t *Sg = p.segmax + static_cast<int64_t>(f) * p.n_seg;
+  const uintptr_t c0 = reinterpret_cast<uintptr_t>(A) / SEG_BYTES;
+  bool fail = false;  // CTA-uniform
+  constexpr int SCAN = 4 * NT;  // chunk maxima per pass, 4 loads in flight per thread
+  for (int base = 0; base < p.n_seg && !fail; base += SCAN) {
+    const int end = min(p.n_seg, base + SCAN);
+    uint32_t sv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = base + u * NT + tid;
+      sv[u] = i < end ? __ldg(Sg + i) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (sv[u] >= tau) {
+        const int slot = atomicAdd(&s_nq, 1);
+        if (slot < PF_QUEUE) queue[slot] = base + u * NT + tid;
+      }
+    }
+    __syncthreads();
+    const int nq = s_nq;
+    if (nq > PF_QUEUE) {
+      fail = true;  // tau is far too low for a sparse search
+      break;
+    }
+#if LD_PF_STATS
+    if (tid == 0) st_hot += nq;
+#endif
+    // 2a: each hot chunk's cells >= tau through the neighbour prefilter
+    for (int qi = warp; qi < nq; qi += NW) {
+      const int64_t w0 = static_cast<int64_t>((c0 + queue[qi]) * SEG_BYTES -
+                                              reinterpret_cast<uintptr_t>(A)) / 4;
+      constexpr int STEPS = SEG_BYTES / 128;
+      uint32_t vv[STEPS];
+#pragma unroll
+      for (int step = 0; step < STEPS; ++step) {
+        const int64_t c = w0 + step * 32 + lane;
+        vv[step] = (c >= 0 && c < ncells) ? __ldg(A + c) : 0u;
+      }
+#pragma unroll
+      for (int step = 0; step < STEPS; ++step) {
+        const uint32_t v = vv[step];
+        if (v >= tau) {
+          const int64_t cell = w0 + step * 32 + lane;
+          const int t = static_cast<int>(cell / n_rho);
+          const int r = static_cast<int>(cell - static_cast<int64_t>(t) * n_rho);
+          const u64 key = mk_key(v, static_cast<uint32_t>(cell));
+          if (beats_neighbours(A, n_theta, n_rho, t, r, v, ht, hr)) {
+            const int pos = find_desc(keys, nv, key);
+            if (pos < 0 || !((s_vbits[pos >> 5] >> (pos & 31)) & 1u)) {
+              const int slot = atomicAdd(&s_nsurv, 1);
+              if (slot < PF_SURV) surv[slot] = key;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int ns = s_nsurv;
+    if (ns > PF_SURV) {
+      fail = true;
+      break;
+    }
+#if LD_PF_STATS
+    if (tid == 0) st_surv += ns;
+#endif
+    // 2b: the survivors, dealt to the warps, through the exact test
+    for (int si = warp; si < ns; si += NW) {
+      const u64 key = surv[si];
+      const uint32_t v = static_cast<uint32_t>(key >> 32);
+      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+      const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
+      const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
+      if (warp_window_max<8, true>(A, n_theta, n_rho, t, r, v, ht, hr, lane) && lane == 0) {
+        const int slot = atomicAdd(&s_ncand, 1);
+        if (slot < SP_CAP) cand[slot] = key;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_nq = 0;
+      s_nsurv = 0;
+    }
+    __syncthreads();
+  }
+  const int nc = s_ncand;
+#if LD_PF_STATS
+  st_t3 = clock64();
+  if (tid == 0 && p.cand) {
+    unsigned long long *o = p.cand + static_cast<int64_t>(f) * SP_CAP;
+    o[0] = st_t1 - st_t0;
+    o[1] = st_t2 - st_t1;
+    o[2] = st_t3 - st_t2;
+    o[3] = st_hot;
+    o[4] = st_surv;
+    o[5] = nc;
+    o[6] = st_rounds;
+    o[7] = n_src;
+    o[8] = tau_f;
+    o[9] = st_tl - st_t0;
+  }
+#endif
+  if (fail || nc > SP_CAP || nc < p.k) {  // (nc >= k always holds with a certified bound)
+    if (tid == 0) {
+      p.gtau[f] = tau_f;
+      p.resolved[f] = 0u;
+    }
+    return;
+  }
+
+  // ---- 3. the best k of the candidates
+  int nc2 = 32;
+  while (nc2 < nc) nc2 <<= 1;
+  {
+    u64 x[SP_CAP / NT];
+#pragma unroll
+    for (int s = 0; s < SP_CAP / NT; ++s) {
+      const int i = s * NT + tid;
+      x[s] = i < nc ? cand[i] : 0ull;
+    }
+    block_sort_desc<NT, SP_CAP / NT>(cand, nc2, x);
+  }
+  ld_peak *out = p.peaks + static_cast<int64_t>(f) * p.k;
+  for (int i = tid; i < p.k; i += NT) {
+    const u64 key = cand[i];
+    const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+    ld_peak pk;
+    pk.theta_bin = static_cast<int32_t>(idx / static_cast<uint32_t>(n_rho));
+    pk.rho_bin = static_cast<int32_t>(idx % static_cast<uint32_t>(n_rho));
+    pk.votes = static_cast<uint32_t>(key >> 32);
+    out[i] = pk;
+  }
+  if (tid == 0) {
+    p.n_peaks[f] = p.k;
+    p.gtau[f] = tau_f;
     p.resolved[f] = 1u;
   }
 }
@@ -1467,7 +1950,9 @@ size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k) {
 static AttrOnce g_tile_attr[PT_MAX_HT + 1];
 static AttrOnce g_stream_attr[2][PT_MAX_HT + 1];
 static AttrOnce g_warp_attr[4];
+static AttrOnce g_fused_attr[2];
 
+#if LD_PEAKS_SPLIT
 // Per-frame starting thresholds: the verified peak hint (R25) when one is
 // given for an unrestricted search and its verification is cheap next to the
 // search it shortens (a window of at most 64 K cells in total over k keys),
@@ -1498,6 +1983,8 @@ static cudaError_t launch_sparse(const PeaksParams &p, cudaStream_t stream) {
   note_launch();
   return cudaGetLastError();
 }
+
+#endif  // LD_PEAKS_SPLIT
 
 cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t stream) {
   PeaksParams p = p_in;
@@ -1531,6 +2018,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
     // the hint (and with it the sparse search) serves the warp and streaming kernels
     PeaksParams ps = p;
     const bool sparse_ok = ps.hint_hdr && ps.segmax && !dense_only;
+#if LD_PEAKS_SPLIT
     ps.ncand = sparse_ok ? p_in.ncand : nullptr;
     ps.resolved = sparse_ok ? p_in.resolved : nullptr;  // the hint kernel clears both
     bool hinted = false;
@@ -1543,6 +2031,31 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
       if (em != cudaSuccess) return em;
       p.resolved = p_in.resolved;
     }
+#else
+    // the bound, the sparse search and its top k in one launch per frame;
+    // dense-only searches take the bound alone
+    const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
+    if (ps.hint_hdr && !restricted && wcells * p.k <= (1 << 20)) {
+      ps.resolved = sparse_ok ? p_in.resolved : nullptr;
+      if (!sparse_ok) ps.segmax = nullptr;
+      // 1024 threads for frames that would leave most SMs idle, else 512
+      // (two CTAs per SM)
+      const bool wide = p.batch < sms;
+      auto kern = wide ? peaks_fused_kernel<1024> : peaks_fused_kernel<512>;
+      const cudaError_t ea = ensure_smem_attr(g_fused_attr[wide], kern, static_cast<int>(PF_SMEM));
+      if (ea != cudaSuccess) return ea;
+      kern<<<p.batch, wide ? 1024 : 512, PF_SMEM, stream>>>(ps);
+      note_launch();
+      const cudaError_t em = cudaGetLastError();
+      if (em != cudaSuccess) return em;
+      p.resolved = ps.resolved;
+    } else {
+      p.hint_hdr = nullptr;
+      p.hint_keys = nullptr;
+      const cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
+      if (em != cudaSuccess) return em;
+    }
+#endif
   }
   if (dense_cheap) {
     WarpKernel kern = warp_kernel(p.half_theta);

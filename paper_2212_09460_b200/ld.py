@@ -601,10 +601,16 @@ class HostDetector:
         self.counts = torch.empty((batch,), dtype=torch.int32).pin_memory()
 
     def __call__(self, gray_host, stream=None):
-        ld_detect_batch_host(gray_host, self.img, self.threshold, self.n_theta, self.cos,
-                             self.sin, self.half_theta, self.half_rho, self.min_votes, self.k,
-                             self.peaks, self.n_peaks, self.counts, self.chunk, self.ws,
-                             self.ws_bytes, stream)
+        """Runs on the detector's device (the C ABI uses the current device),
+        on `stream` or that device's current stream."""
+        import torch
+        with torch.cuda.device(self.device):
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            ld_detect_batch_host(gray_host, self.img, self.threshold, self.n_theta, self.cos,
+                                 self.sin, self.half_theta, self.half_rho, self.min_votes,
+                                 self.k, self.peaks, self.n_peaks, self.counts, self.chunk,
+                                 self.ws, self.ws_bytes, stream)
         return self.peaks, self.n_peaks, self.counts
 
 

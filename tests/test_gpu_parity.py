@@ -864,6 +864,15 @@ def test_extract_segments_vertical_and_synthetic(ld, oracle):
             want, wn = oracle.extract_segments(b[0], tuple(pk[0, i]), c, s, fg, ml, cap=8)
             assert nseg[0, i] == wn
             assert [tuple(int(v) for v in segs[0, i, j]) for j in range(min(wn, 8))] == want
+    # theta bins outside the table (a sentinel, or peaks of another table
+    # size) inside n_peaks: no segments, no out-of-table read
+    bad = np.array([[[-1, d, 1], [180, d + 45, 1], [90, d + 45, 1]]], np.int32)
+    segs, nseg = ld.extract_segments(cuda(b), cuda(bad), cuda(npk), c, s, 15, 0, 8)
+    torch.cuda.synchronize()
+    nseg = nseg.cpu().numpy()
+    assert nseg[0, 0] == 0 and nseg[0, 1] == 0
+    want, wn = oracle.extract_segments(b[0], tuple(bad[0, 2]), c, s, 15, 0, cap=8)
+    assert nseg[0, 2] == wn
 
 
 # ----------------------------------------------------------------------------
