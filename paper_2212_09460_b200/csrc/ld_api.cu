@@ -328,8 +328,7 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   char *ws = static_cast<char *>(workspace);
   p.gtau = reinterpret_cast<uint32_t *>(ws + W.gtau);
   p.resolved = reinterpret_cast<uint32_t *>(ws + W.resolved);
-  p.ncand = reinterpret_cast<uint32_t *>(ws + W.ncand);
-  p.cand = reinterpret_cast<unsigned long long *>(ws + W.cand);
+  p.diag = reinterpret_cast<unsigned long long *>(ws + W.diag);
   p.band_keys = reinterpret_cast<unsigned long long *>(ws + W.keys);
   p.peaks = peaks;
   p.n_peaks = n_peaks;

@@ -94,7 +94,6 @@ constexpr int SEG_BYTES = 1024;  // accumulator bytes per chunk maximum (256 cou
 __host__ __device__ constexpr int seg_count(int64_t n_cells) {
   return static_cast<int>((n_cells * 4 + SEG_BYTES - 1) / SEG_BYTES) + 1;
 }
-constexpr int HINT_MAX_KEYS = 1024;  // per frame, what the verifying kernel sorts (more are merged)
 constexpr int HINT_MAX_RANGES = 32;  // ranges per band (warps of a 1024-thread CTA)
 
 constexpr int HV_THREADS = 1024;  // threads per SM; a CTA has HV_THREADS / CTAS of them
@@ -151,17 +150,17 @@ struct PeaksParams {
   const unsigned long long *hint_keys;
   const uint32_t *segmax;         // hint's chunk maxima [batch][n_seg] (sparse path)
   int32_t n_seg;
-  uint32_t *resolved;             // [batch] 1 = the sparse search wrote this frame's peaks
-  uint32_t *ncand;                // [batch] sparse-search candidates found
-  unsigned long long *cand;       // [batch][SP_CAP] sparse-search candidate keys
+  uint32_t *resolved;             // [batch] 1 = the fused hinted search wrote this frame's peaks
+  unsigned long long *diag;       // [batch][PF_DIAG] diagnostics (LD_PF_STATS builds)
   ld_peak *peaks;
   int32_t *n_peaks;
 };
-constexpr int SP_CAP = 2048;      // sparse search: candidate keys per frame
+constexpr int SP_CAP = 2048;      // fused hinted search: candidate keys per frame
+constexpr int PF_DIAG = 16;       // diagnostics words per frame in the peaks workspace
 
 // Peaks workspace: byte offsets of its parts
 struct PeaksLayout {
-  size_t gtau, resolved, ncand, cand, keys, total;
+  size_t gtau, resolved, diag, keys, total;
 };
 PeaksLayout peaks_layout(int batch, int n_theta, int n_rho, int k);
 size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k);

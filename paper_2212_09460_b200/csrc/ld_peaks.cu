@@ -21,15 +21,12 @@
 // by peaks_hint_kernel from the voting kernel's range maxima (DESIGN R25).
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "ld_internal.cuh"
 
 // largest half_theta for which the streaming kernel loads 4 columns per thread
 // (else 2); a build option (-DLD_PS_CPT4_MAX_HT=...) for experiments
-// the round-2 split hinted search (hint, sparse and finish kernels) instead of
-// the fused one, for A/B timing (-DLD_PEAKS_SPLIT=1)
-#ifndef LD_PEAKS_SPLIT
-#define LD_PEAKS_SPLIT 0
-#endif
 #ifndef LD_PS_CPT4_MAX_HT
 #define LD_PS_CPT4_MAX_HT 6
 #endif
@@ -178,315 +175,6 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
 }
 
 // ---------------------------------------------------------------------------
-// Peak hint (DESIGN R25): one CTA per frame turns the range maxima recorded by
-// the voting kernel into the per-frame starting threshold gtau[f].  The keys
-// (count << 32 | ~cell) are taken largest first -- each warp sorts 32-key
-// chunks with shuffles, then warp 0 merges the chunk heads PH_M keys at a
-// time -- and each batch of PH_M is checked (one warp per key) against the
-// full candidate definition on acc: every count in the clipped window is
-// <= v, and an equal count has a higher (theta, rho) index.  Verified cells
-// are distinct candidates, so the value of the k-th verified key in this
-// order bounds the frame's k-th best candidate from below; with fewer than k
-// verified the bound is 0 (no hint).
-// ---------------------------------------------------------------------------
-constexpr int PH_THREADS = 512;
-constexpr int PH_WARPS = PH_THREADS / 32;
-constexpr int PH_UNROLL = 16;
-constexpr int PH_M = 32;  // keys per merge/verify round
-static_assert(HINT_MAX_KEYS <= 32 * 32, "warp 0 merges at most 32 chunks of 32");
-
-__device__ __forceinline__ u64 warp_sort32_desc(u64 key, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const u64 other = __shfl_xor_sync(0xffffffffu, key, j);
-      const bool desc = (lane & k) == 0, lower = (lane & j) == 0;
-      const u64 hi = other > key ? other : key, lo = other > key ? key : other;
-      key = (desc == lower) ? hi : lo;
-    }
-  }
-  return key;
-}
-
-__global__ void __launch_bounds__(PH_THREADS) peaks_hint_kernel(const PeaksParams p) {
-  __shared__ u64 keys[HINT_MAX_KEYS];
-  __shared__ u64 top[PH_M];
-  __shared__ int s_ok[PH_M];
-  __shared__ uint32_t s_bound;
-  __shared__ int s_done;
-  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t *h = p.hint_hdr;
-  const bool match = h[0] == HINT_MAGIC && h[1] == static_cast<uint32_t>(p.batch) &&
-                     h[2] == static_cast<uint32_t>(p.n_theta) &&
-                     h[3] == static_cast<uint32_t>(p.n_rho) && h[5] >= 1 &&
-                     h[5] <= HINT_MAX_RANGES && h[4] >= 1 && h[4] <= static_cast<uint32_t>(p.n_theta) &&
-                     h[6] == static_cast<uint32_t>(p.n_seg);
-  // the chunk maxima describe the accumulator at the address voting wrote it
-  // to: a copy elsewhere keeps the (verified) keys but not the sparse search
-  const uint64_t acc_addr = reinterpret_cast<uintptr_t>(p.acc);
-  const bool same_acc = h[7] == static_cast<uint32_t>(acc_addr) &&
-                        h[8] == static_cast<uint32_t>(acc_addr >> 32);
-  const int n_src = match ? static_cast<int>(h[4] * h[5]) : 0;
-  if (tid == 0 && p.ncand) {
-    // ncand = SP_CAP + 1 (an "overflow") keeps the sparse search off this
-    // frame when the chunk maxima do not belong to this accumulator
-    p.ncand[f] = (match && same_acc) ? 0u : static_cast<uint32_t>(SP_CAP + 1);
-    p.resolved[f] = 0u;
-  }
-  if (n_src <= 0) {
-    if (tid == 0) p.gtau[f] = 0u;
-    return;
-  }
-  // more keys than the merge holds: combine g consecutive ranges (the
-  // maximum of a union of ranges is again a range maximum)
-  const int g = (n_src + HINT_MAX_KEYS - 1) / HINT_MAX_KEYS;
-  const int n = (n_src + g - 1) / g;
-  const int chunks = (n + 31) >> 5;
-  const u64 *src = p.hint_keys + static_cast<int64_t>(f) * n_src;
-  for (int c = warp; c < chunks; c += PH_WARPS) {
-    const int i = c * 32 + lane;
-    u64 m = 0ull;
-    if (i < n)
-      for (int j = i * g; j < min(i * g + g, n_src); ++j) m = src[j] > m ? src[j] : m;
-    keys[i] = warp_sort32_desc(m, lane);
-  }
-  if (tid == 0) {
-    s_bound = 0u;
-    s_done = 0;
-  }
-  __syncthreads();
-  const uint32_t *A = p.acc + static_cast<int64_t>(f) * p.n_theta * p.n_rho;
-  const int ht = p.half_theta, hr = p.half_rho;
-  int ptr = 0;    // warp 0, lane l: position of chunk l's head
-  u64 head = (warp == 0 && lane < chunks) ? keys[lane * 32] : 0ull;
-  int found = 0;  // thread 0: verified keys so far
-  for (;;) {
-    if (warp == 0) {  // the next PH_M keys, largest first
-      for (int m = 0; m < PH_M; ++m) {
-        u64 best = head;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
-          best = other > best ? other : best;
-        }
-        if (lane == 0) top[m] = best;
-        if (best != 0ull && head == best) {  // keys are distinct: one winner
-          ++ptr;
-          head = ptr < 32 ? keys[lane * 32 + ptr] : 0ull;
-        }
-      }
-    }
-    __syncthreads();
-    for (int j = warp; j < PH_M; j += PH_WARPS) {
-      const u64 key = top[j];
-      const uint32_t v = static_cast<uint32_t>(key >> 32);
-      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
-      int ok = -1;  // below the floor (or exhausted): this and every later key end the search
-      if (key != 0ull && v >= p.floor_votes) {
-        const int t = static_cast<int>(idx / static_cast<uint32_t>(p.n_rho));
-        const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * p.n_rho);
-        const int ta = max(t - ht, 0), tb = min(t + ht, p.n_theta - 1);
-        const int ra = max(r - hr, 0), rb = min(r + hr, p.n_rho - 1);
-        // the clipped window as one flat range of cells, 32 x PH_UNROLL per
-        // warp step: the loads of a step are independent (no early exit
-        // between them), so a small window costs one round trip
-        const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
-        bool bad = false;
-        for (int c0 = 0; c0 < cells && !__any_sync(0xffffffffu, bad); c0 += 32 * PH_UNROLL) {
-          uint32_t w[PH_UNROLL], ci[PH_UNROLL];
-#pragma unroll
-          for (int u = 0; u < PH_UNROLL; ++u) {
-            const int c = c0 + 32 * u + lane;
-            const int tt = ta + c / wc, rr = ra + c % wc;
-            ci[u] = static_cast<uint32_t>(tt) * static_cast<uint32_t>(p.n_rho) + static_cast<uint32_t>(rr);
-            w[u] = c < cells ? __ldg(A + ci[u]) : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < PH_UNROLL; ++u)
-            bad = bad || w[u] > v || (w[u] == v && ci[u] < idx);
-        }
-        ok = !__any_sync(0xffffffffu, bad);
-      }
-      if (lane == 0) s_ok[j] = ok;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int j = 0; j < PH_M; ++j) {
-        if (s_ok[j] < 0) {
-          s_done = 1;
-          break;
-        }
-        if (s_ok[j] && ++found == p.k) {
-          s_bound = static_cast<uint32_t>(top[j] >> 32);
-          s_done = 1;
-          break;
-        }
-      }
-    }
-    __syncthreads();
-    if (s_done) break;
-  }
-  if (tid == 0) p.gtau[f] = s_bound;
-}
-
-// ---------------------------------------------------------------------------
-// Sparse search (DESIGN R30): with a certified bound tau_f = gtau[f] > 0 (the
-// k-th verified hint key, R25) every top-k candidate has votes >= tau_f, and
-// every cell >= tau_f lies in a 1 KB chunk of the accumulator whose maximum
-// (recorded by the voting kernel while the band was in shared memory; a chunk
-// shared by two voting blocks combines their parts) is >= tau_f.  So the
-// search reads the chunk maxima (1/256 of the accumulator), tests only the
-// cells >= tau_f of those chunks against the full candidate definition
-// (one warp per cell, exact window test as in the band kernel), and keeps the
-// keys of the candidates found.  peaks_sparse_finish_kernel then takes their
-// top k.  A frame whose bound is not certified, or whose candidate list
-// overflows SP_CAP, is left unresolved: the dense kernels (which skip
-// resolved frames) compute it.  The result is identical either way.
-// ---------------------------------------------------------------------------
-constexpr int SP_THREADS = 256;
-constexpr int SP_WARPS = SP_THREADS / 32;
-constexpr int SP_QUEUE = 256;   // hot chunks gathered per pass of a CTA
-constexpr int SP_CHUNK = 256;   // chunk maxima scanned per CTA
-
-// Exact candidate test of cell (t, r) with value v by one warp: every count in
-// the clipped window is <= v and an equal count sits at a higher cell index.
-// The +-1 row, +-15 column neighbourhood first (most non-maxima fail there),
-// then the whole window as one flat range, 8 loads in flight per lane.
-__device__ __forceinline__ bool warp_is_candidate(const uint32_t *A, int n_theta, int n_rho, int t,
-                                                  int r, uint32_t v, int ht, int hr, int lane) {
-  const uint32_t idx = static_cast<uint32_t>(t) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(r);
-  const int ta = max(t - ht, 0), tb = min(t + ht, n_theta - 1);
-  const int ra = max(r - hr, 0), rb = min(r + hr, n_rho - 1);
-  bool bad = false;
-  {
-    const int dr = lane - 15;  // lanes 0..30: columns r-15 .. r+15, rows t-1 .. t+1
-    const bool col = lane < 31 && r + dr >= ra && r + dr <= rb;
-    uint32_t w[3], ci[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const int tt = t - 1 + d;
-      ci[d] = static_cast<uint32_t>(tt) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(r + dr);
-      w[d] = (col && tt >= ta && tt <= tb) ? __ldg(A + ci[d]) : 0u;
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) bad = bad || w[d] > v || (w[d] == v && ci[d] < idx);
-  }
-  if (__any_sync(0xffffffffu, bad)) return false;
-  const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
-  for (int c0 = 0; c0 < cells; c0 += 32 * 8) {
-    uint32_t w[8], ci[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int c = c0 + 32 * u + lane;
-      const int tt = ta + c / wc, rr = ra + c % wc;
-      ci[u] = static_cast<uint32_t>(tt) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(rr);
-      w[u] = c < cells ? __ldg(A + ci[u]) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) bad = bad || w[u] > v || (w[u] == v && ci[u] < idx);
-    if (__any_sync(0xffffffffu, bad)) return false;
-  }
-  return true;
-}
-
-__global__ void __launch_bounds__(SP_THREADS) peaks_sparse_kernel(const PeaksParams p) {
-  __shared__ int s_q[SP_QUEUE];
-  __shared__ int s_nq;
-  const int f = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t g = p.gtau[f];
-  // no certified bound, or chunk maxima of another accumulator (ncand set
-  // past SP_CAP by the hint kernel): the dense search handles this frame
-  if (g == 0u || p.ncand[f] > static_cast<uint32_t>(SP_CAP)) return;
-  const uint32_t tau = g > p.floor_votes ? g : p.floor_votes;
-  const int n_rho = p.n_rho, n_theta = p.n_theta;
-  const int64_t ncells = static_cast<int64_t>(n_theta) * n_rho;
-  const uint32_t *S = p.segmax + static_cast<int64_t>(f) * p.n_seg;
-  const uint32_t *A = p.acc + static_cast<int64_t>(f) * ncells;
-  const uintptr_t c0 = reinterpret_cast<uintptr_t>(A) / SEG_BYTES;
-  const int q_begin = blockIdx.x * SP_CHUNK, q_end = min(p.n_seg, q_begin + SP_CHUNK);
-  for (int base = q_begin; base < q_end; base += SP_QUEUE) {
-    if (tid == 0) s_nq = 0;
-    __syncthreads();
-    const int end = min(q_end, base + SP_QUEUE);
-    for (int i = base + tid; i < end; i += SP_THREADS)
-      if (S[i] >= tau) s_q[atomicAdd(&s_nq, 1)] = i;
-    __syncthreads();
-    const int nq = s_nq;
-    for (int q = warp; q < nq; q += SP_WARPS) {
-      // the chunk's 256 words, 32 consecutive per step, all 8 loads in
-      // flight at once; words outside the frame are not read
-      const int64_t w0 = static_cast<int64_t>((c0 + s_q[q]) * SEG_BYTES -
-                                              reinterpret_cast<uintptr_t>(A)) / 4;
-      constexpr int STEPS = SEG_BYTES / 128;
-      uint32_t vv[STEPS];
-#pragma unroll
-      for (int step = 0; step < STEPS; ++step) {
-        const int64_t c = w0 + step * 32 + lane;
-        vv[step] = (c >= 0 && c < ncells) ? __ldg(A + c) : 0u;
-      }
-#pragma unroll
-      for (int step = 0; step < STEPS; ++step) {
-        const uint32_t v = vv[step];
-        uint32_t m = __ballot_sync(0xffffffffu, v >= tau);
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          const uint32_t cv = __shfl_sync(0xffffffffu, v, b);
-          const int64_t cell = w0 + step * 32 + b;
-          const int t = static_cast<int>(cell / n_rho), r = static_cast<int>(cell - static_cast<int64_t>(t) * n_rho);
-          if (warp_is_candidate(A, n_theta, n_rho, t, r, cv, p.half_theta, p.half_rho, lane) &&
-              lane == 0) {
-            const uint32_t slot = atomicAdd(p.ncand + f, 1u);
-            if (slot < static_cast<uint32_t>(SP_CAP))
-              p.cand[static_cast<int64_t>(f) * SP_CAP + slot] =
-                  mk_key(cv, static_cast<uint32_t>(cell));
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// One CTA per frame: the top k of the sparse candidates (a bitonic sort of at
-// most SP_CAP keys) -> peaks, n_peaks, resolved = 1; or nothing (resolved = 0)
-// when the frame had no certified bound or overflowed the list.
-__global__ void __launch_bounds__(PK_THREADS) peaks_sparse_finish_kernel(const PeaksParams p) {
-  __shared__ u64 keys[SP_CAP];
-  const int f = blockIdx.x;
-  const uint32_t n = p.ncand[f];
-  if (p.gtau[f] == 0u || n > static_cast<uint32_t>(SP_CAP)) return;  // resolved stays 0
-  int n2 = 1;
-  while (n2 < static_cast<int>(n)) n2 <<= 1;
-  const u64 *in = p.cand + static_cast<int64_t>(f) * SP_CAP;
-  for (int i = threadIdx.x; i < n2; i += PK_THREADS) keys[i] = i < static_cast<int>(n) ? in[i] : 0ull;
-  __syncthreads();
-  bitonic_desc(keys, n2);
-  const int keep = min(static_cast<int>(n), p.k);
-  ld_peak *out = p.peaks + static_cast<int64_t>(f) * p.k;
-  for (int i = threadIdx.x; i < p.k; i += PK_THREADS) {
-    ld_peak pk;
-    if (i < keep) {
-      const u64 key = keys[i];
-      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
-      pk.theta_bin = static_cast<int32_t>(idx / static_cast<uint32_t>(p.n_rho));
-      pk.rho_bin = static_cast<int32_t>(idx % static_cast<uint32_t>(p.n_rho));
-      pk.votes = static_cast<uint32_t>(key >> 32);
-    } else {
-      pk.theta_bin = -1;
-      pk.rho_bin = -1;
-      pk.votes = 0u;
-    }
-    out[i] = pk;
-  }
-  if (threadIdx.x == 0) {
-    p.n_peaks[f] = keep;
-    p.resolved[f] = 1u;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Fused hinted search (DESIGN R25 + R30, one CTA per frame, one launch): the
 // bound, the sparse search and its top k without a global round trip or a
 // launch between them -- what bounds a single frame's latency.
@@ -512,7 +200,7 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_sparse_finish_kernel(const P
 // only the bound is computed.
 // ---------------------------------------------------------------------------
 // -DLD_PF_STATS=1 (experiments): per-frame phase clocks and counts into the
-// sparse candidate area of the workspace (cand[f][0..8])
+// workspace's diagnostics area (diag[f][0..11], tools/pf_stats.py)
 #ifndef LD_PF_STATS
 #define LD_PF_STATS 0
 #endif
@@ -525,16 +213,23 @@ constexpr size_t PF_SMEM = sizeof(u64) * (PF_KEYS + SP_CAP + PF_SURV) + sizeof(i
 
 // Exact window test of cell idx = (t, r), value v, by one warp: A[idx] == v,
 // every count of the clipped window is <= v and an equal one sits at a higher
-// index.  NEAR: the +-1-row, +-15-column neighbourhood first (one load per
-// lane and row).  The window is then one flat range of cells, U loads in
-// flight per lane; (row, column) advance incrementally (no division per cell).
+// index -- i.e. the cells before idx in (theta, rho) order are < v and the
+// cells after it <= v.  NEAR: the +-1-row, +-15-column neighbourhood first
+// (one load per lane and row), where most non-maxima fail.  Then the centre
+// row cell by cell, then the other rows as 16-byte vectors (each row's cells
+// [ra, rb] from the aligned vector holding ra on; U vectors in flight per
+// lane, (row, vector) advancing incrementally): one maximum per vector, into
+// the maximum above or below the centre row.  A vector reaching outside the
+// frame's cells (misaligned frame edges) is read cell by cell.  Cell indices
+// within a frame fit 32 bits (n_theta * n_rho < 2^31, checked by the host).
 template <int U, bool NEAR>
-__device__ __forceinline__ bool warp_window_max(const uint32_t *A, int n_theta, int n_rho, int t,
-                                                int r, uint32_t v, int ht, int hr, int lane) {
-  const uint32_t idx = static_cast<uint32_t>(t) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(r);
+__device__ __forceinline__ bool warp_window_max(const uint32_t *A, int64_t ncells, int n_theta,
+                                                int n_rho, int t, int r, uint32_t v, int ht,
+                                                int hr, int lane) {
+  const int idx = t * n_rho + r;
   const int ta = max(t - ht, 0), tb = min(t + ht, n_theta - 1);
   const int ra = max(r - hr, 0), rb = min(r + hr, n_rho - 1);
-  bool bad = false;
+  const int nc = static_cast<int>(ncells);
   if (NEAR) {
     const int dr = lane - 15;  // lanes 0..30: columns r-15 .. r+15
     const bool col = lane < 31 && r + dr >= ra && r + dr <= rb;
@@ -544,33 +239,95 @@ __device__ __forceinline__ bool warp_window_max(const uint32_t *A, int n_theta, 
       const int tt = t - 1 + d;
       w[d] = (col && tt >= ta && tt <= tb) ? __ldg(A + (idx + (d - 1) * n_rho + dr)) : 0u;
     }
+    bool bad = false;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
-      bad = bad || w[d] > v || (w[d] == v && (d < 1 || (d == 1 && dr < 0))) ||
-            (d == 1 && dr == 0 && w[d] != v);
+      bad |= w[d] > v || (w[d] == v && (d < 1 || (d == 1 && dr < 0))) ||
+             (d == 1 && dr == 0 && w[d] != v);
     if (__any_sync(0xffffffffu, bad)) return false;
   }
-  const int wc = rb - ra + 1, cells = (tb - ta + 1) * wc;
-  int q = lane / wc, m = lane - q * wc;  // lane's first cell: row ta + q, column ra + m
-  const int dq = 32 / wc, dm = 32 - dq * wc;  // advance by 32 cells
-  for (int c0 = 0; c0 < cells; c0 += 32 * U) {
-    uint32_t w[U], ci[U];
+  {  // the centre row: before r < v, after r <= v, at r == v
+    bool bad = false;
+    const int row0 = t * n_rho;
+#pragma unroll 4
+    for (int c = ra + lane; c <= rb; c += 32) {
+      const uint32_t w = __ldg(A + row0 + c);
+      bad |= c < r ? w >= v : (c > r ? w > v : w != v);  // no short circuit: loads overlap
+    }
+    if (__any_sync(0xffffffffu, bad)) return false;
+  }
+  const int rows = tb - ta;  // rows other than the centre one
+  if (rows == 0) return true;
+  const int nv = (rb - ra + 3) / 4 + 1;  // vectors per row, at any alignment
+  const int items = rows * nv;
+  const int sh = static_cast<int>((reinterpret_cast<uintptr_t>(A) >> 2) & 3u);  // A's word offset mod 4
+  auto row_of = [&](int qq) { return ta + qq + (ta + qq >= t ? 1 : 0); };
+  // first cell of the aligned vector holding cell ra of row tt (frame index)
+  auto first_vec = [&](int tt) {
+    const int c = tt * n_rho + ra;
+    return c - ((c + sh) & 3);
+  };
+  // item 32 u + lane of each step, as (q-th non-centre row, vector j): U
+  // independent chains advancing by 32 U items per step
+  const int dq = 32 * U / nv, dj = 32 * U - dq * nv;
+  int qs[U], js[U], tts[U], a0s[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    qs[u] = (32 * u + lane) / nv;
+    js[u] = 32 * u + lane - qs[u] * nv;
+    tts[u] = row_of(qs[u]);
+    a0s[u] = first_vec(tts[u]);
+  }
+  uint32_t above = 0u, below = 0u;  // maxima over the rows above / below t
+  const int safe = (4 - sh) & 3;  // the frame's first 16-byte-aligned cell
+  for (int i0 = 0; i0 < items; i0 += 32 * U) {
+    uint4 w[U];
+    int lo[U], hi[U], c4[U];  // in-window cells of vector u: e in [lo, hi]
+    bool up[U];
+    bool edge = false;  // a vector reaching outside the frame's cells
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ci[u] = static_cast<uint32_t>(ta + q) * static_cast<uint32_t>(n_rho) + static_cast<uint32_t>(ra + m);
-      w[u] = c0 + 32 * u + lane < cells ? __ldg(A + ci[u]) : 0u;
-      q += dq;
-      m += dm;
-      if (m >= wc) {
-        m -= wc;
-        ++q;
+      c4[u] = a0s[u] + 4 * js[u];
+      const int col0 = c4[u] - tts[u] * n_rho;
+      const bool live = i0 + 32 * u + lane < items && col0 <= rb;
+      lo[u] = ra - col0;
+      hi[u] = live ? rb - col0 : -1;
+      up[u] = tts[u] < t;
+      edge |= live && (c4[u] < 0 || c4[u] + 4 > nc);
+      if (!live) c4[u] = safe;
+      qs[u] += dq;
+      js[u] += dj;
+      if (js[u] >= nv) {
+        js[u] -= nv;
+        ++qs[u];
+      }
+      tts[u] = row_of(qs[u]);
+      a0s[u] = first_vec(tts[u]);
+    }
+    if (!__any_sync(0xffffffffu, edge)) {  // all U vectors of every lane in flight at once
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = __ldg(reinterpret_cast<const uint4 *>(A + c4[u]));
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c4[u];
+        w[u].x = c + 0 >= 0 && c + 0 < nc ? __ldg(A + c + 0) : 0u;
+        w[u].y = c + 1 >= 0 && c + 1 < nc ? __ldg(A + c + 1) : 0u;
+        w[u].z = c + 2 >= 0 && c + 2 < nc ? __ldg(A + c + 2) : 0u;
+        w[u].w = c + 3 >= 0 && c + 3 < nc ? __ldg(A + c + 3) : 0u;
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      bad = bad || w[u] > v || (w[u] == v && ci[u] < idx) ||
-            (ci[u] == idx && w[u] != v && c0 + 32 * u + lane < cells);
-    if (__any_sync(0xffffffffu, bad)) return false;
+    for (int u = 0; u < U; ++u) {
+      const uint32_t m01 = max(0 >= lo[u] && 0 <= hi[u] ? w[u].x : 0u,
+                               1 >= lo[u] && 1 <= hi[u] ? w[u].y : 0u);
+      const uint32_t m23 = max(2 >= lo[u] && 2 <= hi[u] ? w[u].z : 0u,
+                               3 >= lo[u] && 3 <= hi[u] ? w[u].w : 0u);
+      const uint32_t mv = max(m01, m23);
+      above = max(above, up[u] ? mv : 0u);
+      below = max(below, up[u] ? 0u : mv);
+    }
+    if (__any_sync(0xffffffffu, above >= v || below > v)) return false;
   }
   return true;
 }
@@ -613,56 +370,64 @@ __device__ __forceinline__ bool beats_neighbours(const uint32_t *A, int n_theta,
 
 // Sort a[0..n2) descending, n2 a power of two in [32, NT * S]: element e lives
 // in register x[e / NT] of thread e % NT; compare-exchange partners inside a
-// warp go through shuffles, across warps through shared memory (a), across
-// register slots in place.  Returns with a[] holding the sorted keys.
+// warp go through shuffles (run only by the warps that hold elements, all
+// consecutive stages j < 32 of one k in a row), across warps through shared
+// memory (a), across register slots in place.  Returns with a[] holding the
+// sorted keys.
 template <int NT, int S>
 __device__ __forceinline__ void block_sort_desc(u64 *a, int n2, u64 (&x)[S]) {
-  const int tid = threadIdx.x;
+  static_assert(S <= 4, "at most 4 slots");
+  const int tid = threadIdx.x, wbase = tid & ~31;
+  auto cx = [&](u64 &lo_slot, u64 &hi_slot, int s, int k) {  // in-thread pair
+    const int e = s * NT + tid;
+    if (e < n2) {
+      const bool desc = (e & k) == 0;
+      const u64 hi = lo_slot > hi_slot ? lo_slot : hi_slot, lo = lo_slot > hi_slot ? hi_slot : lo_slot;
+      lo_slot = desc ? hi : lo;
+      hi_slot = desc ? lo : hi;
+    }
+  };
   for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= NT) {  // partner in another slot of this thread (S <= 4: slot distance 1 or 2)
-        auto cx = [&](u64 &a, u64 &b, int s) {
-          const int e = s * NT + tid;
-          if (e < n2) {
-            const bool desc = (e & k) == 0;
-            const u64 hi = a > b ? a : b, lo = a > b ? b : a;
-            a = desc ? hi : lo;
-            b = desc ? lo : hi;
-          }
-        };
-        static_assert(S <= 4, "at most 4 slots");
-        if (j == NT) {
-          if (S > 1) cx(x[0], x[1 % S], 0);
-          if (S > 3) cx(x[2 % S], x[3 % S], 2);
-        } else if (S > 3) {
-          cx(x[0], x[2 % S], 0);
-          cx(x[1 % S], x[3 % S], 1);
+    int j = k >> 1;
+    for (; j >= NT; j >>= 1) {  // partner in another slot of this thread
+      if (j == NT) {
+        if (S > 1) cx(x[0], x[1 % S], 0, k);
+        if (S > 3) cx(x[2 % S], x[3 % S], 2, k);
+      } else if (S > 3) {
+        cx(x[0], x[2 % S], 0, k);
+        cx(x[1 % S], x[3 % S], 1, k);
+      }
+    }
+    for (; j >= 32; j >>= 1) {  // partner in another warp
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if (s * NT + tid < n2) a[s * NT + tid] = x[s];
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int e = s * NT + tid;
+        if (e < n2) {
+          const u64 o = a[e ^ j];
+          const bool desc = (e & k) == 0, lower = (e & j) == 0;
+          const u64 hi = x[s] > o ? x[s] : o, lo = x[s] > o ? o : x[s];
+          x[s] = (desc == lower) ? hi : lo;
         }
-      } else if (j >= 32) {  // partner in another warp
+      }
+      __syncthreads();
+    }
+    if (wbase < n2) {  // partners in this warp: stages j .. 1
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-          if (s * NT + tid < n2) a[s * NT + tid] = x[s];
-        __syncthreads();
+      for (int jj = 16; jj > 0; jj >>= 1) {
+        if (jj <= j) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const int e = s * NT + tid;
-          if (e < n2) {
-            const u64 o = a[e ^ j];
-            const bool desc = (e & k) == 0, lower = (e & j) == 0;
-            const u64 hi = x[s] > o ? x[s] : o, lo = x[s] > o ? o : x[s];
-            x[s] = (desc == lower) ? hi : lo;
-          }
-        }
-        __syncthreads();
-      } else {  // partner in this warp: all lanes of a warp share the slot's validity
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const int e = s * NT + tid;
-          if (s * NT + (tid & ~31) < n2) {
-            const u64 o = __shfl_xor_sync(0xffffffffu, x[s], j);
-            const bool desc = (e & k) == 0, lower = (e & j) == 0;
-            const u64 hi = x[s] > o ? x[s] : o, lo = x[s] > o ? o : x[s];
-            x[s] = (desc == lower) ? hi : lo;
+          for (int s = 0; s < S; ++s) {
+            if (s * NT + wbase < n2) {  // warp-uniform
+              const int e = s * NT + tid;
+              const u64 o = __shfl_xor_sync(0xffffffffu, x[s], jj);
+              const bool desc = (e & k) == 0, lower = (e & jj) == 0;
+              const u64 hi = x[s] > o ? x[s] : o, lo = x[s] > o ? o : x[s];
+              x[s] = (desc == lower) ? hi : lo;
+            }
           }
         }
       }
@@ -672,6 +437,93 @@ __device__ __forceinline__ void block_sort_desc(u64 *a, int n2, u64 (&x)[S]) {
   for (int s = 0; s < S; ++s)
     if (s * NT + tid < n2) a[s * NT + tid] = x[s];
   __syncthreads();
+}
+
+// Bitonic networks over L = 32 * M keys held by one warp, element e = 32 i +
+// lane in y[i]: partners inside the warp through shuffles, across registers
+// in place (all indices static).
+template <int M>
+__device__ __forceinline__ void cx_lane(u64 &y, int e, int j, bool desc, int lane) {
+  const u64 o = __shfl_xor_sync(0xffffffffu, y, j);
+  const bool lower = (e & j) == 0;
+  const u64 hi = y > o ? y : o, lo = y > o ? o : y;
+  y = (desc == lower) ? hi : lo;
+}
+template <int M>
+__device__ __forceinline__ void cx_regs(u64 &a, u64 &b, bool desc) {  // a holds the lower element
+  const u64 hi = a > b ? a : b, lo = a > b ? b : a;
+  a = desc ? hi : lo;
+  b = desc ? lo : hi;
+}
+// sort descending
+template <int M>
+__device__ __forceinline__ void warp_sort_desc(u64 (&y)[M], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * M; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+          if ((i & (j >> 5)) == 0) cx_regs<M>(y[i], y[i | (j >> 5)], ((32 * i + lane) & k) == 0);
+      } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) cx_lane<M>(y[i], 32 * i + lane, j, ((32 * i + lane) & k) == 0, lane);
+      }
+    }
+  }
+}
+// a bitonic sequence into descending order
+template <int M>
+__device__ __forceinline__ void warp_merge_desc(u64 (&y)[M], int lane) {
+#pragma unroll
+  for (int j = 16 * M; j > 0; j >>= 1) {
+    if (j >= 32) {
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+        if ((i & (j >> 5)) == 0) cx_regs<M>(y[i], y[i | (j >> 5)], true);
+    } else {
+#pragma unroll
+      for (int i = 0; i < M; ++i) cx_lane<M>(y[i], 32 * i + lane, j, true, lane);
+    }
+  }
+}
+
+// The best L = 32 * M keys of a[0..n2) (n2 a power of two >= L), sorted
+// descending into a[0..L): every warp sorts L-key chunks in registers, then a
+// tree merges chunk pairs keeping the better half -- the elementwise maximum
+// of one sorted list and the other reversed is a bitonic sequence holding
+// the best L of both, which one bitonic merge sorts.  All threads call; ends
+// synchronised.  (A full sort of the 184 .. 2048 range maxima costs 4-19x
+// more: cross-warp stages at every level.)
+template <int NT, int M>
+__device__ void block_top_desc(u64 *a, int n2) {
+  constexpr int NW = NT / 32, L = 32 * M;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int C = n2 / L;
+  for (int c = warp; c < C; c += NW) {
+    u64 y[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) y[i] = a[c * L + 32 * i + lane];
+    warp_sort_desc<M>(y, lane);
+#pragma unroll
+    for (int i = 0; i < M; ++i) a[c * L + 32 * i + lane] = y[i];
+  }
+  __syncthreads();
+  for (int st = 1; st < C; st <<= 1) {
+    for (int c = warp * 2 * st; c < C; c += NW * 2 * st) {
+      u64 y[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const u64 u = a[c * L + 32 * i + lane], z = a[(c + st) * L + (L - 1 - (32 * i + lane))];
+        y[i] = u > z ? u : z;
+      }
+      warp_merge_desc<M>(y, lane);
+#pragma unroll
+      for (int i = 0; i < M; ++i) a[c * L + 32 * i + lane] = y[i];
+    }
+    __syncthreads();
+  }
 }
 
 // position of key in a[0..n) sorted descending (distinct keys), or -1
@@ -685,20 +537,37 @@ __device__ __forceinline__ int find_desc(const u64 *a, int n, u64 key) {
   return lo < n && a[lo] == key ? lo : -1;
 }
 
-template <int NT>
+// Cluster plumbing of the fused search: G CTAs of one frame (a thread-block
+// cluster) split the verification keys and the chunk maxima; CTA 0 of the
+// cluster gathers the candidates (distributed shared memory) and writes the
+// frame's peaks.  G = 1 is the plain one-CTA-per-frame kernel.
+template <int G>
+__device__ __forceinline__ void pf_sync() {
+  if constexpr (G > 1) cooperative_groups::this_cluster().sync();
+  else __syncthreads();
+}
+template <int G, typename T>
+__device__ __forceinline__ T *pf_at(T *p, int rank) {  // p in CTA `rank` of the cluster
+  if constexpr (G > 1) return cooperative_groups::this_cluster().map_shared_rank(p, rank);
+  else return p;
+}
+
+template <int NT, int G>
 __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksParams p) {
   constexpr int NW = NT / 32;
   constexpr int S = PF_KEYS / NT;
+  static_assert(NW <= 32, "one round: at most 32 keys");
   extern __shared__ __align__(16) unsigned char pf_smem[];
   u64 *keys = reinterpret_cast<u64 *>(pf_smem);  // sorted range maxima
-  u64 *cand = keys + PF_KEYS;                     // candidate keys
+  u64 *cand = keys + PF_KEYS;                     // candidate keys (CTA 0)
   u64 *surv = cand + SP_CAP;                      // prefilter survivors
   int *queue = reinterpret_cast<int *>(surv + PF_SURV);
   __shared__ uint32_t s_vbits[PF_KEYS / 32];      // verified keys (by sorted position)
-  __shared__ int s_ok[NW];
-  __shared__ int s_state, s_found, s_nq, s_ncand, s_nsurv, s_last;
+  __shared__ int s_ok[2][NW];                     // a round's results, by parity
+  __shared__ int s_state, s_found, s_nq, s_ncand, s_nsurv, s_last, s_fail;
   __shared__ uint32_t s_tau;
-  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = G > 1 ? static_cast<int>(blockIdx.x % G) : 0;
+  const int f = blockIdx.x / G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_theta = p.n_theta, n_rho = p.n_rho;
   const uint32_t *h = p.hint_hdr;
   const bool match = h[0] == HINT_MAGIC && h[1] == static_cast<uint32_t>(p.batch) &&
@@ -719,7 +588,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
 #if LD_PF_STATS
   long long st_t0 = clock64(), st_t1 = 0, st_t2 = 0, st_t3 = 0, st_tl = 0;
   __shared__ int st_hot, st_surv, st_rounds;
-  if (tid == 0) st_hot = st_surv = st_rounds = 0;
+  __shared__ long long st_lat, st_win;
+  if (tid == 0) {
+    st_hot = st_surv = st_rounds = 0;
+    st_lat = st_win = 0;
+  }
 #endif
 
   // ---- 1. the bound
@@ -727,11 +600,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
   // of a union of ranges is a cell of the accumulator all the same)
   const int g = (n_src + PF_KEYS - 1) / PF_KEYS;
   const int n = n_src > 0 ? (n_src + g - 1) / g : 0;
-  int n2 = 32;
+  // the keys are verified in key order from the best L = 32 m (m from k: the
+  // k-th verified key sat within the best 2k on the road workloads); past
+  // them, all n are sorted and the rounds go on
+  const int m = p.k <= 16 ? 1 : p.k <= 32 ? 2 : 4;
+  int n2 = 32 * m;
   while (n2 < n) n2 <<= 1;
-  {
-    const u64 *src = p.hint_keys + static_cast<int64_t>(f) * n_src;
-    u64 x[S];
+  const u64 *src = p.hint_keys + static_cast<int64_t>(f) * n_src;
+  auto load_keys = [&](u64 (&x)[S]) {
     if (g == 1) {  // every slot's load in flight at once
 #pragma unroll
       for (int s = 0; s < S; ++s) x[s] = s * NT + tid < n ? __ldg(src + s * NT + tid) : 0ull;
@@ -739,15 +615,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int i = s * NT + tid;
-        u64 m = 0ull;
+        u64 mx = 0ull;
         if (i < n)
-          for (int j = i * g; j < min(i * g + g, n_src); ++j) m = src[j] > m ? src[j] : m;
-        x[s] = m;
+          for (int j = i * g; j < min(i * g + g, n_src); ++j) mx = src[j] > mx ? src[j] : mx;
+        x[s] = mx;
       }
     }
+  };
+  {
+    u64 x[S];
+    load_keys(x);
 #if LD_PF_STATS
     st_tl = clock64();
 #endif
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if (s * NT + tid < n2) keys[s * NT + tid] = x[s];
     if (tid < PF_KEYS / 32) s_vbits[tid] = 0u;
     if (tid == 0) {
       s_state = n > 0 ? 0 : 2;
@@ -757,31 +640,59 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
       s_ncand = 0;
       s_nsurv = 0;
       s_last = 0;
+      s_fail = 0;
     }
-    block_sort_desc<NT, S>(keys, n2, x);  // ends synchronised
+    __syncthreads();
+    if (m == 1) block_top_desc<NT, 1>(keys, n2);
+    else if (m == 2) block_top_desc<NT, 2>(keys, n2);
+    else block_top_desc<NT, 4>(keys, n2);
   }
 #if LD_PF_STATS
   st_t1 = clock64();
 #endif
-  for (int r0 = 0; s_state == 0; r0 += NW) {
+  // rounds of NW keys in key order; key r0 + w is tested by warp w of the
+  // cluster's CTA w % G (the others idle), the results read cluster-wide
+  int limit = 32 * m;  // keys[0..limit) are in key order
+  int par = 0;
+  for (int r0 = 0; s_state == 0; r0 += NW, par ^= 1) {
 #if LD_PF_STATS
     if (tid == 0) ++st_rounds;
 #endif
-    const int j = r0 + warp;
-    const u64 key = j < n2 ? keys[j] : 0ull;
-    const uint32_t v = static_cast<uint32_t>(key >> 32);
-    int ok = -1;  // below the floor or exhausted: this and every later key end the search
-    if (key != 0ull && v >= p.floor_votes) {
-      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
-      const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
-      const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
-      ok = (t < n_theta && warp_window_max<16, false>(A, n_theta, n_rho, t, r, v, ht, hr, lane))
-               ? 1 : 0;
+    if (r0 >= limit) {  // past the best L: sort them all (the first L stay in place)
+      u64 x[S];
+      load_keys(x);
+      block_sort_desc<NT, S>(keys, n2, x);
+      limit = n2;
     }
-    if (lane == 0) s_ok[warp] = ok;
-    __syncthreads();
+    const int j = r0 + warp;
+    if (warp % G == rank) {
+      const u64 key = j < n2 ? keys[j] : 0ull;
+      const uint32_t v = static_cast<uint32_t>(key >> 32);
+      int ok = -1;  // below the floor or exhausted: this and every later key end the search
+      if (key != 0ull && v >= p.floor_votes) {
+        const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+        const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
+        const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
+#if LD_PF_STATS
+        long long l0 = clock64();
+        const uint32_t probe = __ldg(A + idx);
+        long long l1 = clock64() + (probe == 0xFFFFFFFFu ? 1 : 0);
+#endif
+        ok = (t < n_theta &&
+              warp_window_max<4, false>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane)) ? 1 : 0;
+#if LD_PF_STATS
+        long long l2 = clock64();
+        if (warp == 0 && lane == 0 && r0 == 0) {
+          st_lat = l1 - l0;
+          st_win = l2 - l1;
+        }
+#endif
+      }
+      if (lane == 0) s_ok[par][warp] = ok;
+    }
+    pf_sync<G>();
     if (warp == 0) {
-      const int o = lane < NW ? s_ok[lane] : 0;  // lanes past the round's keys: neutral
+      const int o = lane < NW ? *pf_at<G>(&s_ok[par][lane], lane % G) : 0;  // past NW: neutral
       const uint32_t endm = __ballot_sync(0xffffffffu, o < 0);
       uint32_t okm = __ballot_sync(0xffffffffu, o > 0);
       if (endm) okm &= (1u << (__ffs(endm) - 1)) - 1u;  // verified keys before the end
@@ -806,31 +717,40 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
     }
     __syncthreads();
   }
-  const uint32_t tau_f = s_tau;  // 0 = no bound
+  // every CTA has read every CTA's last round (its s_ok stays live until here)
+  if (G > 1) pf_sync<G>();
+  const uint32_t tau_f = s_tau;  // 0 = no bound; the same in every CTA of the cluster
 #if LD_PF_STATS
   st_t2 = clock64();
 #endif
   if (tau_f == 0u || !sparse) {
-    if (tid == 0) {
+    if (tid == 0 && rank == 0) {
       p.gtau[f] = tau_f;
       if (p.resolved) p.resolved[f] = 0u;
     }
     return;
   }
 
-  // ---- 2. the sparse search over the chunks whose maximum reaches tau
+  // ---- 2. the sparse search over the chunks whose maximum reaches tau (the
+  // chunk maxima split over the cluster's CTAs; candidates gathered in CTA 0)
   const uint32_t tau = tau_f > p.floor_votes ? tau_f : p.floor_votes;
   const int nv = min(s_last, n2);
+  int *ncand0 = pf_at<G>(&s_ncand, 0);
+  u64 *cand0 = pf_at<G>(cand, 0);
+  int *fail0 = pf_at<G>(&s_fail, 0);
   // the verified keys (all >= tau: verified in key order up to the k-th) are
   // candidates; the chunk scan skips them
-  for (int i = tid; i < nv; i += NT)
-    if ((s_vbits[i >> 5] >> (i & 31)) & 1u) cand[atomicAdd(&s_ncand, 1)] = keys[i];
+  if (rank == 0)
+    for (int i = tid; i < nv; i += NT)
+      if ((s_vbits[i >> 5] >> (i & 31)) & 1u) cand[atomicAdd(&s_ncand, 1)] = keys[i];
   const uint32_t *Sg = p.segmax + static_cast<int64_t>(f) * p.n_seg;
   const uintptr_t c0 = reinterpret_cast<uintptr_t>(A) / SEG_BYTES;
+  const int q_lo = static_cast<int>(static_cast<int64_t>(p.n_seg) * rank / G);
+  const int q_hi = static_cast<int>(static_cast<int64_t>(p.n_seg) * (rank + 1) / G);
   bool fail = false;  // CTA-uniform
   constexpr int SCAN = 4 * NT;  // chunk maxima per pass, 4 loads in flight per thread
-  for (int base = 0; base < p.n_seg && !fail; base += SCAN) {
-    const int end = min(p.n_seg, base + SCAN);
+  for (int base = q_lo; base < q_hi && !fail; base += SCAN) {
+    const int end = min(q_hi, base + SCAN);
     uint32_t sv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -898,9 +818,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
       const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
       const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
       const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
-      if (warp_window_max<8, true>(A, n_theta, n_rho, t, r, v, ht, hr, lane) && lane == 0) {
-        const int slot = atomicAdd(&s_ncand, 1);
-        if (slot < SP_CAP) cand[slot] = key;
+      if (warp_window_max<4, true>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane) &&
+          lane == 0) {
+        const int slot = atomicAdd(ncand0, 1);
+        if (slot < SP_CAP) cand0[slot] = key;
       }
     }
     __syncthreads();
@@ -910,11 +831,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
     }
     __syncthreads();
   }
+  if (fail && tid == 0) atomicOr(fail0, 1);
+  pf_sync<G>();  // every candidate and failure in CTA 0
+  if (rank != 0) return;
   const int nc = s_ncand;
 #if LD_PF_STATS
   st_t3 = clock64();
-  if (tid == 0 && p.cand) {
-    unsigned long long *o = p.cand + static_cast<int64_t>(f) * SP_CAP;
+  if (tid == 0 && p.diag) {
+    unsigned long long *o = p.diag + static_cast<int64_t>(f) * PF_DIAG;
     o[0] = st_t1 - st_t0;
     o[1] = st_t2 - st_t1;
     o[2] = st_t3 - st_t2;
@@ -925,9 +849,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
     o[7] = n_src;
     o[8] = tau_f;
     o[9] = st_tl - st_t0;
+    o[10] = st_lat;
+    o[11] = st_win;
   }
 #endif
-  if (fail || nc > SP_CAP || nc < p.k) {  // (nc >= k always holds with a certified bound)
+  if (s_fail || nc > SP_CAP || nc < p.k) {  // (nc >= k always holds with a certified bound)
     if (tid == 0) {
       p.gtau[f] = tau_f;
       p.resolved[f] = 0u;
@@ -1926,19 +1852,18 @@ extern "C" int ld_debug_error_line(void) {
 #endif
 
 PeaksLayout peaks_layout(int batch, int n_theta, int n_rho, int k) {
-  // per-frame thresholds, resolved flags and sparse candidate counts (each
-  // 256-B padded), the sparse candidate keys, then the per-unit top-k keys:
-  // worst case over the dense kernels (tiles/units of >= 16 rows x >= 32
-  // columns, or bands of PK_ROWS rows)
+  // per-frame thresholds and resolved flags (each 256-B padded), the
+  // diagnostics area (PF_DIAG words per frame, written by experiment builds
+  // only), then the per-unit top-k keys: worst case over the dense kernels
+  // (tiles/units of >= 16 rows x >= 32 columns, or bands of PK_ROWS rows)
   const size_t tiles = static_cast<size_t>((n_theta + PT_TR - 1) / PT_TR) * ((n_rho + 31) / 32);
   const size_t bands = static_cast<size_t>((n_theta + PK_ROWS - 1) / PK_ROWS);
   const size_t head = (sizeof(uint32_t) * static_cast<size_t>(batch) + 255) / 256 * 256;
   PeaksLayout L;
   L.gtau = 0;
   L.resolved = head;
-  L.ncand = 2 * head;
-  L.cand = 3 * head;
-  L.keys = L.cand + sizeof(u64) * static_cast<size_t>(batch) * SP_CAP;
+  L.diag = 2 * head;
+  L.keys = L.diag + sizeof(u64) * static_cast<size_t>(batch) * PF_DIAG;
   L.total = L.keys + static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
   return L;
 }
@@ -1950,41 +1875,43 @@ size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k) {
 static AttrOnce g_tile_attr[PT_MAX_HT + 1];
 static AttrOnce g_stream_attr[2][PT_MAX_HT + 1];
 static AttrOnce g_warp_attr[4];
-static AttrOnce g_fused_attr[2];
+static AttrOnce g_fused_attr[5];
 
-#if LD_PEAKS_SPLIT
-// Per-frame starting thresholds: the verified peak hint (R25) when one is
-// given for an unrestricted search and its verification is cheap next to the
-// search it shortens (a window of at most 64 K cells in total over k keys),
-// else 0.  Returns whether the hint is used (p.hint_hdr is cleared if not,
-// which the warp kernel reads).
-static cudaError_t init_gtau(PeaksParams &p, bool restricted, cudaStream_t stream, bool *hinted) {
-  const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
-  *hinted = p.hint_hdr && !restricted && wcells * p.k <= (1 << 20);
-  if (*hinted) {
-    peaks_hint_kernel<<<p.batch, PH_THREADS, 0, stream>>>(p);
-    note_launch();
-    return cudaGetLastError();
-  }
-  p.hint_hdr = nullptr;
-  p.hint_keys = nullptr;
-  return cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
-}
-
-// The sparse search (R30) over the frames whose bound the hint certified;
-// the dense kernels launched after it skip the frames it resolved.
-static cudaError_t launch_sparse(const PeaksParams &p, cudaStream_t stream) {
-  dim3 g1(static_cast<unsigned>((p.n_seg + SP_CHUNK - 1) / SP_CHUNK), p.batch);
-  peaks_sparse_kernel<<<g1, SP_THREADS, 0, stream>>>(p);
-  note_launch();
-  cudaError_t e = cudaGetLastError();
+// The fused hinted search: 512 threads per frame (two CTAs per SM) for
+// batches that fill the GPU, else 1024, in clusters of G = 2..8 CTAs per
+// frame while the frames alone would leave most SMs idle.
+template <int NT, int G>
+static cudaError_t launch_fused_g(const PeaksParams &p, AttrOnce &attr, cudaStream_t stream) {
+  auto kern = peaks_fused_kernel<NT, G>;
+  cudaError_t e = ensure_smem_attr(attr, kern, static_cast<int>(PF_SMEM));
   if (e != cudaSuccess) return e;
-  peaks_sparse_finish_kernel<<<p.batch, PK_THREADS, 0, stream>>>(p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.batch * G);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = PF_SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, p);
   note_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-#endif  // LD_PEAKS_SPLIT
+static cudaError_t launch_fused(const PeaksParams &p, int sms, cudaStream_t stream) {
+  if (p.batch >= sms) return launch_fused_g<512, 1>(p, g_fused_attr[0], stream);
+  const int per = sms / p.batch;
+  if (per >= 8) return launch_fused_g<1024, 8>(p, g_fused_attr[4], stream);
+  if (per >= 4) return launch_fused_g<1024, 4>(p, g_fused_attr[3], stream);
+  if (per >= 2) return launch_fused_g<1024, 2>(p, g_fused_attr[2], stream);
+  return launch_fused_g<1024, 1>(p, g_fused_attr[1], stream);
+}
+
 
 cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t stream) {
   PeaksParams p = p_in;
@@ -2018,35 +1945,13 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
     // the hint (and with it the sparse search) serves the warp and streaming kernels
     PeaksParams ps = p;
     const bool sparse_ok = ps.hint_hdr && ps.segmax && !dense_only;
-#if LD_PEAKS_SPLIT
-    ps.ncand = sparse_ok ? p_in.ncand : nullptr;
-    ps.resolved = sparse_ok ? p_in.resolved : nullptr;  // the hint kernel clears both
-    bool hinted = false;
-    cudaError_t em = init_gtau(ps, restricted, stream, &hinted);
-    if (em != cudaSuccess) return em;
-    p.hint_hdr = ps.hint_hdr;
-    p.hint_keys = ps.hint_keys;
-    if (hinted && ps.ncand) {
-      em = launch_sparse(ps, stream);
-      if (em != cudaSuccess) return em;
-      p.resolved = p_in.resolved;
-    }
-#else
     // the bound, the sparse search and its top k in one launch per frame;
     // dense-only searches take the bound alone
     const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
     if (ps.hint_hdr && !restricted && wcells * p.k <= (1 << 20)) {
       ps.resolved = sparse_ok ? p_in.resolved : nullptr;
       if (!sparse_ok) ps.segmax = nullptr;
-      // 1024 threads for frames that would leave most SMs idle, else 512
-      // (two CTAs per SM)
-      const bool wide = p.batch < sms;
-      auto kern = wide ? peaks_fused_kernel<1024> : peaks_fused_kernel<512>;
-      const cudaError_t ea = ensure_smem_attr(g_fused_attr[wide], kern, static_cast<int>(PF_SMEM));
-      if (ea != cudaSuccess) return ea;
-      kern<<<p.batch, wide ? 1024 : 512, PF_SMEM, stream>>>(ps);
-      note_launch();
-      const cudaError_t em = cudaGetLastError();
+      const cudaError_t em = launch_fused(ps, sms, stream);
       if (em != cudaSuccess) return em;
       p.resolved = ps.resolved;
     } else {
@@ -2055,7 +1960,6 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
       const cudaError_t em = cudaMemsetAsync(p.gtau, 0, sizeof(uint32_t) * p.batch, stream);
       if (em != cudaSuccess) return em;
     }
-#endif
   }
   if (dense_cheap) {
     WarpKernel kern = warp_kernel(p.half_theta);

@@ -712,8 +712,12 @@ def _hint_case(ld, oracle, frames, cfg, kernel=None, monkeypatch=None, check_ora
     return gtau, p1c, n1c
 
 
-@pytest.mark.parametrize("name,nf", [("cfg1", 1), ("cfg2", 1), ("cfg3", 6), ("cfg4", 2),
-                                     ("cfg5", 1)])
+# (frame counts cover every launch shape of the fused search: clusters of 8
+# CTAs per frame (1-18 frames), 4 (19-37), 2 (38-73, cfg4's 64), one 1024-
+# thread CTA (74-147) and one 512-thread CTA (>= 148: cfg3's 256, in
+# test_gpu_full_configs))
+@pytest.mark.parametrize("name,nf", [("cfg1", 1), ("cfg2", 1), ("cfg3", 6), ("cfg3", 24),
+                                     ("cfg3", 100), ("cfg4", 2), ("cfg5", 1)])
 def test_hinted_peaks_identical(ld, oracle, name, nf):
     cfg = synth.CONFIGS[name]
     frames = synth.gen_batch(name, 0, nf) if cfg.batch > 1 else synth.gen_frame(name, 0)[None]
@@ -753,6 +757,53 @@ def test_hint_header_mismatch_ignored(ld, oracle):
     with pytest.raises(ld.LdError):  # too small a hint buffer
         ld.ld_hough_accumulate_hint(edges, counts, stride, 1, 1280, 720, cfg.n_theta, c, s, acc,
                                     hint, 64)
+
+
+_MISALIGNED_CACHE = {}
+
+
+@pytest.mark.parametrize("shift", [1, 2, 3])
+@pytest.mark.parametrize("name", ["cfg1", "cfg4"])
+def test_hinted_peaks_misaligned_accumulator(ld, oracle, name, shift):
+    # an accumulator that starts 4/8/12 bytes past a 16-byte boundary (the
+    # ABI asks only for 4-byte alignment): the window tests read 16-byte
+    # vectors aligned to the allocation, so frame edges fall inside vectors;
+    # voting and the hinted search against the oracle, frame by frame
+    cfg = synth.CONFIGS[name]
+    nf = 2
+    frames = synth.gen_batch(name, 0, nf) if cfg.batch > 1 else np.stack(
+        [synth.gen_frame(name, 0)] * nf)
+    c, s = synth.q15_table(cfg.n_theta)
+    b, h, w = frames.shape
+    _, edges, counts, stride = ld.sobel_binarize(cuda(frames), cfg.threshold, want_binary=False)
+    nr = 2 * ld.ld_rho_offset(w, h) + 1
+    buf = torch.full((b * cfg.n_theta * nr + 4,), -1, dtype=torch.int32, device="cuda")
+    acc = buf[shift:shift + b * cfg.n_theta * nr].view(b, cfg.n_theta, nr)
+    hb = ld.ld_hough_hint_bytes(b, w, h, cfg.n_theta)
+    hint = torch.empty((hb,), dtype=torch.uint8, device="cuda")
+    ld.ld_hough_accumulate_hint(edges, counts, stride, b, w, h, cfg.n_theta, c, s, acc, hint, hb)
+    wsb = ld.ld_hough_peaks_workspace_bytes(b, cfg.n_theta, nr, cfg.k)
+    ws = torch.zeros((wsb,), dtype=torch.uint8, device="cuda")
+    pk = torch.empty((b, cfg.k, 3), dtype=torch.int32, device="cuda")
+    npk = torch.empty((b,), dtype=torch.int32, device="cuda")
+    ld.ld_hough_peaks_hinted(acc, b, cfg.n_theta, nr, cfg.half_theta, cfg.half_rho,
+                             cfg.min_votes, cfg.k, hint, hb, pk, npk, ws, wsb)
+    torch.cuda.synchronize()
+    assert buf[:shift].eq(-1).all() and buf[shift + acc.numel():].eq(-1).all()
+    A = acc.cpu().numpy().view(np.uint32)
+    pkc, npc = pk.cpu().numpy(), npk.cpu().numpy()
+    for f in range(b):
+        key = (name, f)
+        if key not in _MISALIGNED_CACHE:  # the oracle's result does not depend on the shift
+            want = oracle.hough_accumulate(
+                oracle.compact(oracle.sobel_binarize(frames[f], cfg.threshold)), w, h, c, s)
+            _MISALIGNED_CACHE[key] = (want, oracle.hough_peaks(want, cfg.half_theta,
+                                                               cfg.half_rho, cfg.min_votes,
+                                                               cfg.k))
+        want, (opk, onp) = _MISALIGNED_CACHE[key]
+        assert np.array_equal(A[f], want)
+        assert int(npc[f]) == onp
+        assert peak_tuples(pkc[f]) == oracle_peak_tuples(opk)
 
 
 # ----------------------------------------------------------------------------

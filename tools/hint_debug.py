@@ -4,7 +4,7 @@
     python tools/hint_debug.py cfg2 [cfg5 ...]
 
 Votes one frame with ld_hough_accumulate_hint, then (host numpy) sorts the
-hint keys, tests each against its window exactly as peaks_hint_kernel does and
+hint keys, tests each against its window exactly as peaks_fused_kernel does and
 prints at which sorted position the k-th verified key sits (the number of
 verification rounds of PH_M keys the kernel needs), the threshold it leaves
 and the frame's true k-th peak value (from the hinted search's output)."""

@@ -33,11 +33,11 @@ def main():
                                  cfg.k, hint, hint.numel(), pk, npk, ws, wsb)
         torch.cuda.synchronize()
         head = (4 * b + 255) // 256 * 256
-        cand = ws[3 * head:].cpu().numpy()[:8 * 2048 * b].view(np.uint64).reshape(b, 2048)
+        cand = ws[2 * head:].cpu().numpy()[:8 * 16 * b].view(np.uint64).reshape(b, 16)
         res = ws[head:head + 4 * b].cpu().numpy().view(np.uint32)
-        print(name, "cycles bound-sort/verify/sparse, hot, survivors, cand, rounds, n_src, tau, load-cycles, resolved")
+        print(name, "cycles bound-sort/verify/sparse, hot, survivors, cand, rounds, n_src, tau, load-cycles, 1-load latency, window-test cycles, resolved")
         for f in range(b):
-            print("  ", cand[f, :10].tolist(), int(res[f]))
+            print("  ", cand[f, :12].tolist(), int(res[f]))
 
 
 if __name__ == "__main__":
