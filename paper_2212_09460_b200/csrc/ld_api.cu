@@ -187,7 +187,7 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
   cuuint64_t gdim[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(rows_read),
                         static_cast<cuuint64_t>(img->batch)};
   cuuint64_t gstride[2] = {static_cast<cuuint64_t>(img->pitch), static_cast<cuuint64_t>(fstride)};
-  const SobelCfg cfg = sobel_cfg();
+  const SobelCfg cfg = sobel_cfg(W, img->row_end - img->row_begin, img->batch, dev.sm_count);
   const int tile_h = cfg.sr * SB_STRIPS;
   cuuint32_t box[3] = {SB_BOX_W, static_cast<cuuint32_t>(tile_h + 2), 1};
   cuuint32_t estr[3] = {1, 1, 1};
@@ -206,6 +206,7 @@ static int sobel_impl(const uint8_t *gray, const ld_image *img, int32_t threshol
   p.tiles_x = (W + SB_TILE_W - 1) / SB_TILE_W;
   p.tiles_y = (img->row_end - img->row_begin + tile_h - 1) / tile_h;
   p.tiles_per_frame = p.tiles_x * p.tiles_y;
+  p.sr = cfg.sr;
   const int64_t n_tiles = static_cast<int64_t>(p.tiles_per_frame) * img->batch;
   if (n_tiles > (1ll << 30)) return fail(LD_ERR_INVALID_ARG, "batch too large");
   p.n_tiles = static_cast<int32_t>(n_tiles);

@@ -29,7 +29,8 @@ struct SobelCfg {
   int sr, stages, ctas_per_sm;
   int cap = SB_STAGE_CAP;  // per-warp edge staging entries (0: direct global stores)
 };
-SobelCfg sobel_cfg();
+// rows = output rows owned, frames = batch, sms = SM count
+SobelCfg sobel_cfg(int width, int rows, int frames, int sms);
 
 struct SobelParams {
   int32_t width, height;
@@ -37,6 +38,7 @@ struct SobelParams {
   int32_t ry0;                 // global row of tensor row 0 = max(row_begin-1, 0)
   int32_t tiles_x, tiles_y, tiles_per_frame, n_tiles;
   int32_t batch;
+  int32_t sr;                  // output rows per thread strip (sobel_cfg; tile height 16 * sr)
   int32_t t2;                  // ceil(T/2) clamped to [0, 766]
   int32_t zero_pad;            // LD_FLAG_ZERO_PAD: filter the border on a zero-padded image
   uint8_t *binary;

@@ -552,10 +552,11 @@ __device__ __forceinline__ T *pf_at(T *p, int rank) {  // p in CTA `rank` of the
   else return p;
 }
 
-template <int NT, int G>
-__global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksParams p) {
+template <int NT, int G, int MINB>
+__global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams p) {
   constexpr int NW = NT / 32;
   constexpr int S = PF_KEYS / NT;
+  constexpr int WU = MINB > 1 ? 2 : 4;  // window-test vectors in flight per lane (register budget)
   static_assert(NW <= 32, "one round: at most 32 keys");
   extern __shared__ __align__(16) unsigned char pf_smem[];
   u64 *keys = reinterpret_cast<u64 *>(pf_smem);  // sorted range maxima
@@ -650,11 +651,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
 #if LD_PF_STATS
   st_t1 = clock64();
 #endif
-  // rounds of NW keys in key order; key r0 + w is tested by warp w of the
-  // cluster's CTA w % G (the others idle), the results read cluster-wide
+  // rounds of RW keys in key order; key r0 + i is tested by warp i / G of the
+  // cluster's CTA i % G, the results read cluster-wide
+  constexpr int RW = NW * G < 32 ? NW * G : 32;
   int limit = 32 * m;  // keys[0..limit) are in key order
   int par = 0;
-  for (int r0 = 0; s_state == 0; r0 += NW, par ^= 1) {
+  for (int r0 = 0; s_state == 0; r0 += RW, par ^= 1) {
 #if LD_PF_STATS
     if (tid == 0) ++st_rounds;
 #endif
@@ -664,8 +666,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
       block_sort_desc<NT, S>(keys, n2, x);
       limit = n2;
     }
-    const int j = r0 + warp;
-    if (warp % G == rank) {
+    const int i = warp * G + rank;
+    if (i < RW) {
+      const int j = r0 + i;
       const u64 key = j < n2 ? keys[j] : 0ull;
       const uint32_t v = static_cast<uint32_t>(key >> 32);
       int ok = -1;  // below the floor or exhausted: this and every later key end the search
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
         long long l1 = clock64() + (probe == 0xFFFFFFFFu ? 1 : 0);
 #endif
         ok = (t < n_theta &&
-              warp_window_max<4, false>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane)) ? 1 : 0;
+              warp_window_max<WU, false>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane)) ? 1 : 0;
 #if LD_PF_STATS
         long long l2 = clock64();
         if (warp == 0 && lane == 0 && r0 == 0) {
@@ -692,7 +695,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
     }
     pf_sync<G>();
     if (warp == 0) {
-      const int o = lane < NW ? *pf_at<G>(&s_ok[par][lane], lane % G) : 0;  // past NW: neutral
+      // key r0 + lane: warp lane / G of CTA lane % G; past RW: neutral
+      const int o = lane < RW ? *pf_at<G>(&s_ok[par][lane / G], lane % G) : 0;
       const uint32_t endm = __ballot_sync(0xffffffffu, o < 0);
       uint32_t okm = __ballot_sync(0xffffffffu, o > 0);
       if (endm) okm &= (1u << (__ffs(endm) - 1)) - 1u;  // verified keys before the end
@@ -708,11 +712,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
         }
       } else if (lane == 0) {
         s_found += c;
-        if (endm || r0 + NW >= n2) s_state = 2;
+        if (endm || r0 + RW >= n2) s_state = 2;
       }
       if (lane == 0) {
-        s_vbits[r0 >> 5] |= okm << (r0 & 31);  // NW <= 32 keys per round, r0 % NW == 0
-        s_last = r0 + NW;
+        s_vbits[r0 >> 5] |= okm << (r0 & 31);  // RW divides 32: a round stays in one word
+        s_last = r0 + RW;
       }
     }
     __syncthreads();
@@ -818,7 +822,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) peaks_fused_kernel(const PeaksP
       const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
       const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
       const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
-      if (warp_window_max<4, true>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane) &&
+      if (warp_window_max<WU, true>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane) &&
           lane == 0) {
         const int slot = atomicAdd(ncand0, 1);
         if (slot < SP_CAP) cand0[slot] = key;
@@ -1877,12 +1881,13 @@ static AttrOnce g_stream_attr[2][PT_MAX_HT + 1];
 static AttrOnce g_warp_attr[4];
 static AttrOnce g_fused_attr[5];
 
-// The fused hinted search: 512 threads per frame (two CTAs per SM) for
-// batches that fill the GPU, else 1024, in clusters of G = 2..8 CTAs per
-// frame while the frames alone would leave most SMs idle.
-template <int NT, int G>
+// The fused hinted search: 512 threads per CTA; two CTAs per SM (64
+// registers) for batches that fill the GPU, else one (128 registers: the
+// window tests' loads and chains stay in registers), in clusters of G = 2..8
+// CTAs per frame while the frames alone would leave most SMs idle.
+template <int NT, int G, int MINB>
 static cudaError_t launch_fused_g(const PeaksParams &p, AttrOnce &attr, cudaStream_t stream) {
-  auto kern = peaks_fused_kernel<NT, G>;
+  auto kern = peaks_fused_kernel<NT, G, MINB>;
   cudaError_t e = ensure_smem_attr(attr, kern, static_cast<int>(PF_SMEM));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1904,12 +1909,12 @@ static cudaError_t launch_fused_g(const PeaksParams &p, AttrOnce &attr, cudaStre
 }
 
 static cudaError_t launch_fused(const PeaksParams &p, int sms, cudaStream_t stream) {
-  if (p.batch >= sms) return launch_fused_g<512, 1>(p, g_fused_attr[0], stream);
+  if (p.batch >= sms) return launch_fused_g<512, 1, 2>(p, g_fused_attr[0], stream);
   const int per = sms / p.batch;
-  if (per >= 8) return launch_fused_g<1024, 8>(p, g_fused_attr[4], stream);
-  if (per >= 4) return launch_fused_g<1024, 4>(p, g_fused_attr[3], stream);
-  if (per >= 2) return launch_fused_g<1024, 2>(p, g_fused_attr[2], stream);
-  return launch_fused_g<1024, 1>(p, g_fused_attr[1], stream);
+  if (per >= 8) return launch_fused_g<512, 8, 1>(p, g_fused_attr[4], stream);
+  if (per >= 4) return launch_fused_g<512, 4, 1>(p, g_fused_attr[3], stream);
+  if (per >= 2) return launch_fused_g<512, 2, 1>(p, g_fused_attr[2], stream);
+  return launch_fused_g<512, 1, 1>(p, g_fused_attr[1], stream);
 }
 
 

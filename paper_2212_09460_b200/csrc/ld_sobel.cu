@@ -404,17 +404,25 @@ static cudaError_t launch_cfg(const CUtensorMap &tmap, const SobelParams &p, int
 // stages, 2 CTAs per SM, 1024-entry per-warp edge staging.  Measured on B200
 // (profiles/) against 3 stages (smaller staging), 3 CTAs per SM
 // (register-capped), 64- and 96-row tiles and direct (unstaged) edge stores:
-// all slower on cfg3 and cfg4.
+// all slower on cfg3 and cfg4.  Work too small to give every SM a 128-row
+// tile (single frames: cfg1, cfg2, 512 x 512) takes 32-row tiles (SR = 2),
+// four times as many CTAs each with a quarter of the latency.
 #ifndef LD_SOBEL_SR
 #define LD_SOBEL_SR 8  // output rows per thread strip (tile height 16 * SR)
 #endif
-SobelCfg sobel_cfg() { return SobelCfg{LD_SOBEL_SR, 2, 2, SB_STAGE_CAP}; }
+SobelCfg sobel_cfg(int width, int rows, int frames, int sms) {
+  const int64_t tiles = static_cast<int64_t>((width + SB_TILE_W - 1) / SB_TILE_W) *
+                        ((rows + 16 * LD_SOBEL_SR - 1) / (16 * LD_SOBEL_SR)) * frames;
+  return SobelCfg{tiles < sms ? 2 : LD_SOBEL_SR, 2, 2, SB_STAGE_CAP};
+}
 
 cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_count,
                          cudaStream_t stream) {
-  const SobelCfg c = sobel_cfg();
-  const int64_t max_ctas = static_cast<int64_t>(sm_count) * c.ctas_per_sm;
+  const int64_t max_ctas = static_cast<int64_t>(sm_count) * 2;
   const int n_ctas = static_cast<int>(p.n_tiles < max_ctas ? p.n_tiles : max_ctas);
+  if (p.sr == 2)
+    return p.binary != nullptr ? launch_cfg<2, 2, 2, true>(tmap, p, n_ctas, stream)
+                               : launch_cfg<2, 2, 2, false>(tmap, p, n_ctas, stream);
   return p.binary != nullptr ? launch_cfg<LD_SOBEL_SR, 2, 2, true>(tmap, p, n_ctas, stream)
                              : launch_cfg<LD_SOBEL_SR, 2, 2, false>(tmap, p, n_ctas, stream);
 }
