@@ -140,30 +140,34 @@ __constant__ uint32_t kNibbleBytes[16] = {
     0x00FFFF00u, 0x00FFFFFFu, 0xFF000000u, 0xFF0000FFu, 0xFF00FF00u, 0xFF00FFFFu,
     0xFFFF0000u, 0xFFFF00FFu, 0xFFFFFF00u, 0xFFFFFFFFu};
 
-// The edges of one 16-pixel row mask m (bit b <-> pixel x0 + b, value v0 + b)
-// at list positions pos .. pos+popc(m)-1 (any order: the list is a set, R15).
-// Four predicated slots (lowest, highest, then the lowest and highest of the
-// rest) cover a row with <= 4 edges without a data-dependent branch -- 98%
-// of rows at road densities -- so a warp does not run as many iterations as
-// its busiest lane; the rest go through a short loop.
+// The edges of two rows of 16 pixels at list positions pos .. pos+popc(m)-1
+// (any order: the list is a set, R15): m holds row y in bits 0..15 and row
+// y + 1 in bits 16..31 (pixel x0 + (b & 15)); the edge of bit b is
+// v0 + b + 65520 (b >> 4) = (y + (b >> 4)) << 16 | (x0 + (b & 15)).  Four
+// predicated slots (lowest, highest, then the lowest and highest of the rest)
+// cover a row pair with <= 4 edges without a data-dependent branch, so a
+// warp does not run as many iterations as its busiest lane; the rest go
+// through a short loop.  (One 16-bit row per word took 5.5 % more time on
+// cfg4, 2 % on cfg3: tools/ab_time.py, round 2.)
 template <typename Store>
-__device__ __forceinline__ uint32_t emit_row(uint32_t m, uint32_t v0, uint32_t pos, Store st) {
+__device__ __forceinline__ uint32_t emit_pair(uint32_t m, uint32_t v0, uint32_t pos, Store st) {
+  auto val = [&](uint32_t b) { return v0 + b + (b >> 4) * 65520u; };
   const uint32_t n = __popc(m);
-  const uint32_t ml = m & (m - 1u);             // without its lowest bit
-  const uint32_t b0 = __ffs(m) - 1u;            // lowest
-  const uint32_t b1 = 31u - __clz(ml);          // highest (n >= 2)
+  const uint32_t ml = m & (m - 1u);
+  const uint32_t b0 = __ffs(m) - 1u;
+  const uint32_t b1 = 31u - __clz(ml);
   const uint32_t m2 = n >= 2 ? ml ^ (1u << (b1 & 31u)) : 0u;
   const uint32_t m2l = m2 & (m2 - 1u);
-  const uint32_t b2 = __ffs(m2) - 1u;           // (n >= 3)
-  const uint32_t b3 = 31u - __clz(m2l);         // (n >= 4)
-  if (n >= 1) st(pos, v0 + b0);
-  if (n >= 2) st(pos + 1u, v0 + b1);
-  if (n >= 3) st(pos + 2u, v0 + b2);
-  if (n >= 4) st(pos + 3u, v0 + b3);
+  const uint32_t b2 = __ffs(m2) - 1u;
+  const uint32_t b3 = 31u - __clz(m2l);
+  if (n >= 1) st(pos, val(b0));
+  if (n >= 2) st(pos + 1u, val(b1));
+  if (n >= 3) st(pos + 2u, val(b2));
+  if (n >= 4) st(pos + 3u, val(b3));
   if (n > 4) {
     uint32_t r = m2l ^ (1u << (b3 & 31u)), q = pos + 4u;
     while (r) {
-      st(q++, v0 + (__ffs(r) - 1u));
+      st(q++, val(__ffs(r) - 1u));
       r &= r - 1u;
     }
   }
@@ -175,10 +179,11 @@ __device__ __forceinline__ uint32_t emit_row(uint32_t m, uint32_t v0, uint32_t p
 template <int SR, typename Store>
 __device__ __forceinline__ void emit_block(const uint32_t masks[SR], int ybase, int xs,
                                            uint32_t pos, Store st) {
+  static_assert(SR % 2 == 0, "rows go out in pairs");
 #pragma unroll
-  for (int i = 0; i < SR; ++i)
-    pos = emit_row(masks[i], (static_cast<uint32_t>(ybase + i) << 16) | static_cast<uint32_t>(xs),
-                   pos, st);
+  for (int i = 0; i < SR; i += 2)
+    pos = emit_pair(masks[i] | (masks[i + 1] << 16),
+                    (static_cast<uint32_t>(ybase + i) << 16) | static_cast<uint32_t>(xs), pos, st);
 }
 
 // Warp-specialised persistent kernel.  Warps 0..6 (224 threads = 14 column
