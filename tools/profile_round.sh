@@ -23,7 +23,10 @@ timeout 600 python bench.py --workload cfg4 --steps 10 --warmup 3 > $out/${tag}_
 for sh in band theta; do
   timeout 300 python bench.py --workload cfg5 --shard $sh --steps 10 --warmup 3 > $out/${tag}_bench_cfg5_$sh.jsonl 2> $out/${tag}_bench_cfg5_$sh.err; echo cfg5_$sh=$?
 done
-timeout 300 python bench.py --workload cfg2 --steps 20 --warmup 5 --no-e2e > $out/${tag}_bench_cfg2.jsonl 2> $out/${tag}_bench_cfg2.err; echo cfg2=$?
+for w in cfg1 cfg2; do
+  timeout 300 python bench.py --workload $w --steps 20 --warmup 5 > $out/${tag}_bench_$w.jsonl 2> $out/${tag}_bench_$w.err; echo $w=$?
+done
+timeout 300 python bench.py --workload cfg5 --steps 10 --warmup 3 > $out/${tag}_bench_cfg5.jsonl 2> $out/${tag}_bench_cfg5.err; echo cfg5=$?
 # ncu only after the same command exited 0 above (bench.py --profile: one stream, no extras)
 for w in cfg3 cfg4; do
   timeout 300 python bench.py --workload $w --profile --steps 1 --warmup 3 > /dev/null 2>&1 && \
