@@ -1038,14 +1038,24 @@ def test_pipelined_detector_matches_single_stream(ld, oracle):
     frames = [synth.gen_batch("cfg3", 8 * i, 8) for i in range(5)]
     pd = ld.PipelinedDetector(1280, 720, 8, cfg.n_theta, c, s, cfg.threshold, cfg.k,
                               cfg.half_theta, cfg.half_rho, cfg.min_votes, streams=3)
+    # more batches than slots in flight, no host synchronisation in between:
+    # each input is a fresh tensor dropped right after submit (the caching
+    # allocator may hand its block to the next allocation -- submit() must
+    # have recorded the slot's stream on it), and the outputs are copied on
+    # the current stream after the slot's event (a slot is reused 3 submits
+    # later, after this stream's copies: submit() orders it after them)
     outs = []
-    inputs = [cuda(f) for f in frames]  # 1280 is a multiple of 16: pitch == width
-    for g in inputs:
+    for f in frames:
+        g = cuda(f)  # 1280 is a multiple of 16: pitch == width
         pk, npk, cnt, ev = pd.submit(g)
-        ev.synchronize()
+        del g
+        junk = torch.full((8, 720, 1280), 255, dtype=torch.uint8, device="cuda")
+        del junk
+        torch.cuda.current_stream().wait_event(ev)
         outs.append((pk.clone(), npk.clone(), cnt.clone()))
+    torch.cuda.synchronize()
     for i, f in enumerate(frames):
-        ref = ld.detect_batch(inputs[i], cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
+        ref = ld.detect_batch(cuda(f), cfg.threshold, c, s, cfg.half_theta, cfg.half_rho,
                               cfg.min_votes, cfg.k, export_acc=False)
         torch.cuda.synchronize()
         assert torch.equal(outs[i][0], ref[0]) and torch.equal(outs[i][1], ref[1])

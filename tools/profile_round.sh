@@ -28,10 +28,12 @@ for w in cfg1 cfg2; do
 done
 timeout 300 python bench.py --workload cfg5 --steps 10 --warmup 3 > $out/${tag}_bench_cfg5.jsonl 2> $out/${tag}_bench_cfg5.err; echo cfg5=$?
 # ncu only after the same command exited 0 above (bench.py --profile: one stream, no extras)
-for w in cfg3 cfg4; do
-  timeout 300 python bench.py --workload $w --profile --steps 1 --warmup 3 > /dev/null 2>&1 && \
-  timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:ld:: -s 28 -c 10 \
-      -o $out/${tag}_prof_$w -f python bench.py --workload $w --profile --steps 1 --warmup 3 > $out/${tag}_ncu_$w.log 2>&1; echo ncu_$w=$?
+# (a --profile run launches 5 ld:: kernels per step after max(warmup, 4)
+# warm-up steps: skip 20, capture the next step whole)
+for w in cfg3 cfg4 cfg5; do
+  timeout 300 python bench.py --workload $w --profile --steps 3 --warmup 3 > /dev/null 2>&1 && \
+  timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:ld:: -s 20 -c 5 \
+      -o $out/${tag}_prof_$w -f python bench.py --workload $w --profile --steps 3 --warmup 3 > $out/${tag}_ncu_$w.log 2>&1; echo ncu_$w=$?
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $out/${tag}_launches.csv python bench.py --profile --steps 2 --warmup 3 > /dev/null 2>&1; echo launches=$?
