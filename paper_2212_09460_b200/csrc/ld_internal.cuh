@@ -21,7 +21,10 @@ constexpr int SB_CHUNKS = 14;       // 16-px output chunks per tile row
 constexpr int SB_TILE_W = SB_CHUNKS * 16;  // 224 output columns per tile
 constexpr int SB_STRIPS = 16;       // thread strips per tile (vertical)
 constexpr int SB_THREADS = SB_CHUNKS * SB_STRIPS;  // 224 = 7 consumer warps
-constexpr int SB_STAGE_CAP = 1024;  // per-warp edge staging buffer (uint32 entries)
+#ifndef LD_SOBEL_CAP
+#define LD_SOBEL_CAP 1024
+#endif
+constexpr int SB_STAGE_CAP = LD_SOBEL_CAP;  // per-warp edge staging buffer (uint32 entries)
 
 // launch configuration: SR output rows per strip (tile height 16*SR), TMA ring
 // depth, CTAs per SM, per-warp edge staging entries

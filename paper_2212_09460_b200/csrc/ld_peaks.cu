@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParam
 #define LD_PF_STATS 0
 #endif
 constexpr int PF_KEYS = 2048;   // range maxima sorted per frame (more are combined)
-constexpr int PF_QUEUE = 2048;  // hot chunks per pass
+constexpr int PF_QUEUE = 4096;  // hot chunks per pass
 constexpr int PF_SURV = 2048;   // prefilter survivors per pass
 static_assert(SP_CAP == 2048, "candidate list size");
 // dynamic shared memory: keys, candidates, survivors (u64) + queue (int)
@@ -556,7 +556,7 @@ template <int NT, int G, int MINB>
 __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams p) {
   constexpr int NW = NT / 32;
   constexpr int S = PF_KEYS / NT;
-  constexpr int WU = MINB > 1 ? 2 : 4;  // window-test vectors in flight per lane (register budget)
+  constexpr int WU = MINB > 1 ? 2 : 4;  // window-test vectors in flight per lane (register budget; 8 measured no faster)
   static_assert(NW <= 32, "one round: at most 32 keys");
   extern __shared__ __align__(16) unsigned char pf_smem[];
   u64 *keys = reinterpret_cast<u64 *>(pf_smem);  // sorted range maxima
@@ -651,10 +651,11 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
 #if LD_PF_STATS
   st_t1 = clock64();
 #endif
-  // rounds of RW keys in key order; key r0 + i is tested by warp i / G of the
+  // rounds of RW keys in key order (all the cluster's warps, at most the best
+  // L per round, at most 128); key r0 + i is tested by warp i / G of the
   // cluster's CTA i % G, the results read cluster-wide
-  constexpr int RW = NW * G < 32 ? NW * G : 32;
   int limit = 32 * m;  // keys[0..limit) are in key order
+  const int RW = min(min(NW * G, 128), limit);
   int par = 0;
   for (int r0 = 0; s_state == 0; r0 += RW, par ^= 1) {
 #if LD_PF_STATS
@@ -695,28 +696,38 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
     }
     pf_sync<G>();
     if (warp == 0) {
-      // key r0 + lane: warp lane / G of CTA lane % G; past RW: neutral
-      const int o = lane < RW ? *pf_at<G>(&s_ok[par][lane / G], lane % G) : 0;
-      const uint32_t endm = __ballot_sync(0xffffffffu, o < 0);
-      uint32_t okm = __ballot_sync(0xffffffffu, o > 0);
-      if (endm) okm &= (1u << (__ffs(endm) - 1)) - 1u;  // verified keys before the end
-      const int need = p.k - s_found;
-      const int c = __popc(okm);
-      if (c >= need) {  // the need-th verified key of this round sets the bound
-        const bool me = ((okm >> lane) & 1u) && __popc(okm & ((2u << lane) - 1u)) == need;
-        const uint32_t who = __ballot_sync(0xffffffffu, me);
-        okm &= (2u << (__ffs(who) - 1)) - 1u;  // up to and including it
-        if (lane == 0) {
-          s_tau = static_cast<uint32_t>(keys[r0 + __ffs(who) - 1] >> 32);
-          s_state = 1;
+      // the round's results 32 keys at a time, in key order, up to the decision
+      for (int c0 = 0; c0 < RW; c0 += 32) {
+        const int ii = c0 + lane;  // key r0 + ii: warp ii / G of CTA ii % G
+        const int o = ii < RW ? *pf_at<G>(&s_ok[par][ii / G], ii % G) : 0;
+        const uint32_t endm = __ballot_sync(0xffffffffu, o < 0);
+        uint32_t okm = __ballot_sync(0xffffffffu, o > 0);
+        if (endm) okm &= (1u << (__ffs(endm) - 1)) - 1u;  // verified keys before the end
+        const int need = p.k - s_found;
+        const int c = __popc(okm);
+        bool done = false;
+        if (c >= need) {  // the need-th verified key sets the bound
+          const bool me = ((okm >> lane) & 1u) && __popc(okm & ((2u << lane) - 1u)) == need;
+          const uint32_t who = __ballot_sync(0xffffffffu, me);
+          okm &= (2u << (__ffs(who) - 1)) - 1u;  // up to and including it
+          if (lane == 0) {
+            s_tau = static_cast<uint32_t>(keys[r0 + c0 + __ffs(who) - 1] >> 32);
+            s_state = 1;
+          }
+          done = true;
+        } else {
+          if (lane == 0) s_found += c;
+          done = endm != 0u;  // (keys past the list read as 0: an end)
+          if (done && lane == 0) s_state = 2;
         }
-      } else if (lane == 0) {
-        s_found += c;
-        if (endm || r0 + RW >= n2) s_state = 2;
+        // verified positions (rounds start at multiples of min(RW, 32))
+        if (lane == 0) s_vbits[(r0 + c0) >> 5] |= okm << ((r0 + c0) & 31);
+        __syncwarp();
+        if (done) break;
       }
       if (lane == 0) {
-        s_vbits[r0 >> 5] |= okm << (r0 & 31);  // RW divides 32: a round stays in one word
         s_last = r0 + RW;
+        if (s_state == 0 && r0 + RW >= n2) s_state = 2;
       }
     }
     __syncthreads();
@@ -752,28 +763,30 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
   const int q_lo = static_cast<int>(static_cast<int64_t>(p.n_seg) * rank / G);
   const int q_hi = static_cast<int>(static_cast<int64_t>(p.n_seg) * (rank + 1) / G);
   bool fail = false;  // CTA-uniform
-  constexpr int SCAN = 4 * NT;  // chunk maxima per pass, 4 loads in flight per thread
-  for (int base = q_lo; base < q_hi && !fail; base += SCAN) {
-    const int end = min(q_hi, base + SCAN);
-    uint32_t sv[4];
+  constexpr int SCAN = 8 * NT;  // chunk maxima per batch, 8 loads in flight per thread
+  static_assert(SCAN <= PF_QUEUE, "a batch never overflows an empty queue");
+  for (int base = q_lo; base < q_hi && !fail;) {
+    // queue the hot chunks of as many batches as the queue surely holds
+    // (usually the CTA's whole range: hot chunks are rare), then test them
+    do {
+      const int end = min(q_hi, base + SCAN);
+      uint32_t sv[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = base + u * NT + tid;
-      sv[u] = i < end ? __ldg(Sg + i) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (sv[u] >= tau) {
-        const int slot = atomicAdd(&s_nq, 1);
-        if (slot < PF_QUEUE) queue[slot] = base + u * NT + tid;
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * NT + tid;
+        sv[u] = i < end ? __ldg(Sg + i) : 0u;
       }
-    }
-    __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (sv[u] >= tau) {
+          const int slot = atomicAdd(&s_nq, 1);
+          if (slot < PF_QUEUE) queue[slot] = base + u * NT + tid;
+        }
+      }
+      base += SCAN;
+      __syncthreads();
+    } while (base < q_hi && s_nq + SCAN <= PF_QUEUE);
     const int nq = s_nq;
-    if (nq > PF_QUEUE) {
-      fail = true;  // tau is far too low for a sparse search
-      break;
-    }
 #if LD_PF_STATS
     if (tid == 0) st_hot += nq;
 #endif

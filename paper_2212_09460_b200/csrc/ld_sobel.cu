@@ -421,15 +421,19 @@ SobelCfg sobel_cfg(int width, int rows, int frames, int sms) {
   return SobelCfg{tiles < sms ? 2 : LD_SOBEL_SR, 2, 2, SB_STAGE_CAP};
 }
 
+#ifndef LD_SOBEL_MINB
+#define LD_SOBEL_MINB 2  // CTAs per SM (register budget 65536 / (288 * MINB))
+#endif
 cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_count,
                          cudaStream_t stream) {
-  const int64_t max_ctas = static_cast<int64_t>(sm_count) * 2;
+  constexpr int MB = LD_SOBEL_MINB;
+  const int64_t max_ctas = static_cast<int64_t>(sm_count) * MB;
   const int n_ctas = static_cast<int>(p.n_tiles < max_ctas ? p.n_tiles : max_ctas);
   if (p.sr == 2)
-    return p.binary != nullptr ? launch_cfg<2, 2, 2, true>(tmap, p, n_ctas, stream)
-                               : launch_cfg<2, 2, 2, false>(tmap, p, n_ctas, stream);
-  return p.binary != nullptr ? launch_cfg<LD_SOBEL_SR, 2, 2, true>(tmap, p, n_ctas, stream)
-                             : launch_cfg<LD_SOBEL_SR, 2, 2, false>(tmap, p, n_ctas, stream);
+    return p.binary != nullptr ? launch_cfg<2, 2, MB, true>(tmap, p, n_ctas, stream)
+                               : launch_cfg<2, 2, MB, false>(tmap, p, n_ctas, stream);
+  return p.binary != nullptr ? launch_cfg<LD_SOBEL_SR, 2, MB, true>(tmap, p, n_ctas, stream)
+                             : launch_cfg<LD_SOBEL_SR, 2, MB, false>(tmap, p, n_ctas, stream);
 }
 
 }  // namespace ld
