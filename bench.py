@@ -77,6 +77,9 @@ def parse():
                          "float64 mode (a second workload, no peak hint)")
     ap.add_argument("--streams", type=int, default=4,
                     help="streams (each with its own buffers) the steps go to round-robin")
+    ap.add_argument("--graph", default="on", choices=["on", "off"],
+                    help="replay each stream's step as a captured CUDA graph in the timed "
+                         "loop (the host launch cost of small batches leaves the GPU idle)")
     ap.add_argument("--no-hint", action="store_true",
                     help="plain ld_hough_accumulate + ld_hough_peaks (no peak hint)")
     ap.add_argument("--shard", default="band", choices=["band", "theta"],
@@ -506,8 +509,8 @@ def run_batch(args, rank, world, dist):
     bufs = [Buffers(stream if i == 0 else torch.cuda.Stream()) for i in range(args.streams)]
     launches = [0]
 
-    def step(bf, ev=None):
-        st = bf.stream
+    def step(bf, ev=None, st=None):
+        st = bf.stream if st is None else st
         if ev is not None:
             ev[0].record(st)
         ld.ld_sobel_binarize(gray, img, cfg.threshold, None, bf.edges, stride, bf.counts, st)
@@ -550,6 +553,34 @@ def run_batch(args, rank, world, dist):
             print(json.dumps({"profile_run": True, "votes": votes}), flush=True)
         return
 
+    # each buffer set's step captured once as a CUDA graph (the library
+    # enqueues without host synchronisation); replays run it with one launch
+    graphs = []
+    if args.graph == "on":
+        cap = torch.cuda.Stream()  # (capture needs a non-default stream; replays
+        for bf in bufs:            # then run on each buffer set's own stream)
+            g = torch.cuda.CUDAGraph()
+            launches[0] = 0
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g, stream=cap):
+                step(bf, st=cap)
+            graphs.append((g, launches[0]))
+        torch.cuda.synchronize()
+
+    def run_step(i):
+        bf = bufs[i % len(bufs)]
+        if graphs:
+            g, n = graphs[i % len(bufs)]
+            with torch.cuda.stream(bf.stream):
+                g.replay()
+            launches[0] += n
+        else:
+            step(bf)
+
+    for i in range(len(bufs)):
+        run_step(i)
+    torch.cuda.synchronize()
+
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -565,7 +596,7 @@ def run_batch(args, rank, world, dist):
     for bf in bufs[1:]:
         bf.stream.wait_event(e_start)
     for i in range(args.steps):
-        step(bufs[i % len(bufs)])
+        run_step(i)
     for bf in bufs[1:]:
         j = torch.cuda.Event()
         j.record(bf.stream)
@@ -643,6 +674,7 @@ def run_batch(args, rank, world, dist):
                                    "frame-shard dp%d (%s)" % (world, scaling)),
                    "dist_backend": args.dist_backend if world > 1 else None,
                    "peak_hint": use_hint, "trig": args.trig, "streams": args.streams,
+                   "cuda_graph_steps": bool(graphs),
                    "ms_per_step_one_stream": serial_ms,
                    "l2": "inputs %.0f MB + accumulators %.0f MB per GPU vs L2 %.0f MB; no flush"
                          % (B * H * pitch / 1e6, B * cfg.n_theta * n_rho * 4 / 1e6,
