@@ -37,6 +37,9 @@ namespace ld {
 #ifndef LD_HV_UNROLL
 #define LD_HV_UNROLL 4  // band rows per unrolled step (plain kernel)
 #endif
+#ifndef LD_HV_CTAS_MAX
+#define LD_HV_CTAS_MAX 2  // experiment: 1 = always one CTA per SM (taller bands)
+#endif
 #ifndef LD_HV_PAIR_UNROLL
 #define LD_HV_PAIR_UNROLL 2  // pairs per unrolled step (paired kernel)
 #endif
@@ -272,7 +275,8 @@ int hough_plan(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *rpb, i
   const int r1 = rows_per_band(n_theta, n_rho, smem_optin - fixed, &nb1);
   if (r1 < 1) return 0;
   const int r2 = rows_per_band(n_theta, n_rho, smem_optin / 2 - fixed, &nb2);
-  const bool two = r2 >= 8 && (smem_optin - fixed) / (static_cast<size_t>(n_rho) * 4u) >= 16;
+  const bool two = LD_HV_CTAS_MAX > 1 && r2 >= 8 &&
+                   (smem_optin - fixed) / (static_cast<size_t>(n_rho) * 4u) >= 16;
   *ctas = two ? 2 : 1;
   *rpb = two ? r2 : r1;
   *n_bands = two ? nb2 : nb1;
@@ -536,7 +540,7 @@ int hough_plan_pairs(int n_theta, int n_rho, size_t smem_optin, int *ctas, int *
   const int p1 = plan(smem_optin - fixed, &nb1);
   if (p1 < 1) return 0;
   const int p2 = plan(smem_optin / 2 - fixed, &nb2);
-  const bool two = p2 >= 4 && p1 >= 8;
+  const bool two = LD_HV_CTAS_MAX > 1 && p2 >= 4 && p1 >= 8;
   *ctas = two ? 2 : 1;
   *ppb = two ? p2 : p1;
   *n_bands = two ? nb2 : nb1;
