@@ -594,14 +594,19 @@ cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int 
   if (cluster > 1) {
     const int gi = cluster == 8 ? 3 : cluster == 4 ? 2 : 1;
     AttrOnce &a = g_pairs_cl_attr[ctas][gi];
-    if (ctas == 2) {
-      if (cluster == 8) return launch_pairs_cluster<2, 8>(p, trig, smem_bytes, stream, a);
-      if (cluster == 4) return launch_pairs_cluster<2, 4>(p, trig, smem_bytes, stream, a);
-      return launch_pairs_cluster<2, 2>(p, trig, smem_bytes, stream, a);
-    }
-    if (cluster == 8) return launch_pairs_cluster<1, 8>(p, trig, smem_bytes, stream, a);
-    if (cluster == 4) return launch_pairs_cluster<1, 4>(p, trig, smem_bytes, stream, a);
-    return launch_pairs_cluster<1, 2>(p, trig, smem_bytes, stream, a);
+    cudaError_t e;
+    if (ctas == 2)
+      e = cluster == 8 ? launch_pairs_cluster<2, 8>(p, trig, smem_bytes, stream, a)
+        : cluster == 4 ? launch_pairs_cluster<2, 4>(p, trig, smem_bytes, stream, a)
+                       : launch_pairs_cluster<2, 2>(p, trig, smem_bytes, stream, a);
+    else
+      e = cluster == 8 ? launch_pairs_cluster<1, 8>(p, trig, smem_bytes, stream, a)
+        : cluster == 4 ? launch_pairs_cluster<1, 4>(p, trig, smem_bytes, stream, a)
+                       : launch_pairs_cluster<1, 2>(p, trig, smem_bytes, stream, a);
+    if (e != cudaErrorLaunchOutOfResources && e != cudaErrorInvalidClusterSize) return e;
+    // no room for the cluster (a partitioned or shared GPU): the per-band
+    // kernel computes the same accumulator and hint
+    cudaGetLastError();
   }
   auto kern = ctas == 2 ? hough_vote_pairs_kernel<2, 1> : hough_vote_pairs_kernel<1, 1>;
   cudaError_t e = ensure_smem_attr(g_pairs_attr[ctas], kern, -(227 * 1024 / ctas));

@@ -1924,9 +1924,12 @@ static cudaError_t launch_fused_g(const PeaksParams &p, AttrOnce &attr, cudaStre
 static cudaError_t launch_fused(const PeaksParams &p, int sms, cudaStream_t stream) {
   if (p.batch >= sms) return launch_fused_g<512, 1, 2>(p, g_fused_attr[0], stream);
   const int per = sms / p.batch;
-  if (per >= 8) return launch_fused_g<512, 8, 1>(p, g_fused_attr[4], stream);
-  if (per >= 4) return launch_fused_g<512, 4, 1>(p, g_fused_attr[3], stream);
-  if (per >= 2) return launch_fused_g<512, 2, 1>(p, g_fused_attr[2], stream);
+  cudaError_t e = cudaErrorInvalidClusterSize;
+  if (per >= 8) e = launch_fused_g<512, 8, 1>(p, g_fused_attr[4], stream);
+  else if (per >= 4) e = launch_fused_g<512, 4, 1>(p, g_fused_attr[3], stream);
+  else if (per >= 2) e = launch_fused_g<512, 2, 1>(p, g_fused_attr[2], stream);
+  if (e != cudaErrorLaunchOutOfResources && e != cudaErrorInvalidClusterSize) return e;
+  cudaGetLastError();  // no room for a cluster (or none asked for): one CTA per frame
   return launch_fused_g<512, 1, 1>(p, g_fused_attr[1], stream);
 }
 
