@@ -290,7 +290,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+// (bar_s: the barrier's shared-memory address, for loops that hoist it)
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar_s) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar_s, uint32_t parity) {
   // try_wait with a suspend-time hint: the waiting thread sleeps in hardware
   // until the phase completes (or the hint expires) instead of spinning on
   // the issue slots other warps need
@@ -298,9 +303,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "{\n\t.reg .pred p;\n"
       "LD_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 0x989680;\n\t"
-      "@!p bra LD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "@!p bra LD_WAIT_%=;\n}" ::"r"(bar_s),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  mbar_wait_s(smem_u32(bar), parity);
 }
 
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,

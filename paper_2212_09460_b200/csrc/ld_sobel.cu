@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
   }
 
   // ---------------- consumer warps
+  const uint32_t full_s = smem_u32(full_bar), empty_s = smem_u32(empty_bar);
   const int chunk = tid % SB_CHUNKS;
   const int strip = tid / SB_CHUNKS;
   const uint32_t k0 = static_cast<uint32_t>(32768 - p.t2) * 0x00010001u;
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
   int it = 0;
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const int stage = it % STAGES;
-    mbar_wait(&full_bar[stage], (it / STAGES) & 1);
+    mbar_wait_s(full_s + 8u * stage, (it / STAGES) & 1);
     const int4 ti = tile_info[stage];
     const int f = ti.x;
     const int xs = ti.z + chunk * 16;     // first column of this thread's chunk
@@ -337,6 +338,9 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
     uint32_t masks[SR];
 #pragma unroll
     for (int i = 0; i < SR; ++i) masks[i] = 0u;
+    // every row of the strip inside the output rows (all but the frame's top
+    // and bottom strips): no per-row test
+    const bool rows_in = ybase >= ylo_g && ybase + SR - 1 <= yhi_g;
     if (ybase < p.row_end && xs < p.width) {  // skip strips/chunks outside the image
       RowP r0, r1, r2;
       load_row(buf, r0);
@@ -346,11 +350,11 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
         load_row(buf + (i + 2) * SB_BOX_W, r2);
         const int y = ybase + i;
         const uint32_t m = sobel_row(r0, r1, r2, k0, k2, colmask);
-        masks[i] = (y >= ylo_g && y <= yhi_g) ? m : 0u;
+        masks[i] = m;
         if (WB && y < p.row_end && xs < p.width) {
           uint8_t *dst = p.binary + static_cast<int64_t>(f) * p.bin_frame_stride +
                          static_cast<int64_t>(y - p.row_begin) * p.bin_pitch + xs;
-          const uint32_t mm = masks[i];
+          const uint32_t mm = (y >= ylo_g && y <= yhi_g) ? m : 0u;
           *reinterpret_cast<uint4 *>(dst) =
               make_uint4(kNibbleBytes[mm & 15u], kNibbleBytes[(mm >> 4) & 15u],
                          kNibbleBytes[(mm >> 8) & 15u], kNibbleBytes[(mm >> 12) & 15u]);
@@ -358,9 +362,14 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
         r0 = r1;
         r1 = r2;
       }
+      if (!rows_in) {  // the frame's top / bottom strips: rows outside the output rows
+#pragma unroll
+        for (int i = 0; i < SR; ++i)
+          if (ybase + i < ylo_g || ybase + i > yhi_g) masks[i] = 0u;
+      }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[stage]);  // stage consumed by this warp
+    if (lane == 0) mbar_arrive_s(empty_s + 8u * stage);  // stage consumed by this warp
 
     // warp-level reservation of this tile's slice, scanned in rank order
     uint32_t cnt = 0;
