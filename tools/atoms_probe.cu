@@ -18,8 +18,13 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// -DADD_VAL=65536: the increment of a 16-bit counter in a word's high half
+// (SASS ATOMS.ADD with a register operand instead of ATOMS.POPC.INC)
+#ifndef ADD_VAL
+#define ADD_VAL 1
+#endif
 __device__ __forceinline__ void red_add(uint32_t a) {
-  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a) : "memory");
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "n"(ADD_VAL) : "memory");
 }
 
 __global__ void probe(int mode, int iters, unsigned long long *cyc, uint32_t *sink) {
