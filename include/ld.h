@@ -226,14 +226,18 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
  * the candidate definition above (a full window test on acc): verified cells
  * are distinct candidates, so the value of the k-th verified one is a lower
  * bound on the frame's k-th best candidate, and the search starts from it
- * instead of min_votes.  While each band is in shared memory the voting
- * kernel also records the maximum of every 32-cell segment of every row; with
- * a certified bound the search then only reads those maxima and tests the
- * cells of the segments that reach the bound (the sparse search, DESIGN R30),
- * falling back to the full search for a frame whose bound is not certified.
- * peaks / n_peaks are bit-identical to ld_hough_peaks.  The hint must come from the ld_hough_accumulate_hint call
- * that produced acc; a hint whose header (written by that call) does not
- * match batch, n_theta and n_rho is ignored.
+ * instead of min_votes (a recorded cell also has to hold its recorded value).
+ * While each band is in shared memory the voting kernel also records the
+ * maximum of every 1 KB chunk (256 counters) of the accumulator's memory;
+ * with a certified bound the search then only reads those maxima and tests
+ * the cells of the chunks that reach it (the sparse search, DESIGN R30) --
+ * bound, sparse search and top k in one kernel per frame -- and falls back to
+ * the full search for a frame whose bound is not certified.  peaks / n_peaks
+ * are bit-identical to ld_hough_peaks.  The hint must come from the
+ * ld_hough_accumulate_hint call that produced acc; a hint whose header
+ * (written by that call) does not match batch, n_theta and n_rho is ignored,
+ * and the chunk maxima are used only for acc at the address that call wrote
+ * (a copy of acc elsewhere gets the full search).
  *  hint : device, >= ld_hough_hint_bytes(batch, width, height, n_theta),
  *         16-B aligned; fully owned by the library between the two calls. */
 size_t ld_hough_hint_bytes(int32_t batch, int32_t width, int32_t height, int32_t n_theta);
