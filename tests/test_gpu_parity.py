@@ -743,6 +743,41 @@ def test_hinted_peaks_ties_and_sparse(ld, oracle, seed, k):
         _hint_case(ld, oracle, frames, cfg)
 
 
+@pytest.mark.parametrize("k", [64, 256, 1024])
+def test_hinted_peaks_large_k(ld, oracle, k):
+    # k past the best 32 m keys the fused search selects first (the full-sort
+    # continuation), and past what the hint can certify (dense fallback), on
+    # road frames with min_votes 1 (thousands of local maxima)
+    cfg = synth.CONFIGS["cfg3"]
+    frames = synth.gen_batch("cfg3", 3, 2)
+    cfg = synth.Config("k%d" % k, 1280, 720, 2, cfg.threshold, cfg.n_theta, k, cfg.half_theta,
+                       cfg.half_rho)
+    _hint_case(ld, oracle, frames, cfg)
+
+
+def test_hint_of_another_accumulator(ld, oracle):
+    # a hint recorded while voting frame A, used with frame B's accumulator
+    # of the same shape at another address: the header matches, the chunk
+    # maxima are not used (other address) and A's keys are verified against
+    # B's counts (a key must hold its value there) -- B's exact peaks
+    cfg = synth.CONFIGS["cfg2"]
+    c, s = synth.q15_table(cfg.n_theta)
+    fa = synth.gen_frame("cfg2", 0)[None]
+    fb = synth.gen_batch("cfg3", 11, 1)
+    _, ea, ca, sa = ld.sobel_binarize(cuda(fa), cfg.threshold, want_binary=False)
+    _, eb, cb, sb = ld.sobel_binarize(cuda(fb), cfg.threshold, want_binary=False)
+    _, hint_a = ld.hough_accumulate(ea, ca, sa, 1280, 720, c, s, want_hint=True)
+    acc_b = ld.hough_accumulate(eb, cb, sb, 1280, 720, c, s)
+    p1, n1 = ld.hough_peaks(acc_b, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k, hint=hint_a)
+    p0, n0 = ld.hough_peaks(acc_b, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+    torch.cuda.synchronize()
+    assert torch.equal(p0, p1) and torch.equal(n0, n1)
+    A = acc_b.cpu().numpy().view(np.uint32)
+    pk, npk = oracle.hough_peaks(A[0], cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+    assert int(n1.cpu()[0]) == npk
+    assert peak_tuples(p1.cpu().numpy()[0]) == oracle_peak_tuples(pk)
+
+
 def test_hint_header_mismatch_ignored(ld, oracle):
     cfg = synth.CONFIGS["cfg2"]
     frames = synth.gen_frame("cfg2", 0)[None]
