@@ -264,6 +264,20 @@ static int hough_impl(const uint32_t *edge_xy, const uint32_t *edge_count, int64
   if (!paired &&
       !hough_plan(n_theta, n_rho, static_cast<size_t>(dev.smem_optin), &ctas, &rpb, &n_bands, &smem))
     return fail(LD_ERR_UNSUPPORTED, "one accumulator row (%d bins) exceeds shared memory", n_rho);
+// Launches too small to fill the GPU (single frames): one pair per band, so
+// the frame's bands alone give more CTAs -- each streams the whole edge list
+// for two rows, with no cluster reduction (cfg2 voting 18.4 -> 14.3 us, cfg1
+// 11.7 -> 5.6 us; cfg2 frames/s +13 % with 4 streams; DESIGN 6.2).  The
+// cluster split (below) still applies when even one-pair bands are too few.
+#ifndef LD_HV_SMALL_PPB
+#define LD_HV_SMALL_PPB 1
+#endif
+  if (LD_HV_SMALL_PPB > 0 && paired && 2 * static_cast<int64_t>(batch) * n_bands <= dev.sm_count &&
+      rpb > LD_HV_SMALL_PPB) {
+    rpb = LD_HV_SMALL_PPB;
+    n_bands = (hough_pair_count(n_theta) + rpb - 1) / rpb;
+    smem = ((static_cast<size_t>(rpb) * n_rho * 8u + 15) / 16) * 16 + 64;
+  }
   static thread_local TrigTable trig;  // 16 KB: keep it off the stack
   memcpy(trig.c, cos_q15, sizeof(int32_t) * n_theta);
   memcpy(trig.s, sin_q15, sizeof(int32_t) * n_theta);

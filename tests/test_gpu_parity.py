@@ -1121,13 +1121,17 @@ def test_detect_is_cuda_graph_capturable(ld):
     assert torch.equal(det.counts, ref[2])
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
-def test_vote_cluster_split_equals_single_cta(ld, oracle, name):
-    """Single frames vote through thread-block clusters (a band's edges split
-    over the cluster's CTAs, copies summed over distributed shared memory):
-    the accumulator, the chunk maxima and the hinted peaks equal the one-CTA-
-    per-band path and the oracle."""
+@pytest.mark.parametrize("name,n_theta", [("cfg1", 16), ("cfg2", 32), ("cfg2", 48), ("cfg1", 180)])
+def test_vote_cluster_split_equals_single_cta(ld, oracle, name, n_theta):
+    """Launches whose one-pair bands still leave most SMs idle (single frames
+    with few theta bins) vote through thread-block clusters (a band's edges
+    split over the cluster's CTAs, copies summed over distributed shared
+    memory): the accumulator, the chunk maxima and the hinted peaks equal the
+    one-CTA-per-band path and the oracle.  (A full 180-bin table on a single
+    frame fills the GPU with one-pair bands: no cluster.)"""
     cfg = synth.CONFIGS[name]
+    cfg = synth.Config(cfg.name, cfg.width, cfg.height, 1, cfg.threshold, n_theta, cfg.k,
+                       cfg.half_theta, cfg.half_rho)
     c, s = synth.q15_table(cfg.n_theta)
     img = synth.gen_frame(name, 0)
     _, edges, counts, stride = ld.sobel_binarize(cuda(img[None]), cfg.threshold,
@@ -1138,6 +1142,10 @@ def test_vote_cluster_split_equals_single_cta(ld, oracle, name):
                                    flags=ld.LD_VOTE_NO_CLUSTER)
     torch.cuda.synchronize()
     assert torch.equal(a_cl, a_1)
+    # hint header word 5 = keys per band: one per CTA of a cluster (G = 8
+    # here), one per warp (16) without
+    kpb = int(h_cl[:64].view(torch.int32)[5].item()), int(h_1[:64].view(torch.int32)[5].item())
+    assert kpb == ((16, 16) if n_theta == 180 else (8, 16)), kpb
     want = oracle.hough_accumulate(oracle.compact(oracle.sobel_binarize(img, cfg.threshold)),
                                    w, h, c, s)
     assert np.array_equal(a_cl.cpu().numpy().view(np.uint32)[0], want)
