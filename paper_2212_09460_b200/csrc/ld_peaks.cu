@@ -597,14 +597,16 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
 #endif
 
   // ---- 1. the bound
-  // more keys than the sort holds: combine g consecutive ranges (the maximum
-  // of a union of ranges is a cell of the accumulator all the same)
-  const int g = (n_src + PF_KEYS - 1) / PF_KEYS;
-  const int n = n_src > 0 ? (n_src + g - 1) / g : 0;
   // the keys are verified in key order from the best L = 32 m (m from k: the
   // k-th verified key sat within the best 2k on the road workloads); past
   // them, all n are sorted and the rounds go on
   const int m = p.k <= 16 ? 1 : p.k <= 32 ? 2 : 4;
+  // more keys than the selection takes (2048; 512 for k <= 16, where the
+  // best 32 decide): combine g consecutive ranges (the maximum of a union of
+  // ranges is a cell of the accumulator all the same)
+  const int cap = m == 1 ? 512 : PF_KEYS;
+  const int g = (n_src + cap - 1) / cap;
+  const int n = n_src > 0 ? (n_src + g - 1) / g : 0;
   int n2 = 32 * m;
   while (n2 < n) n2 <<= 1;
   const u64 *src = p.hint_keys + static_cast<int64_t>(f) * n_src;
