@@ -556,8 +556,9 @@ template <int NT, int G, int MINB>
 __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams p) {
   constexpr int NW = NT / 32;
   constexpr int S = PF_KEYS / NT;
-  constexpr int WU = MINB > 1 ? 2 : 4;  // window-test vectors in flight per lane (register budget; 8 measured no faster)
-  static_assert(NW <= 32, "one round: at most 32 keys");
+  // window-test vectors in flight per lane (the register budget; 8 measured no faster)
+  constexpr int WU = MINB > 1 ? 2 : 4;
+  static_assert(NW <= 32, "warp 0 reads one result per lane of each 32-key chunk");
   extern __shared__ __align__(16) unsigned char pf_smem[];
   u64 *keys = reinterpret_cast<u64 *>(pf_smem);  // sorted range maxima
   u64 *cand = keys + PF_KEYS;                     // candidate keys (CTA 0)

@@ -2,8 +2,8 @@
 # Standard measurement of one round, run on the GPU box from the repo root:
 #   /usr/local/graft/bin/gpurun --timeout 2700 -- 'bash tools/profile_round.sh r02x'
 # Writes gpurun_out/<tag>_*: smoke, GPU tests, default bench line, reference
-# arm, cfg4/cfg5 lines, a full ncu capture of one serialised step per config
-# (cfg3, cfg4) and the cfg3 launch list, and an ncu capture of the B5 kernel.
+# arm, cfg1/cfg2/cfg4/cfg5 lines, the cfg3 launch list and an ncu capture of
+# the B5 kernel (the full captures per config: tools/ncu_round.sh).
 # Summarise afterwards (no GPU needed):
 #   python tools/ncu_summary.py gpurun_out/<tag>_prof.ncu-rep gpurun_out/<tag>_launches.csv
 #   python tools/ncu_summary.py --traffic cfg3 gpurun_out/<tag>_prof.ncu-rep
@@ -24,17 +24,12 @@ for sh in band theta; do
   timeout 300 python bench.py --workload cfg5 --shard $sh --steps 10 --warmup 3 > $out/${tag}_bench_cfg5_$sh.jsonl 2> $out/${tag}_bench_cfg5_$sh.err; echo cfg5_$sh=$?
 done
 for w in cfg1 cfg2; do
-  timeout 300 python bench.py --workload $w --steps 20 --warmup 5 > $out/${tag}_bench_$w.jsonl 2> $out/${tag}_bench_$w.err; echo $w=$?
+  timeout 300 python bench.py --workload $w --steps 200 --warmup 5 > $out/${tag}_bench_$w.jsonl 2> $out/${tag}_bench_$w.err; echo $w=$?
 done
 timeout 300 python bench.py --workload cfg5 --steps 10 --warmup 3 > $out/${tag}_bench_cfg5.jsonl 2> $out/${tag}_bench_cfg5.err; echo cfg5=$?
-# ncu only after the same command exited 0 above (bench.py --profile: one stream, no extras)
-# (a --profile run launches 5 ld:: kernels per step after max(warmup, 4)
-# warm-up steps: skip 20, capture the next step whole)
-for w in cfg3 cfg4 cfg5; do
-  timeout 300 python bench.py --workload $w --profile --steps 3 --warmup 3 > /dev/null 2>&1 && \
-  timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:ld:: -s 20 -c 5 \
-      -o $out/${tag}_prof_$w -f python bench.py --workload $w --profile --steps 3 --warmup 3 > $out/${tag}_ncu_$w.log 2>&1; echo ncu_$w=$?
-done
+# the full ncu captures (~20 MB each) go in separate calls so that each call's
+# gpurun_out stays under gpurun's 64 MiB copy-back limit:
+#   gpurun -- 'bash tools/ncu_round.sh <tag> cfg3'; ... 'bash tools/ncu_round.sh <tag> "cfg4 cfg5"'
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $out/${tag}_launches.csv python bench.py --profile --steps 2 --warmup 3 > /dev/null 2>&1; echo launches=$?
 timeout 300 ncu --set full --clock-control none -k regex:smem_atomic -o $out/${tag}_b5 -f \
