@@ -252,10 +252,30 @@ int ld_hough_peaks_hinted(const uint32_t *acc, int32_t batch, int32_t n_theta, i
                           int32_t *n_peaks, void *workspace, size_t workspace_bytes,
                           void *stream);
 
+/* The peak hint of an accumulator that did not come out of one
+ * ld_hough_accumulate_hint call -- a sum of partial accumulators after an
+ * all_reduce (row-band multi-GPU), a theta shard voted with a slice of the
+ * table -- by one read of acc (DESIGN R25, R30): the maximum of every 1 KB
+ * chunk of acc's memory and, as range maxima, the best counter of each group
+ * of consecutive chunks among candidate rows [cand_row_begin, cand_row_end).
+ * Same layout, header and use as the hint of ld_hough_accumulate_hint
+ * (ld_hough_peaks_hinted, or ld_hough_peaks_opt with the same candidate rows);
+ * it describes acc at this address.  Stream-ordered, no host sync.
+ *  acc  : device [batch][n_theta][n_rho] uint32, 4-byte aligned, read only;
+ *         n_theta * n_rho < 2^31.
+ *  hint : device, >= the ld_hough_hint_bytes of this shape (n_rho =
+ *         2 ld_rho_offset(width, height) + 1), 16-B aligned; overwritten.
+ * Errors: LD_ERR_INVALID_ARG (NULL pointer, bad shape or rows),
+ * LD_ERR_WORKSPACE (hint too small or misaligned). */
+int ld_hough_hint_from_acc(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                           int32_t cand_row_begin, int32_t cand_row_end, void *hint,
+                           size_t hint_bytes, void *stream);
+
 /* The peak search with every option (ld_hough_peaks, _ex and _hinted are
  * this call with defaults): candidate rows and theta offset as
- * ld_hough_peaks_ex; hint nullable (as ld_hough_peaks_hinted; ignored for a
- * restricted row range); flags select the search kernels -- every choice
+ * ld_hough_peaks_ex; hint nullable (as ld_hough_peaks_hinted; with a
+ * restricted row range its keys outside the rows are not used and the sparse
+ * search covers those rows only); flags select the search kernels -- every choice
  * returns the same peaks:
  *  LD_PEAKS_DENSE        : no sparse search (DESIGN R30) even with a hint
  *  LD_PEAKS_FORCE_STREAM : the CTA streaming kernel instead of the warp kernel

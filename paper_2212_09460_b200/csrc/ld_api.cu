@@ -616,6 +616,32 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
                             n_peaks, workspace, workspace_bytes, stream);
 }
 
+int ld_hough_hint_from_acc(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
+                           int32_t cand_row_begin, int32_t cand_row_end, void *hint,
+                           size_t hint_bytes_, void *stream) {
+  g_launches = 0;
+  if (!acc || !hint) return fail(LD_ERR_INVALID_ARG, "NULL acc/hint");
+  if (batch < 1 || n_theta < 1 || n_theta > LD_MAX_THETA || n_rho < 1)
+    return fail(LD_ERR_INVALID_ARG, "bad accumulator shape [%d][%d][%d]", batch, n_theta, n_rho);
+  if (static_cast<int64_t>(n_theta) * n_rho >= (1ll << 31))
+    return fail(LD_ERR_INVALID_ARG, "a frame of %d x %d counters exceeds 2^31", n_theta, n_rho);
+  if (cand_row_begin < 0 || cand_row_end < cand_row_begin || cand_row_end > n_theta)
+    return fail(LD_ERR_INVALID_ARG, "candidate rows [%d, %d) outside [0, %d]", cand_row_begin,
+                cand_row_end, n_theta);
+  if (!aligned(acc, 4)) return fail(LD_ERR_INVALID_ARG, "acc not 4-byte aligned");
+  if (!aligned(hint, 16) || hint_bytes_ < hint_bytes(batch, n_theta, n_rho))
+    return fail(LD_ERR_WORKSPACE, "hint needs %zu bytes, 16-byte aligned",
+                hint_bytes(batch, n_theta, n_rho));
+  DevInfo dev;
+  int rc = device_info(&dev);
+  if (rc) return rc;
+  const cudaError_t e = launch_hint_from_acc(acc, batch, n_theta, n_rho, cand_row_begin,
+                                             cand_row_end, hint, hint_keys_bytes(batch, n_theta),
+                                             static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "hint_from_acc_kernel launch");
+  return LD_OK;
+}
+
 int ld_hough_peaks_hinted(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
                           int32_t half_theta, int32_t half_rho, uint32_t min_votes, int32_t k,
                           const void *hint, size_t hint_bytes_, ld_peak *peaks, int32_t *n_peaks,

@@ -171,6 +171,10 @@ PeaksLayout peaks_layout(int batch, int n_theta, int n_rho, int k);
 size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k);
 // flags: LD_PEAKS_* of ld.h
 cudaError_t launch_peaks(const PeaksParams &p, uint32_t flags, cudaStream_t stream);
+// the peak hint of an existing accumulator (keys_bytes: the hint's key region)
+cudaError_t launch_hint_from_acc(const uint32_t *acc, int batch, int n_theta, int n_rho,
+                                 int cand_t0, int cand_t1, void *hint, size_t keys_bytes,
+                                 cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // NEXT 3: lanes module (ld_lanes.cu)

@@ -685,7 +685,8 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
         const uint32_t probe = __ldg(A + idx);
         long long l1 = clock64() + (probe == 0xFFFFFFFFu ? 1 : 0);
 #endif
-        ok = (t < n_theta &&
+        // (a cell outside the candidate rows is no candidate of this search)
+        ok = (t >= p.cand_t0 && t < p.cand_t1 &&
               warp_window_max<WU, false>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane)) ? 1 : 0;
 #if LD_PF_STATS
         long long l2 = clock64();
@@ -763,8 +764,13 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
       if ((s_vbits[i >> 5] >> (i & 31)) & 1u) cand[atomicAdd(&s_ncand, 1)] = keys[i];
   const uint32_t *Sg = p.segmax + static_cast<int64_t>(f) * p.n_seg;
   const uintptr_t c0 = reinterpret_cast<uintptr_t>(A) / SEG_BYTES;
-  const int q_lo = static_cast<int>(static_cast<int64_t>(p.n_seg) * rank / G);
-  const int q_hi = static_cast<int>(static_cast<int64_t>(p.n_seg) * (rank + 1) / G);
+  // the chunks of the candidate rows [cand_t0, cand_t1), split over the cluster
+  const int64_t rc0 = static_cast<int64_t>(p.cand_t0) * n_rho, rc1 = static_cast<int64_t>(p.cand_t1) * n_rho;
+  const uintptr_t a_addr = reinterpret_cast<uintptr_t>(A);
+  const int qa = static_cast<int>((a_addr + 4 * rc0) / SEG_BYTES - c0);
+  const int qb = rc1 > rc0 ? static_cast<int>((a_addr + 4 * (rc1 - 1)) / SEG_BYTES - c0) + 1 : qa;
+  const int q_lo = qa + static_cast<int>(static_cast<int64_t>(qb - qa) * rank / G);
+  const int q_hi = qa + static_cast<int>(static_cast<int64_t>(qb - qa) * (rank + 1) / G);
   bool fail = false;  // CTA-uniform
   constexpr int SCAN = 8 * NT;  // chunk maxima per batch, 8 loads in flight per thread
   static_assert(SCAN <= PF_QUEUE, "a batch never overflows an empty queue");
@@ -807,8 +813,8 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
 #pragma unroll
       for (int step = 0; step < STEPS; ++step) {
         const uint32_t v = vv[step];
-        if (v >= tau) {
-          const int64_t cell = w0 + step * 32 + lane;
+        const int64_t cell = w0 + step * 32 + lane;
+        if (v >= tau && cell >= rc0 && cell < rc1) {
           const int t = static_cast<int>(cell / n_rho);
           const int r = static_cast<int>(cell - static_cast<int64_t>(t) * n_rho);
           const u64 key = mk_key(v, static_cast<uint32_t>(cell));
@@ -898,7 +904,7 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
     const u64 key = cand[i];
     const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
     ld_peak pk;
-    pk.theta_bin = static_cast<int32_t>(idx / static_cast<uint32_t>(n_rho));
+    pk.theta_bin = static_cast<int32_t>(idx / static_cast<uint32_t>(n_rho)) + p.theta_offset;
     pk.rho_bin = static_cast<int32_t>(idx % static_cast<uint32_t>(n_rho));
     pk.votes = static_cast<uint32_t>(key >> 32);
     out[i] = pk;
@@ -908,6 +914,110 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
     p.gtau[f] = tau_f;
     p.resolved[f] = 1u;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Peak hint from an existing accumulator (ld_hough_hint_from_acc): what the
+// voting kernel records while a band is in shared memory (R25, R30), computed
+// by one read of the accumulator -- for accumulators that did not come
+// straight out of one ld_hough_accumulate_hint call (a sum of partial
+// accumulators after an all_reduce, a theta shard voted with a slice of the
+// table).  One warp per 1 KB chunk q of a frame's memory: the chunk maximum
+// (exact, written once: no atomics), and the best cell (count << 32 | ~cell)
+// among the chunk's counters in candidate rows [cand_t0, cand_t1), folded by
+// atomicMax into the key of its group of gc consecutive chunks (gc such that
+// the keys fit the hint's capacity of n_theta * HINT_MAX_RANGES per frame;
+// the host zeroes the keys first).  Header: n_bands * HINT_MAX_RANGES keys.
+// ---------------------------------------------------------------------------
+struct HintFromAccParams {
+  const uint32_t *acc;
+  int32_t batch, n_theta, n_rho, cand_t0, cand_t1, n_seg, gc, n_bands;
+  uint32_t *hdr;
+  unsigned long long *keys;  // [batch][n_bands * HINT_MAX_RANGES]
+  uint32_t *segmax;          // [batch][n_seg]
+};
+
+constexpr int HF_WARPS = 8;
+
+__global__ void __launch_bounds__(32 * HF_WARPS) hint_from_acc_kernel(const HintFromAccParams p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, f = blockIdx.y;
+  const int q = blockIdx.x * HF_WARPS + warp;
+  if (f == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint32_t *h = p.hdr;
+    h[0] = HINT_MAGIC;
+    h[1] = static_cast<uint32_t>(p.batch);
+    h[2] = static_cast<uint32_t>(p.n_theta);
+    h[3] = static_cast<uint32_t>(p.n_rho);
+    h[4] = static_cast<uint32_t>(p.n_bands);
+    h[5] = static_cast<uint32_t>(HINT_MAX_RANGES);
+    h[6] = static_cast<uint32_t>(p.n_seg);
+    const uint64_t a = reinterpret_cast<uintptr_t>(p.acc);
+    h[7] = static_cast<uint32_t>(a);
+    h[8] = static_cast<uint32_t>(a >> 32);
+  }
+  if (q >= p.n_seg) return;  // whole warp
+  const int64_t ncells = static_cast<int64_t>(p.n_theta) * p.n_rho;
+  const uint32_t *A = p.acc + static_cast<int64_t>(f) * ncells;
+  const uintptr_t c0 = reinterpret_cast<uintptr_t>(A) / SEG_BYTES;
+  const int64_t w0 = static_cast<int64_t>((c0 + q) * SEG_BYTES - reinterpret_cast<uintptr_t>(A)) / 4;
+  const int64_t r0 = static_cast<int64_t>(p.cand_t0) * p.n_rho, r1 = static_cast<int64_t>(p.cand_t1) * p.n_rho;
+  constexpr int STEPS = SEG_BYTES / 128;
+  uint32_t v[STEPS];
+#pragma unroll
+  for (int s = 0; s < STEPS; ++s) {
+    const int64_t c = w0 + 32 * s + lane;
+    v[s] = (c >= 0 && c < ncells) ? __ldg(A + c) : 0u;
+  }
+  uint32_t m = 0u;
+  u64 best = 0ull;
+#pragma unroll
+  for (int s = 0; s < STEPS; ++s) {
+    const int64_t c = w0 + 32 * s + lane;
+    m = max(m, v[s]);
+    if (v[s] != 0u && c >= r0 && c < r1) {
+      const u64 key = mk_key(v[s], static_cast<uint32_t>(c));
+      best = key > best ? key : best;
+    }
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
+    best = other > best ? other : best;
+  }
+  if (lane == 0) {
+    p.segmax[static_cast<int64_t>(f) * p.n_seg + q] = m;
+    if (best)
+      atomicMax(p.keys + static_cast<int64_t>(f) * p.n_bands * HINT_MAX_RANGES + q / p.gc, best);
+  }
+}
+
+cudaError_t launch_hint_from_acc(const uint32_t *acc, int batch, int n_theta, int n_rho,
+                                 int cand_t0, int cand_t1, void *hint, size_t keys_bytes,
+                                 cudaStream_t stream) {
+  HintFromAccParams p;
+  p.acc = acc;
+  p.batch = batch;
+  p.n_theta = n_theta;
+  p.n_rho = n_rho;
+  p.cand_t0 = cand_t0;
+  p.cand_t1 = cand_t1;
+  p.n_seg = seg_count(static_cast<int64_t>(n_theta) * n_rho);
+  const int64_t cap = static_cast<int64_t>(n_theta) * HINT_MAX_RANGES;  // keys per frame
+  p.gc = static_cast<int>((p.n_seg + cap - 1) / cap);
+  const int n_keys = (p.n_seg + p.gc - 1) / p.gc;
+  p.n_bands = (n_keys + HINT_MAX_RANGES - 1) / HINT_MAX_RANGES;  // <= n_theta
+  p.hdr = static_cast<uint32_t *>(hint);
+  p.keys = reinterpret_cast<unsigned long long *>(static_cast<char *>(hint) + HINT_HDR_BYTES);
+  p.segmax = reinterpret_cast<uint32_t *>(static_cast<char *>(hint) + HINT_HDR_BYTES + keys_bytes);
+  cudaError_t e = cudaMemsetAsync(p.keys, 0,
+                                  sizeof(u64) * static_cast<size_t>(batch) * p.n_bands * HINT_MAX_RANGES,
+                                  stream);
+  if (e != cudaSuccess) return e;
+  dim3 grid(static_cast<unsigned>((p.n_seg + HF_WARPS - 1) / HF_WARPS), batch);
+  hint_from_acc_kernel<<<grid, 32 * HF_WARPS, 0, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksParams p) {
@@ -1972,7 +2082,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
     // the bound, the sparse search and its top k in one launch per frame;
     // dense-only searches take the bound alone
     const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
-    if (ps.hint_hdr && !restricted && wcells * p.k <= (1 << 20)) {
+    if (ps.hint_hdr && wcells * p.k <= (1 << 20)) {
       ps.resolved = sparse_ok ? p_in.resolved : nullptr;
       if (!sparse_ok) ps.segmax = nullptr;
       const cudaError_t em = launch_fused(ps, sms, stream);

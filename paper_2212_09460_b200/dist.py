@@ -105,7 +105,7 @@ class BandedDetector:
         self.ld = ld
         self.plan = BandPlan.make(width, height, rank, world)
         self.device = torch.device("cuda") if device is None else device
-        self.group = group
+        self.group, self.world = group, world
         self.w, self.h, self.n_theta = width, height, n_theta
         self.cos, self.sin = ld._host_i32(cos_q15), ld._host_i32(sin_q15)
         self.threshold, self.k = threshold, k
@@ -125,11 +125,11 @@ class BandedDetector:
         self.ws = torch.empty((max(self.ws_bytes, 16),), dtype=torch.uint8, device=self.device)
         self.peaks = torch.empty((1, k, 3), dtype=torch.int32, device=self.device)
         self.n_peaks = torch.empty((1,), dtype=torch.int32, device=self.device)
-        # one rank holds the whole accumulator: the peak hint (DESIGN R25) is
-        # valid; with several ranks the band partials are summed afterwards
-        self.hint_bytes = ld.ld_hough_hint_bytes(1, width, height, n_theta) if world == 1 else 0
-        self.hint = (torch.empty((self.hint_bytes,), dtype=torch.uint8, device=self.device)
-                     if self.hint_bytes else None)
+        # peak hint (DESIGN R25, R30): one rank holds the whole accumulator, so
+        # voting records it; with several ranks the band partials are summed
+        # afterwards and the hint is taken from the sum (ld_hough_hint_from_acc)
+        self.hint_bytes = ld.ld_hough_hint_bytes(1, width, height, n_theta)
+        self.hint = torch.empty((self.hint_bytes,), dtype=torch.uint8, device=self.device)
         self.launches = 0
 
     def load(self, gray_full):
@@ -169,13 +169,19 @@ class BandedDetector:
         else:
             self.count.zero_()
         mark(1)
+        whole = self.world == 1
         ld.ld_hough_accumulate_opt(self.edges, self.count, self.edge_stride, 1, self.w, self.h,
-                                   self.n_theta, self.cos, self.sin, 0, self.acc, self.hint,
-                                   self.hint_bytes, stream)
+                                   self.n_theta, self.cos, self.sin, 0, self.acc,
+                                   self.hint if whole else None,
+                                   self.hint_bytes if whole else 0, stream)
         self.launches += ld.ld_last_launch_count()
         mark(2)
         allreduce_accumulator(self.acc, self.group)
         mark(3)
+        if not whole:
+            ld.ld_hough_hint_from_acc(self.acc, 1, self.n_theta, self.n_rho, 0, self.n_theta,
+                                      self.hint, self.hint_bytes, stream)
+            self.launches += ld.ld_last_launch_count()
         ld.ld_hough_peaks_opt(self.acc, 1, self.n_theta, self.n_rho, self.half_theta,
                               self.half_rho, self.min_votes, self.k, 0, self.n_theta, 0,
                               self.hint, self.hint_bytes, 0, self.peaks, self.n_peaks, self.ws,
@@ -264,6 +270,8 @@ class ThetaShardedDetector:
         self.acc = torch.empty((1, ns, self.n_rho), dtype=torch.int32, device=self.device)
         self.ws_bytes = ld.ld_hough_peaks_workspace_bytes(1, ns, self.n_rho, k)
         self.ws = torch.empty((max(self.ws_bytes, 16),), dtype=torch.uint8, device=self.device)
+        self.hint_bytes = ld.ld_hough_hint_bytes(1, width, height, ns)
+        self.hint = torch.empty((self.hint_bytes,), dtype=torch.uint8, device=self.device)
         self.peaks = torch.empty((1, k, 3), dtype=torch.int32, device=self.device)
         self.n_peaks = torch.empty((1,), dtype=torch.int32, device=self.device)
         self.allp = torch.empty((world, k, 3), dtype=torch.int32, device=self.device)
@@ -333,16 +341,20 @@ class ThetaShardedDetector:
         `edges`, device `count`) into rows g0 .. g1-1, then the top-k of the
         shard's own rows with global theta bins -> self.peaks, self.n_peaks."""
         ld = self.ld
+        ns = max(self.g1 - self.g0, 1)
         if self.g1 > self.g0:
-            ld.ld_hough_accumulate(edges, count, stride, 1, self.w, self.h, self.g1 - self.g0,
-                                   self.cos_s, self.sin_s, self.acc, None)
+            # the shard's peak hint (its own keys and chunk maxima) comes with
+            # the votes; the search uses the keys of the shard's own rows
+            ld.ld_hough_accumulate_hint(edges, count, stride, 1, self.w, self.h, ns, self.cos_s,
+                                        self.sin_s, self.acc, self.hint, self.hint_bytes, None)
             self.launches += ld.ld_last_launch_count()
         if mark:
             mark(3)
-        ld.ld_hough_peaks_ex(self.acc, 1, max(self.g1 - self.g0, 1), self.n_rho, self.half_theta,
-                             self.half_rho, self.min_votes, self.k, self.t0 - self.g0,
-                             self.t1 - self.g0, self.g0, self.peaks, self.n_peaks, self.ws,
-                             self.ws_bytes, None)
+        hint = self.hint if self.g1 > self.g0 else None
+        ld.ld_hough_peaks_opt(self.acc, 1, ns, self.n_rho, self.half_theta, self.half_rho,
+                              self.min_votes, self.k, self.t0 - self.g0, self.t1 - self.g0,
+                              self.g0, hint, self.hint_bytes if hint is not None else 0, 0,
+                              self.peaks, self.n_peaks, self.ws, self.ws_bytes, None)
         self.launches += ld.ld_last_launch_count()
         if mark:
             mark(4)

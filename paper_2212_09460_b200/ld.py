@@ -56,7 +56,7 @@ LD_PEAKS_DENSE, LD_PEAKS_FORCE_STREAM, LD_PEAKS_FORCE_TILE, LD_PEAKS_FORCE_BAND 
 
 EXPORTS = ["ld_rho_offset", "ld_sobel_binarize", "ld_sobel_binarize_ex", "ld_hough_accumulate",
            "ld_hough_hint_bytes", "ld_hough_accumulate_hint", "ld_hough_peaks_hinted",
-           "ld_hough_accumulate_f64", "ld_hough_accumulate_opt", "ld_hough_peaks_opt",
+           "ld_hough_hint_from_acc", "ld_hough_accumulate_f64", "ld_hough_accumulate_opt", "ld_hough_peaks_opt",
            "ld_edge_bitmask_words", "ld_edges_to_bitmask", "ld_bitmask_to_edges",
            "ld_merge_peak_lists",
            "ld_hough_peaks_workspace_bytes", "ld_hough_peaks", "ld_hough_peaks_ex",
@@ -90,6 +90,7 @@ def lib():
             "ld_hough_accumulate_f64": ([P, P, i64, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
             "ld_hough_accumulate_hint": ([P, P, i64, i32, i32, i32, i32, P, P, P, P, sz, P],
                                          ctypes.c_int),
+            "ld_hough_hint_from_acc": ([P, i32, i32, i32, i32, i32, P, sz, P], ctypes.c_int),
             "ld_hough_peaks_hinted": ([P, i32, i32, i32, i32, i32, u32, i32, P, sz, P, P, P, sz,
                                        P], ctypes.c_int),
             "ld_hough_peaks_workspace_bytes": ([i32, i32, i32, i32], sz),
@@ -251,6 +252,13 @@ def ld_hough_accumulate_hint(edge_xy, edge_count, edge_stride, batch, width, hei
                                           int(batch), int(width), int(height), int(n_theta),
                                           _addr(c), _addr(s), _addr(acc), _addr(hint),
                                           int(hint_bytes), _stream(stream)))
+
+
+def ld_hough_hint_from_acc(acc, batch, n_theta, n_rho, cand_row_begin, cand_row_end, hint,
+                           hint_bytes, stream=None):
+    _check(lib().ld_hough_hint_from_acc(_addr(acc), int(batch), int(n_theta), int(n_rho),
+                                        int(cand_row_begin), int(cand_row_end), _addr(hint),
+                                        int(hint_bytes), _stream(stream)))
 
 
 def ld_hough_peaks_hinted(acc, batch, n_theta, n_rho, half_theta, half_rho, min_votes, k, hint,
@@ -466,6 +474,19 @@ def hough_accumulate(edges, counts, edge_stride, width, height, cos_q15, sin_q15
     return (acc, hint) if want_hint else acc
 
 
+def hint_from_acc(acc, width, height, cand_rows=None, stream=None):
+    """The peak hint of an existing accumulator (ld_hough_hint_from_acc):
+    acc int32 CUDA [B][n_theta][n_rho] of a width x height image (n_rho =
+    2 ld_rho_offset + 1); cand_rows=(begin, end) limits the recorded keys."""
+    import torch
+    b, n_theta, n_rho = acc.shape
+    hb = ld_hough_hint_bytes(b, width, height, n_theta)
+    hint = torch.empty((hb,), dtype=torch.uint8, device=acc.device)
+    c0, c1 = cand_rows if cand_rows is not None else (0, n_theta)
+    ld_hough_hint_from_acc(acc, b, n_theta, n_rho, c0, c1, hint, hb, stream)
+    return hint
+
+
 def hough_peaks(acc, half_theta, half_rho, min_votes, k, stream=None, cand_rows=None,
                 theta_offset=0, hint=None, flags=0):
     """acc: int32 CUDA [B][n_theta][n_rho] (uint32 bits).  cand_rows=(begin, end)
@@ -478,7 +499,7 @@ def hough_peaks(acc, half_theta, half_rho, min_votes, k, stream=None, cand_rows=
     ws = torch.empty((max(ws_bytes, 16),), dtype=torch.uint8, device=acc.device)
     peaks = torch.empty((b, k, 3), dtype=torch.int32, device=acc.device)
     n_peaks = torch.empty((b,), dtype=torch.int32, device=acc.device)
-    if flags:
+    if flags or (hint is not None and (cand_rows is not None or theta_offset)):
         c0, c1 = cand_rows if cand_rows is not None else (0, n_theta)
         ld_hough_peaks_opt(acc, b, n_theta, n_rho, half_theta, half_rho, min_votes, k, c0, c1,
                            theta_offset, hint, 0 if hint is None else hint.numel(), flags, peaks,

@@ -146,6 +146,11 @@ def test_cfg5_decompositions_whole_image(ld, oracle, world, shard):
         assert sum(int(d.count.item()) for d in bands) == want["n_edges"]
         assert np.array_equal(total.cpu().numpy().view(np.uint32)[0], want["acc"])
         pk, n = ld.hough_peaks(total, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+        # the summed accumulator's own hint (ld_hough_hint_from_acc, what a
+        # rank does after the all_reduce): the same peaks
+        pkh, nh = ld.hough_peaks(total, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k,
+                                 hint=ld.hint_from_acc(total, W, H))
+        assert torch.equal(pk, pkh) and torch.equal(n, nh)
         got = [tuple(int(v) for v in p) for p in pk[0].cpu().numpy()[: int(n[0])]]
         got = [(a, b, int(np.uint32(np.int32(v)))) for a, b, v in got]
     else:

@@ -637,6 +637,68 @@ def test_peaks_ex_theta_slices(ld, oracle, kernel):
             assert got == want, (kernel, trial, t0, t1)
 
 
+@pytest.mark.parametrize("keys_rows", ["slice", "all"])
+def test_peaks_ex_theta_slices_hint_from_acc(ld, oracle, keys_rows):
+    """ld_hough_hint_from_acc on theta slices (halo rows included), with its
+    keys taken from the candidate rows only or from every row (the search
+    must drop the others), through the fused search with candidate rows and a
+    theta offset: the definition restricted to those rows (oracle)."""
+    rng = np.random.default_rng(321)
+    W, H = 360, 480  # 2 ld_rho_offset + 1 = 1201 bins: sizes the hint buffer
+    for trial, (nt, ht, hr, k) in enumerate([(180, 2, 29, 4), (1024, 10, 116, 64),
+                                              (97, 3, 5, 16), (33, 7, 44, 8)]):
+        big = rng.integers(0, 12 if trial % 2 else 5000, size=(nt, 1201)).astype(np.uint32)
+        # a few strong peaks, so that the hint certifies a bound
+        for j in range(3 * k):
+            big[rng.integers(0, nt), rng.integers(0, 1201)] = 20000 + j
+        cands = oracle_all_candidates(oracle, big, ht, hr, 1)
+        for (t0, t1) in [(0, nt), (0, nt // 3), (nt // 3, 2 * nt // 3), (2 * nt // 3, nt)]:
+            g0, g1 = max(t0 - ht, 0), min(t1 + ht, nt)
+            sl = cuda(np.ascontiguousarray(big[g0:g1])[None].view(np.int32))
+            rows = (t0 - g0, t1 - g0)
+            hint = ld.hint_from_acc(sl, W, H, cand_rows=rows if keys_rows == "slice" else None)
+            peaks, npk = ld.hough_peaks(sl, ht, hr, 1, k, cand_rows=rows, theta_offset=g0,
+                                        hint=hint)
+            torch.cuda.synchronize()
+            want = oracle_slice_peaks(cands, t0, t1, k)
+            assert int(npk[0]) == len(want), (trial, t0, t1)
+            assert peak_tuples(peaks[0].cpu())[:len(want)] == want, (trial, t0, t1)
+
+
+@pytest.mark.parametrize("name,nf", [("cfg2", 1), ("cfg3", 6), ("cfg4", 2)])
+def test_hint_from_acc_whole_frames(ld, oracle, name, nf):
+    """The hint of a finished accumulator (what a row-band all_reduce sum
+    needs) gives the exact peaks, and describes the chunks exactly."""
+    cfg = synth.CONFIGS[name]
+    c, s = synth.q15_table(cfg.n_theta)
+    frames = synth.gen_batch(name, 0, nf) if cfg.batch > 1 else synth.gen_frame(name, 0)[None]
+    b, h, w = frames.shape
+    _, edges, counts, stride = ld.sobel_binarize(cuda(frames), cfg.threshold, want_binary=False)
+    acc = ld.hough_accumulate(edges, counts, stride, w, h, c, s)
+    hint = ld.hint_from_acc(acc, w, h)
+    check_chunk_maxima(acc, hint)
+    p0, n0 = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+    p1, n1 = ld.hough_peaks(acc, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k, hint=hint)
+    _, nt, nr = acc.shape
+    wsb = ld.ld_hough_peaks_workspace_bytes(b, nt, nr, cfg.k)
+    ws = torch.zeros((wsb,), dtype=torch.uint8, device="cuda")
+    p2 = torch.empty((b, cfg.k, 3), dtype=torch.int32, device="cuda")
+    n2 = torch.empty((b,), dtype=torch.int32, device="cuda")
+    ld.ld_hough_peaks_hinted(acc, b, nt, nr, cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k,
+                             hint, hint.numel(), p2, n2, ws, wsb)
+    torch.cuda.synchronize()
+    assert torch.equal(p0, p1) and torch.equal(n0, n1)
+    assert torch.equal(p0, p2) and torch.equal(n0, n2)
+    # the search was resolved by the hint (the sparse path ran)
+    head = (4 * b + 255) // 256 * 256
+    assert ws[head:head + 4 * b].view(torch.int32).min().item() == 1
+    A = acc.cpu().numpy().view(np.uint32)
+    for f in range(b):
+        pk, npk = oracle.hough_peaks(A[f], cfg.half_theta, cfg.half_rho, cfg.min_votes, cfg.k)
+        assert int(n1.cpu()[f]) == npk
+        assert peak_tuples(p1.cpu().numpy()[f]) == oracle_peak_tuples(pk)
+
+
 def test_theta_sharded_detector_emulated(ld, oracle):
     # every rank of world N in one process: the whole-image edge list stands in
     # for the all-gathered band lists; per-rank top-k lists merged on device
