@@ -433,16 +433,19 @@ SobelCfg sobel_cfg(int width, int rows, int frames, int sms) {
 #ifndef LD_SOBEL_MINB
 #define LD_SOBEL_MINB 2  // CTAs per SM (register budget 65536 / (288 * MINB))
 #endif
+#ifndef LD_SOBEL_STAGES
+#define LD_SOBEL_STAGES 2  // TMA ring depth per CTA
+#endif
 cudaError_t launch_sobel(const CUtensorMap &tmap, const SobelParams &p, int sm_count,
                          cudaStream_t stream) {
-  constexpr int MB = LD_SOBEL_MINB;
+  constexpr int MB = LD_SOBEL_MINB, ST = LD_SOBEL_STAGES;
   const int64_t max_ctas = static_cast<int64_t>(sm_count) * MB;
   const int n_ctas = static_cast<int>(p.n_tiles < max_ctas ? p.n_tiles : max_ctas);
   if (p.sr == 2)
-    return p.binary != nullptr ? launch_cfg<2, 2, MB, true>(tmap, p, n_ctas, stream)
-                               : launch_cfg<2, 2, MB, false>(tmap, p, n_ctas, stream);
-  return p.binary != nullptr ? launch_cfg<LD_SOBEL_SR, 2, MB, true>(tmap, p, n_ctas, stream)
-                             : launch_cfg<LD_SOBEL_SR, 2, MB, false>(tmap, p, n_ctas, stream);
+    return p.binary != nullptr ? launch_cfg<2, ST, MB, true>(tmap, p, n_ctas, stream)
+                               : launch_cfg<2, ST, MB, false>(tmap, p, n_ctas, stream);
+  return p.binary != nullptr ? launch_cfg<LD_SOBEL_SR, ST, MB, true>(tmap, p, n_ctas, stream)
+                             : launch_cfg<LD_SOBEL_SR, ST, MB, false>(tmap, p, n_ctas, stream);
 }
 
 }  // namespace ld
