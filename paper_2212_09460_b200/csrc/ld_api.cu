@@ -10,6 +10,8 @@
 
 #include "ld_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges cost nothing without a profiler
+
 namespace ld {
 
 static thread_local char g_err[512] = "";
@@ -395,6 +397,16 @@ static DetectLayout detect_layout(const ld_image *img, int32_t n_theta, int32_t 
 
 }  // namespace ld
 
+
+// An NVTX range over one ABI call (nsys / ncu --nvtx timelines name the
+// library's stages; inert without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 using namespace ld;
 
 extern "C" {
@@ -432,6 +444,7 @@ int64_t ld_device_l2_bytes(void) {
 int ld_sobel_binarize_ex(const uint8_t *gray, const ld_image *img, int32_t threshold,
                          uint32_t flags, uint8_t *binary, uint32_t *edge_xy,
                          int64_t edge_stride, uint32_t *edge_count, void *stream) {
+  NvtxRange nvtx_range_("ld_sobel_binarize_ex");
   g_launches = 0;
   int rc = check_image(gray, img);
   if (rc) return rc;
@@ -470,6 +483,7 @@ int ld_hough_accumulate_opt(const uint32_t *edge_xy, const uint32_t *edge_count,
                             int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
                             uint32_t flags, uint32_t *acc, void *hint, size_t hint_bytes_,
                             void *stream) {
+  NvtxRange nvtx_range_("ld_hough_accumulate_opt");
   g_launches = 0;
   int rc = check_vote_args(edge_xy, edge_count, acc, edge_stride, batch, width, height);
   if (rc) return rc;
@@ -498,6 +512,7 @@ int ld_hough_accumulate_f64(const uint32_t *edge_xy, const uint32_t *edge_count,
                             int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
                             int32_t n_theta, const double *cos_f64, const double *sin_f64,
                             uint32_t *acc, void *stream) {
+  NvtxRange nvtx_range_("ld_hough_accumulate_f64");
   g_launches = 0;
   const int rc0 = check_vote_args(edge_xy, edge_count, acc, edge_stride, batch, width, height);
   if (rc0) return rc0;
@@ -560,6 +575,7 @@ int ld_hough_accumulate_hint(const uint32_t *edge_xy, const uint32_t *edge_count
                              int64_t edge_stride, int32_t batch, int32_t width, int32_t height,
                              int32_t n_theta, const int32_t *cos_q15, const int32_t *sin_q15,
                              uint32_t *acc, void *hint, size_t hint_bytes_, void *stream) {
+  NvtxRange nvtx_range_("ld_hough_accumulate_hint");
   if (!hint) {
     g_launches = 0;
     return fail(LD_ERR_INVALID_ARG, "NULL hint");
@@ -579,6 +595,7 @@ int ld_hough_peaks_opt(const uint32_t *acc, int32_t batch, int32_t n_theta, int3
                        const void *hint, size_t hint_bytes_, uint32_t flags, ld_peak *peaks,
                        int32_t *n_peaks, void *workspace, size_t workspace_bytes,
                        void *stream) {
+  NvtxRange nvtx_range_("ld_hough_peaks_opt");
   g_launches = 0;
   int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
   if (rc) return rc;
@@ -619,6 +636,7 @@ int ld_hough_peaks_ex(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
 int ld_hough_hint_from_acc(const uint32_t *acc, int32_t batch, int32_t n_theta, int32_t n_rho,
                            int32_t cand_row_begin, int32_t cand_row_end, void *hint,
                            size_t hint_bytes_, void *stream) {
+  NvtxRange nvtx_range_("ld_hough_hint_from_acc");
   g_launches = 0;
   if (!acc || !hint) return fail(LD_ERR_INVALID_ARG, "NULL acc/hint");
   if (batch < 1 || n_theta < 1 || n_theta > LD_MAX_THETA || n_rho < 1)
@@ -699,6 +717,7 @@ int ld_hough_peaks_nms(const uint32_t *acc, int32_t batch, int32_t n_theta, int3
                        uint32_t ratio_num, uint32_t ratio_den, int32_t k, ld_peak *peaks,
                        int32_t *n_peaks, void *workspace, size_t workspace_bytes,
                        void *stream) {
+  NvtxRange nvtx_range_("ld_hough_peaks_nms");
   g_launches = 0;
   int rc = check_peaks_args(acc, batch, n_theta, n_rho, half_theta, half_rho, k, peaks, n_peaks);
   if (rc) return rc;
@@ -763,6 +782,7 @@ static int lanes_common(const ld_peak *peaks, const int32_t *n_peaks, int32_t ba
 int ld_peak_lines(const ld_peak *peaks, const int32_t *n_peaks, int32_t batch, int32_t k,
                   int32_t width, int32_t height, int32_t n_theta, const int32_t *cos_q15,
                   const int32_t *sin_q15, ld_segment *lines, int32_t *hit, void *stream) {
+  NvtxRange nvtx_range_("ld_peak_lines");
   g_launches = 0;
   static thread_local TrigTable trig;
   LanesParams p;
@@ -782,6 +802,7 @@ int ld_extract_segments(const uint8_t *binary, const ld_image *img, const ld_pea
                         const int32_t *cos_q15, const int32_t *sin_q15, int32_t fill_gap,
                         int32_t min_len, int32_t max_segments, ld_segment *segments,
                         int32_t *n_segments, void *stream) {
+  NvtxRange nvtx_range_("ld_extract_segments");
   g_launches = 0;
   if (!img || !binary) return fail(LD_ERR_INVALID_ARG, "NULL binary/img");
   if (img->pitch < img->width || img->batch < 1 ||
@@ -814,6 +835,7 @@ int ld_detect_batch_ex(const uint8_t *gray, const ld_image *img, int32_t thresho
                        uint32_t min_votes, int32_t k, ld_peak *peaks, int32_t *n_peaks,
                        uint32_t *edge_count, uint32_t *acc, void *workspace,
                        size_t workspace_bytes, void *stream) {
+  NvtxRange nvtx_range_("ld_detect_batch_ex");
   g_launches = 0;
   int rc = check_image(gray, img);
   if (rc) return rc;
@@ -943,6 +965,7 @@ int ld_detect_batch_host(const uint8_t *gray_host, const ld_image *img, int32_t 
                          ld_peak *peaks_host, int32_t *n_peaks_host, uint32_t *edge_count_host,
                          int32_t chunk_frames, void *workspace, size_t workspace_bytes,
                          void *stream) {
+  NvtxRange nvtx_range_("ld_detect_batch_host");
   if (!gray_host || !img || !peaks_host || !n_peaks_host)
     return fail(LD_ERR_INVALID_ARG, "NULL host pointer");
   if (chunk_frames < 1) return fail(LD_ERR_INVALID_ARG, "chunk_frames must be >= 1");
@@ -1017,6 +1040,7 @@ int64_t ld_edge_bitmask_words(int32_t width, int32_t rows) {
 
 int ld_edges_to_bitmask(const uint32_t *edge_xy, const uint32_t *edge_count, int32_t width,
                         int32_t row_begin, int32_t rows, uint32_t *bits, void *stream) {
+  NvtxRange nvtx_range_("ld_edges_to_bitmask");
   g_launches = 0;
   if (!edge_xy || !edge_count || !bits) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
   if (width < 1 || width > LD_MAX_DIM || rows < 1 || row_begin < 0 ||
@@ -1037,6 +1061,7 @@ int ld_bitmask_to_edges(const uint32_t *bits, int32_t width, int32_t n_blocks,
                         const int32_t *block_row_begin, const int32_t *block_rows,
                         int32_t block_stride_rows, uint32_t *edge_xy, int64_t edge_capacity,
                         uint32_t *edge_count, void *stream) {
+  NvtxRange nvtx_range_("ld_bitmask_to_edges");
   g_launches = 0;
   if (!bits || !edge_xy || !edge_count) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
   if (!block_row_begin || !block_rows) return fail(LD_ERR_INVALID_ARG, "NULL block table");
@@ -1060,6 +1085,7 @@ int ld_bitmask_to_edges(const uint32_t *bits, int32_t width, int32_t n_blocks,
 
 int ld_merge_peak_lists(const ld_peak *peaks, const int32_t *n_peaks, int32_t n_lists,
                         int32_t k, int32_t n_rho, ld_peak *out, int32_t *n_out, void *stream) {
+  NvtxRange nvtx_range_("ld_merge_peak_lists");
   g_launches = 0;
   if (!peaks || !n_peaks || !out || !n_out) return fail(LD_ERR_INVALID_ARG, "NULL device pointer");
   if (n_lists < 1 || k < 1 || k > LD_MAX_K || n_rho < 1 ||
