@@ -346,6 +346,9 @@ static int peaks_impl(const uint32_t *acc, int32_t batch, int32_t n_theta, int32
   p.gtau = reinterpret_cast<uint32_t *>(ws + W.gtau);
   p.resolved = reinterpret_cast<uint32_t *>(ws + W.resolved);
   p.diag = reinterpret_cast<unsigned long long *>(ws + W.diag);
+  p.self_hdr = reinterpret_cast<uint32_t *>(ws + W.self_hdr);
+  p.self_keys = reinterpret_cast<unsigned long long *>(ws + W.self_keys);
+  p.self_segmax = reinterpret_cast<uint32_t *>(ws + W.self_segmax);
   p.band_keys = reinterpret_cast<unsigned long long *>(ws + W.keys);
   p.peaks = peaks;
   p.n_peaks = n_peaks;
@@ -653,9 +656,12 @@ int ld_hough_hint_from_acc(const uint32_t *acc, int32_t batch, int32_t n_theta, 
   DevInfo dev;
   int rc = device_info(&dev);
   if (rc) return rc;
-  const cudaError_t e = launch_hint_from_acc(acc, batch, n_theta, n_rho, cand_row_begin,
-                                             cand_row_end, hint, hint_keys_bytes(batch, n_theta),
-                                             static_cast<cudaStream_t>(stream));
+  char *hb = static_cast<char *>(hint);
+  const cudaError_t e = launch_hint_from_acc(
+      acc, batch, n_theta, n_rho, cand_row_begin, cand_row_end, reinterpret_cast<uint32_t *>(hb),
+      reinterpret_cast<unsigned long long *>(hb + HINT_HDR_BYTES),
+      reinterpret_cast<uint32_t *>(hb + HINT_HDR_BYTES + hint_keys_bytes(batch, n_theta)),
+      static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "hint_from_acc_kernel launch");
   return LD_OK;
 }

@@ -157,6 +157,9 @@ struct PeaksParams {
   int32_t n_seg;
   uint32_t *resolved;             // [batch] 1 = the fused hinted search wrote this frame's peaks
   unsigned long long *diag;       // [batch][PF_DIAG] diagnostics (LD_PF_STATS builds)
+  uint32_t *self_hdr = nullptr;   // workspace hint of the accumulator itself (no hint given)
+  unsigned long long *self_keys = nullptr;
+  uint32_t *self_segmax = nullptr;
   ld_peak *peaks;
   int32_t *n_peaks;
 };
@@ -165,16 +168,17 @@ constexpr int PF_DIAG = 16;       // diagnostics words per frame in the peaks wo
 
 // Peaks workspace: byte offsets of its parts
 struct PeaksLayout {
-  size_t gtau, resolved, diag, keys, total;
+  size_t gtau, resolved, diag, keys, self_hdr, self_keys, self_segmax, total;
 };
 PeaksLayout peaks_layout(int batch, int n_theta, int n_rho, int k);
 size_t peaks_workspace_bytes(int batch, int n_theta, int n_rho, int k);
 // flags: LD_PEAKS_* of ld.h
 cudaError_t launch_peaks(const PeaksParams &p, uint32_t flags, cudaStream_t stream);
-// the peak hint of an existing accumulator (keys_bytes: the hint's key region)
+// the peak hint of an existing accumulator into header, keys and chunk maxima
 cudaError_t launch_hint_from_acc(const uint32_t *acc, int batch, int n_theta, int n_rho,
-                                 int cand_t0, int cand_t1, void *hint, size_t keys_bytes,
-                                 cudaStream_t stream);
+                                 int cand_t0, int cand_t1, uint32_t *hdr,
+                                 unsigned long long *keys, uint32_t *segmax, cudaStream_t stream);
+size_t hint_self_keys_bytes(int batch, int n_theta, int n_rho);
 
 // ---------------------------------------------------------------------------
 // NEXT 3: lanes module (ld_lanes.cu)

@@ -19,6 +19,7 @@
 // merges the per-unit lists.  The warp and stream kernels share a per-frame
 // running threshold (the k-th best found so far, gtau), optionally started
 // by peaks_hint_kernel from the voting kernel's range maxima (DESIGN R25).
+#include <algorithm>
 #include <cstdlib>
 
 #include <cooperative_groups.h>
@@ -941,7 +942,6 @@ constexpr int HF_WARPS = 8;
 
 __global__ void __launch_bounds__(32 * HF_WARPS) hint_from_acc_kernel(const HintFromAccParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, f = blockIdx.y;
-  const int q = blockIdx.x * HF_WARPS + warp;
   if (f == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
     uint32_t *h = p.hdr;
     h[0] = HINT_MAGIC;
@@ -955,46 +955,92 @@ __global__ void __launch_bounds__(32 * HF_WARPS) hint_from_acc_kernel(const Hint
     h[7] = static_cast<uint32_t>(a);
     h[8] = static_cast<uint32_t>(a >> 32);
   }
-  if (q >= p.n_seg) return;  // whole warp
   const int64_t ncells = static_cast<int64_t>(p.n_theta) * p.n_rho;
   const uint32_t *A = p.acc + static_cast<int64_t>(f) * ncells;
   const uintptr_t c0 = reinterpret_cast<uintptr_t>(A) / SEG_BYTES;
-  const int64_t w0 = static_cast<int64_t>((c0 + q) * SEG_BYTES - reinterpret_cast<uintptr_t>(A)) / 4;
   const int64_t r0 = static_cast<int64_t>(p.cand_t0) * p.n_rho, r1 = static_cast<int64_t>(p.cand_t1) * p.n_rho;
-  constexpr int STEPS = SEG_BYTES / 128;
-  uint32_t v[STEPS];
+  // a chunk is 1 KB-aligned: lane l reads its counters 4l .. 4l+3 and
+  // 128+4l .. 131+4l as two 16-byte vectors; the frame's first and last
+  // chunks (bytes outside the frame) are read counter by counter
+  constexpr int CH = 4;  // chunks per warp in flight
+  const int stride = gridDim.x * HF_WARPS;
+  for (int q0 = blockIdx.x * HF_WARPS + warp; q0 < p.n_seg; q0 += CH * stride) {
+    uint4 v[CH][2];
+    int64_t w0[CH];
 #pragma unroll
-  for (int s = 0; s < STEPS; ++s) {
-    const int64_t c = w0 + 32 * s + lane;
-    v[s] = (c >= 0 && c < ncells) ? __ldg(A + c) : 0u;
-  }
-  uint32_t m = 0u;
-  u64 best = 0ull;
+    for (int h = 0; h < CH; ++h) {
+      const int q = q0 + h * stride;
+      w0[h] = static_cast<int64_t>((c0 + q) * SEG_BYTES - reinterpret_cast<uintptr_t>(A)) / 4;
 #pragma unroll
-  for (int s = 0; s < STEPS; ++s) {
-    const int64_t c = w0 + 32 * s + lane;
-    m = max(m, v[s]);
-    if (v[s] != 0u && c >= r0 && c < r1) {
-      const u64 key = mk_key(v[s], static_cast<uint32_t>(c));
-      best = key > best ? key : best;
+      for (int j = 0; j < 2; ++j) {
+        const int64_t c = w0[h] + 128 * j + 4 * lane;
+        if (q >= p.n_seg) {
+          v[h][j] = make_uint4(0u, 0u, 0u, 0u);
+        } else if (w0[h] >= 0 && w0[h] + 256 <= ncells) {
+          v[h][j] = __ldg(reinterpret_cast<const uint4 *>(A + c));
+        } else {
+          v[h][j].x = c + 0 >= 0 && c + 0 < ncells ? __ldg(A + c + 0) : 0u;
+          v[h][j].y = c + 1 >= 0 && c + 1 < ncells ? __ldg(A + c + 1) : 0u;
+          v[h][j].z = c + 2 >= 0 && c + 2 < ncells ? __ldg(A + c + 2) : 0u;
+          v[h][j].w = c + 3 >= 0 && c + 3 < ncells ? __ldg(A + c + 3) : 0u;
+        }
+      }
     }
-  }
-  m = __reduce_max_sync(0xffffffffu, m);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
-    best = other > best ? other : best;
-  }
-  if (lane == 0) {
-    p.segmax[static_cast<int64_t>(f) * p.n_seg + q] = m;
-    if (best)
-      atomicMax(p.keys + static_cast<int64_t>(f) * p.n_bands * HINT_MAX_RANGES + q / p.gc, best);
+    for (int h = 0; h < CH; ++h) {
+      const int q = q0 + h * stride;
+      if (q >= p.n_seg) break;  // warp-uniform
+      // the chunk maximum, and the lane's first (lowest-index) maximum among
+      // the candidate rows' counters
+      uint32_t m = 0u, lm = 0u;
+      int64_t li = 0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t e4[4] = {v[h][j].x, v[h][j].y, v[h][j].z, v[h][j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int64_t c = w0[h] + 128 * j + 4 * lane + e;
+          m = max(m, e4[e]);
+          if (e4[e] > lm && c >= r0 && c < r1) {
+            lm = e4[e];
+            li = c;
+          }
+        }
+      }
+      m = __reduce_max_sync(0xffffffffu, m);
+      u64 best = lm ? mk_key(lm, static_cast<uint32_t>(li)) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other > best ? other : best;
+      }
+      if (lane == 0) {
+        p.segmax[static_cast<int64_t>(f) * p.n_seg + q] = m;
+        if (best)
+          atomicMax(p.keys + static_cast<int64_t>(f) * p.n_bands * HINT_MAX_RANGES + q / p.gc, best);
+      }
+    }
   }
 }
 
+// keys and chunk groups of the hint of an n_theta x n_rho accumulator
+static void hint_geometry(int n_theta, int n_rho, int *n_seg, int *gc, int *n_bands) {
+  *n_seg = seg_count(static_cast<int64_t>(n_theta) * n_rho);
+  const int64_t cap = static_cast<int64_t>(n_theta) * HINT_MAX_RANGES;  // keys per frame
+  *gc = static_cast<int>((*n_seg + cap - 1) / cap);
+  const int n_keys = (*n_seg + *gc - 1) / *gc;
+  *n_bands = (n_keys + HINT_MAX_RANGES - 1) / HINT_MAX_RANGES;  // <= n_theta
+}
+
+size_t hint_self_keys_bytes(int batch, int n_theta, int n_rho) {
+  int n_seg, gc, n_bands;
+  hint_geometry(n_theta, n_rho, &n_seg, &gc, &n_bands);
+  return sizeof(u64) * static_cast<size_t>(batch) * n_bands * HINT_MAX_RANGES;
+}
+
 cudaError_t launch_hint_from_acc(const uint32_t *acc, int batch, int n_theta, int n_rho,
-                                 int cand_t0, int cand_t1, void *hint, size_t keys_bytes,
-                                 cudaStream_t stream) {
+                                 int cand_t0, int cand_t1, uint32_t *hdr,
+                                 unsigned long long *keys, uint32_t *segmax, cudaStream_t stream) {
   HintFromAccParams p;
   p.acc = acc;
   p.batch = batch;
@@ -1002,19 +1048,21 @@ cudaError_t launch_hint_from_acc(const uint32_t *acc, int batch, int n_theta, in
   p.n_rho = n_rho;
   p.cand_t0 = cand_t0;
   p.cand_t1 = cand_t1;
-  p.n_seg = seg_count(static_cast<int64_t>(n_theta) * n_rho);
-  const int64_t cap = static_cast<int64_t>(n_theta) * HINT_MAX_RANGES;  // keys per frame
-  p.gc = static_cast<int>((p.n_seg + cap - 1) / cap);
-  const int n_keys = (p.n_seg + p.gc - 1) / p.gc;
-  p.n_bands = (n_keys + HINT_MAX_RANGES - 1) / HINT_MAX_RANGES;  // <= n_theta
-  p.hdr = static_cast<uint32_t *>(hint);
-  p.keys = reinterpret_cast<unsigned long long *>(static_cast<char *>(hint) + HINT_HDR_BYTES);
-  p.segmax = reinterpret_cast<uint32_t *>(static_cast<char *>(hint) + HINT_HDR_BYTES + keys_bytes);
+  hint_geometry(n_theta, n_rho, &p.n_seg, &p.gc, &p.n_bands);
+  p.hdr = hdr;
+  p.keys = keys;
+  p.segmax = segmax;
   cudaError_t e = cudaMemsetAsync(p.keys, 0,
                                   sizeof(u64) * static_cast<size_t>(batch) * p.n_bands * HINT_MAX_RANGES,
                                   stream);
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>((p.n_seg + HF_WARPS - 1) / HF_WARPS), batch);
+  // about 8 CTAs per SM over the whole batch, every warp looping over chunks
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int want = (8 * sms + batch - 1) / batch;
+  const int gx = std::max(1, std::min(want, (p.n_seg + HF_WARPS - 1) / HF_WARPS));
+  dim3 grid(static_cast<unsigned>(gx), batch);
   hint_from_acc_kernel<<<grid, 32 * HF_WARPS, 0, stream>>>(p);
   note_launch();
   return cudaGetLastError();
@@ -1994,7 +2042,14 @@ PeaksLayout peaks_layout(int batch, int n_theta, int n_rho, int k) {
   L.resolved = head;
   L.diag = 2 * head;
   L.keys = L.diag + sizeof(u64) * static_cast<size_t>(batch) * PF_DIAG;
-  L.total = L.keys + static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
+  // + the peak hint computed from the accumulator itself (searches called
+  // without one): header, range keys, chunk maxima
+  const size_t keys_end = L.keys + static_cast<size_t>(batch) * (tiles > bands ? tiles : bands) * k * sizeof(u64);
+  L.self_hdr = (keys_end + 255) / 256 * 256;
+  L.self_keys = L.self_hdr + HINT_HDR_BYTES;
+  L.self_segmax = L.self_keys + hint_self_keys_bytes(batch, n_theta, n_rho);
+  L.total = L.self_segmax +
+            sizeof(uint32_t) * static_cast<size_t>(batch) * seg_count(static_cast<int64_t>(n_theta) * n_rho);
   return L;
 }
 
@@ -2078,10 +2133,21 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
   if (dense_cheap || dense_stream) {
     // the hint (and with it the sparse search) serves the warp and streaming kernels
     PeaksParams ps = p;
+    const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
+    if (!ps.hint_hdr && !dense_only && ps.self_hdr && wcells * p.k <= (1 << 20)) {
+      // no hint from voting: take it from the accumulator (one read of it)
+      // for the same fused search (R25, R30: the result is unchanged)
+      const cudaError_t eh = launch_hint_from_acc(p.acc, p.batch, p.n_theta, p.n_rho, p.cand_t0,
+                                                  p.cand_t1, ps.self_hdr, ps.self_keys,
+                                                  ps.self_segmax, stream);
+      if (eh != cudaSuccess) return eh;
+      ps.hint_hdr = p.hint_hdr = ps.self_hdr;
+      ps.hint_keys = p.hint_keys = ps.self_keys;
+      ps.segmax = p.segmax = ps.self_segmax;
+    }
     const bool sparse_ok = ps.hint_hdr && ps.segmax && !dense_only;
     // the bound, the sparse search and its top k in one launch per frame;
     // dense-only searches take the bound alone
-    const int64_t wcells = static_cast<int64_t>(2 * p.half_theta + 1) * (2 * p.half_rho + 1);
     if (ps.hint_hdr && wcells * p.k <= (1 << 20)) {
       ps.resolved = sparse_ok ? p_in.resolved : nullptr;
       if (!sparse_ok) ps.segmax = nullptr;
