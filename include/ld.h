@@ -189,6 +189,11 @@ int ld_hough_accumulate_opt(const uint32_t *edge_xy, const uint32_t *edge_count,
  * |r'-r| <= half_rho clipped to the accumulator (no theta wrap-around).
  * peaks[f][0..k) = the min(k, #candidates) largest keys, descending, then the
  * sentinel; n_peaks[f] = min(k, #candidates).
+ * The search first derives the peak hint of acc into the workspace (one read
+ * of acc, as ld_hough_hint_from_acc) and searches only the chunks that can
+ * hold a top-k candidate; frames it cannot settle that way go through the
+ * dense kernels (LD_PEAKS_DENSE of ld_hough_peaks_opt: those alone).  The
+ * result is the same either way.
  *  acc       : [batch][n_theta][n_rho] uint32 (device).
  *  k         : 1..LD_MAX_K.   half_theta, half_rho >= 0.
  *  workspace : device, >= ld_hough_peaks_workspace_bytes(...), 16-B aligned. */
