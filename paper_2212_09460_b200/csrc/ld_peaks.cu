@@ -8,17 +8,22 @@
 // candidate iff acc >= max(1, min_votes) and its key is the maximum of its
 // (2ht+1) x (2hr+1) window clipped to the accumulator.  DESIGN.md 6.3.
 //
-// Kernel 1, chosen per window (launch_peaks, in this order):
+// launch_peaks: first peaks_fused_kernel (one CTA or cluster per frame): the
+// certified bound from the peak hint (the voting kernel's, or one taken from
+// acc by hint_from_acc_kernel), the sparse search over the chunks that can
+// hold a top-k candidate, and the frame's top k (DESIGN R25, R30).  Frames it
+// cannot settle -- and every frame with LD_PEAKS_DENSE -- go through a dense
+// kernel, chosen per window (in this order):
 //   peaks_warp_kernel    -- half_theta <= 3, 4 <= half_rho <= 64, k <= 64:
 //                           every warp an independent strip x row chunk;
 //   peaks_stream_kernel  -- half_theta <= 12: a CTA per strip x row chunk;
 //   peaks_tile_kernel    -- separable window maximum over 16-row tiles
 //                           (unrestricted searches);
 //   peaks_band_kernel    -- generic fallback: a window scan per cell.
-// All keep a per-unit top-k; kernel 2 (peaks_merge_kernel, one CTA per frame)
-// merges the per-unit lists.  The warp and stream kernels share a per-frame
-// running threshold (the k-th best found so far, gtau), optionally started
-// by peaks_hint_kernel from the voting kernel's range maxima (DESIGN R25).
+// All keep a per-unit top-k; peaks_merge_kernel (one CTA per frame) merges
+// the per-unit lists.  The dense kernels skip the frames the fused search
+// resolved; the warp and stream kernels start from its bound (gtau) and
+// share a per-frame running threshold.
 #include <algorithm>
 #include <cstdlib>
 
