@@ -8,7 +8,8 @@
 // candidate iff acc >= max(1, min_votes) and its key is the maximum of its
 // (2ht+1) x (2hr+1) window clipped to the accumulator.  DESIGN.md 6.3.
 //
-// launch_peaks: first peaks_fused_kernel (one CTA or cluster per frame): the
+// launch_peaks: first (windows of half_theta <= 12 and a window-cells x k
+// product <= 2^20) peaks_fused_kernel, one CTA or cluster per frame: the
 // certified bound from the peak hint (the voting kernel's, or one taken from
 // acc by hint_from_acc_kernel), the sparse search over the chunks that can
 // hold a top-k candidate, and the frame's top k (DESIGN R25, R30).  Frames it
