@@ -558,13 +558,17 @@ def run_batch(args, rank, world, dist):
     graphs = []
     if args.graph == "on":
         cap = torch.cuda.Stream()  # (capture needs a non-default stream; replays
-        for bf in bufs:            # then run on each buffer set's own stream)
-            g = torch.cuda.CUDAGraph()
-            launches[0] = 0
-            cap.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.graph(g, stream=cap):
-                step(bf, st=cap)
-            graphs.append((g, launches[0]))
+        try:                       # then run on each buffer set's own stream)
+            for bf in bufs:
+                g = torch.cuda.CUDAGraph()
+                launches[0] = 0
+                cap.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.graph(g, stream=cap):
+                    step(bf, st=cap)
+                graphs.append((g, launches[0]))
+        except RuntimeError as e:  # not capturable here: time the eager steps
+            print("bench: CUDA graph capture failed (%s); eager steps" % e, file=sys.stderr)
+            graphs = []
         torch.cuda.synchronize()
 
     def run_step(i):
