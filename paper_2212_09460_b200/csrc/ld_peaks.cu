@@ -946,7 +946,13 @@ struct HintFromAccParams {
 
 constexpr int HF_WARPS = 8;
 
-__global__ void __launch_bounds__(32 * HF_WARPS) hint_from_acc_kernel(const HintFromAccParams p) {
+#ifndef LD_HF_MINB
+#define LD_HF_MINB 4  // CTAs per SM the register budget is sized for (1 or 8: slower)
+#endif
+#ifndef LD_HF_CH
+#define LD_HF_CH 4  // chunks per warp in flight
+#endif
+__global__ void __launch_bounds__(32 * HF_WARPS, LD_HF_MINB) hint_from_acc_kernel(const HintFromAccParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, f = blockIdx.y;
   if (f == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
     uint32_t *h = p.hdr;
@@ -968,7 +974,7 @@ __global__ void __launch_bounds__(32 * HF_WARPS) hint_from_acc_kernel(const Hint
   // a chunk is 1 KB-aligned: lane l reads its counters 4l .. 4l+3 and
   // 128+4l .. 131+4l as two 16-byte vectors; the frame's first and last
   // chunks (bytes outside the frame) are read counter by counter
-  constexpr int CH = 4;  // chunks per warp in flight
+  constexpr int CH = LD_HF_CH;  // chunks per warp in flight
   const int stride = gridDim.x * HF_WARPS;
   for (int q0 = blockIdx.x * HF_WARPS + warp; q0 < p.n_seg; q0 += CH * stride) {
     uint4 v[CH][2];
