@@ -229,15 +229,18 @@ constexpr size_t PF_SMEM = sizeof(u64) * (PF_KEYS + SP_CAP + PF_SURV) + sizeof(i
 // the maximum above or below the centre row.  A vector reaching outside the
 // frame's cells (misaligned frame edges) is read cell by cell.  Cell indices
 // within a frame fit 32 bits (n_theta * n_rho < 2^31, checked by the host).
+// part / parts: a team of `parts` warps shares one test -- warp `part` takes
+// the non-centre rows q with q % parts == part (and part 0 the NEAR check and
+// the centre row); the cell is a window maximum iff every part returns true.
 template <int U, bool NEAR>
 __device__ __forceinline__ bool warp_window_max(const uint32_t *A, int64_t ncells, int n_theta,
                                                 int n_rho, int t, int r, uint32_t v, int ht,
-                                                int hr, int lane) {
+                                                int hr, int lane, int part = 0, int parts = 1) {
   const int idx = t * n_rho + r;
   const int ta = max(t - ht, 0), tb = min(t + ht, n_theta - 1);
   const int ra = max(r - hr, 0), rb = min(r + hr, n_rho - 1);
   const int nc = static_cast<int>(ncells);
-  if (NEAR) {
+  if (NEAR && part == 0) {
     const int dr = lane - 15;  // lanes 0..30: columns r-15 .. r+15
     const bool col = lane < 31 && r + dr >= ra && r + dr <= rb;
     uint32_t w[3];
@@ -253,7 +256,7 @@ __device__ __forceinline__ bool warp_window_max(const uint32_t *A, int64_t ncell
              (d == 1 && dr == 0 && w[d] != v);
     if (__any_sync(0xffffffffu, bad)) return false;
   }
-  {  // the centre row: before r < v, after r <= v, at r == v
+  if (part == 0) {  // the centre row: before r < v, after r <= v, at r == v
     bool bad = false;
     const int row0 = t * n_rho;
 #pragma unroll 4
@@ -263,12 +266,16 @@ __device__ __forceinline__ bool warp_window_max(const uint32_t *A, int64_t ncell
     }
     if (__any_sync(0xffffffffu, bad)) return false;
   }
-  const int rows = tb - ta;  // rows other than the centre one
+  // rows other than the centre one, this part's share: q = part + parts * i
+  const int rows = part < tb - ta ? (tb - ta - part + parts - 1) / parts : 0;
   if (rows == 0) return true;
   const int nv = (rb - ra + 3) / 4 + 1;  // vectors per row, at any alignment
   const int items = rows * nv;
   const int sh = static_cast<int>((reinterpret_cast<uintptr_t>(A) >> 2) & 3u);  // A's word offset mod 4
-  auto row_of = [&](int qq) { return ta + qq + (ta + qq >= t ? 1 : 0); };
+  auto row_of = [&](int qi) {  // the part's qi-th row
+    const int qq = part + parts * qi;
+    return ta + qq + (ta + qq >= t ? 1 : 0);
+  };
   // first cell of the aligned vector holding cell ra of row tt (frame index)
   auto first_vec = [&](int tt) {
     const int c = tt * n_rho + ra;
@@ -573,6 +580,7 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
   int *queue = reinterpret_cast<int *>(surv + PF_SURV);
   __shared__ uint32_t s_vbits[PF_KEYS / 32];      // verified keys (by sorted position)
   __shared__ int s_ok[2][NW];                     // a round's results, by parity
+  __shared__ int s_pok[NW];                       // the parts of the survivors' tests
   __shared__ int s_state, s_found, s_nq, s_ncand, s_nsurv, s_last, s_fail;
   __shared__ uint32_t s_tau;
   const int rank = G > 1 ? static_cast<int>(blockIdx.x % G) : 0;
@@ -844,20 +852,51 @@ __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams
 #if LD_PF_STATS
     if (tid == 0) st_surv += ns;
 #endif
-    // 2b: the survivors, dealt to the warps, through the exact test
-    for (int si = warp; si < ns; si += NW) {
-      const u64 key = surv[si];
-      const uint32_t v = static_cast<uint32_t>(key >> 32);
-      const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
-      const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
-      const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
-      if (warp_window_max<WU, true>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane) &&
-          lane == 0) {
-        const int slot = atomicAdd(ncand0, 1);
-        if (slot < SP_CAP) cand0[slot] = key;
+    // 2b: the survivors through the exact test, each by a team of T warps
+    // (few survivors: the whole CTA shares their windows' rows; many: one
+    // warp each), results combined in shared memory
+    int T = 1;
+    while (T < NW && T * 2 * ns <= NW) T *= 2;
+    if (T == 1) {  // a warp per survivor, no barrier between them
+      for (int si = warp; si < ns; si += NW) {
+        const u64 key = surv[si];
+        const uint32_t v = static_cast<uint32_t>(key >> 32);
+        const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+        const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
+        const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
+        if (warp_window_max<WU, true>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane) &&
+            lane == 0) {
+          const int slot = atomicAdd(ncand0, 1);
+          if (slot < SP_CAP) cand0[slot] = key;
+        }
+      }
+      __syncthreads();
+    } else {
+      const int per = NW / T;  // survivors per round (one round: ns <= per)
+      for (int sb = 0; sb < ns; sb += per) {
+        const int si = sb + warp / T, part = warp % T;
+        bool ok = true;
+        if (si < ns) {
+          const u64 key = surv[si];
+          const uint32_t v = static_cast<uint32_t>(key >> 32);
+          const uint32_t idx = 0xFFFFFFFFu - static_cast<uint32_t>(key);
+          const int t = static_cast<int>(idx / static_cast<uint32_t>(n_rho));
+          const int r = static_cast<int>(idx - static_cast<uint32_t>(t) * n_rho);
+          ok = warp_window_max<WU, true>(A, ncells, n_theta, n_rho, t, r, v, ht, hr, lane, part, T);
+        }
+        if (lane == 0) s_pok[warp] = ok ? 1 : 0;
+        __syncthreads();
+        if (tid < per && sb + tid < ns) {
+          bool all = true;
+          for (int j = 0; j < T; ++j) all = all && s_pok[tid * T + j];
+          if (all) {
+            const int slot = atomicAdd(ncand0, 1);
+            if (slot < SP_CAP) cand0[slot] = surv[sb + tid];
+          }
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
     if (tid == 0) {
       s_nq = 0;
       s_nsurv = 0;
