@@ -24,7 +24,7 @@ for sh in band theta; do
   timeout 300 python bench.py --workload cfg5 --shard $sh --steps 10 --warmup 3 > $out/${tag}_bench_cfg5_$sh.jsonl 2> $out/${tag}_bench_cfg5_$sh.err; echo cfg5_$sh=$?
 done
 for w in cfg1 cfg2; do
-  timeout 300 python bench.py --workload $w --steps 200 --warmup 5 > $out/${tag}_bench_$w.jsonl 2> $out/${tag}_bench_$w.err; echo $w=$?
+  timeout 300 python bench.py --workload $w --steps 1000 --warmup 5 > $out/${tag}_bench_$w.jsonl 2> $out/${tag}_bench_$w.err; echo $w=$?
 done
 timeout 300 python bench.py --workload cfg5 --steps 10 --warmup 3 > $out/${tag}_bench_cfg5.jsonl 2> $out/${tag}_bench_cfg5.err; echo cfg5=$?
 # the full ncu captures (~20 MB each) go in separate calls so that each call's
