@@ -817,6 +817,18 @@ def test_hinted_peaks_large_k(ld, oracle, k):
     _hint_case(ld, oracle, frames, cfg)
 
 
+@pytest.mark.parametrize("min_votes", [150, 200, 260, 100000])
+def test_hinted_peaks_min_votes_floor(ld, oracle, min_votes):
+    # a floor at, above or far above the k-th best peak (fewer than k
+    # candidates, or none): the keys below the floor end the verification, the
+    # result is the oracle's (sentinels included)
+    cfg = synth.CONFIGS["cfg2"]
+    frames = np.stack([synth.gen_frame("cfg2", 0), synth.gen_batch("cfg3", 5, 1)[0]])
+    cfg = synth.Config("mv", 1280, 720, 2, cfg.threshold, cfg.n_theta, cfg.k, cfg.half_theta,
+                       cfg.half_rho, min_votes)
+    _hint_case(ld, oracle, frames, cfg)
+
+
 def test_hint_of_another_accumulator(ld, oracle):
     # a hint recorded while voting frame A, used with frame B's accumulator
     # of the same shape at another address: the header matches, the chunk
