@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
   extern __shared__ __align__(16) uint32_t slice_raw[];
   __shared__ uint4 rowk[HV_MAX_ROWS];  // per pair: C, S, K = koff + (row t address << 13), -2C
 
+  LD_PDL_TRIGGER();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int band = blockIdx.x / G;
   const int rank = G > 1 ? static_cast<int>(blockIdx.x % G) : 0;  // rank in the cluster
@@ -448,6 +449,9 @@ __global__ void __launch_bounds__(HV_THREADS / CTAS, CTAS)
     }
   }
   __syncthreads();
+  // (the slice zeroed and the trig rows staged while the previous kernel of
+  // the stream -- the edge list's producer -- finished)
+  pdl_wait();
 
   // this CTA's part of the frame's list: all of it, or (cluster) the rank-th
   // of G parts, cut at multiples of 32 entries
@@ -571,22 +575,8 @@ static cudaError_t launch_pairs_cluster(const HoughParams &p, const TrigTable &t
   auto kern = hough_vote_pairs_kernel<CTAS, G>;
   cudaError_t e = ensure_smem_attr(attr, kern, -(227 * 1024 / CTAS));
   if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_bands * G, p.batch);
-  cfg.blockDim = dim3(HV_THREADS / CTAS);
-  cfg.dynamicSmemBytes = smem_bytes;
-  cfg.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = G;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, p, trig);
-  note_launch();
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(p.n_bands * G, p.batch), dim3(HV_THREADS / CTAS), smem_bytes, stream,
+                   G, p, trig);
 }
 
 cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int ctas,
@@ -611,10 +601,8 @@ cudaError_t launch_hough_pairs(const HoughParams &p, const TrigTable &trig, int 
   auto kern = ctas == 2 ? hough_vote_pairs_kernel<2, 1> : hough_vote_pairs_kernel<1, 1>;
   cudaError_t e = ensure_smem_attr(g_pairs_attr[ctas], kern, -(227 * 1024 / ctas));
   if (e != cudaSuccess) return e;
-  dim3 grid(p.n_bands, p.batch);
-  kern<<<grid, HV_THREADS / ctas, smem_bytes, stream>>>(p, trig);
-  note_launch();
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(p.n_bands, p.batch), dim3(HV_THREADS / ctas), smem_bytes, stream, 1,
+                   p, trig);
 }
 
 // ---------------------------------------------------------------------------

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <mutex>
+#include <utility>
 
 #include "../../include/ld.h"
 
@@ -272,6 +273,43 @@ static inline cudaError_t ensure_smem_attr(AttrOnce &a, K kern, int bytes) {
   return a.err[dev & 63];
 }
 
+// One kernel launch of the detect path: programmatic stream serialization
+// (the kernel may start while the previous kernel of the stream finishes; it
+// calls pdl_wait before reading that kernel's outputs) and, for cluster > 1,
+// a thread-block cluster of that many CTAs along x.  Counts the launch.
+#ifndef LD_PDL
+#define LD_PDL 1
+#endif
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t stream, int cluster, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (LD_PDL) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = static_cast<unsigned>(cluster);
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  note_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // PTX helpers
 // ---------------------------------------------------------------------------
@@ -328,6 +366,29 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+
+// Programmatic dependent launch (the kernels of one detect step are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization, launch_ex below):
+// every CTA lets the next kernel of the stream launch as soon as it runs
+// (pdl_launch_dependents: the next grid then fills the SMs this one frees in
+// its last wave and runs its own set-up), and waits for the previous kernel
+// to complete and flush (pdl_wait) before it reads that kernel's outputs.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// an early trigger in every CTA (experiment; default: the implicit trigger
+// at CTA exit, so waiting dependents never hold SM resources other streams'
+// kernels could use)
+#ifndef LD_PDL_EARLY
+#define LD_PDL_EARLY 0
+#endif
+#if LD_PDL_EARLY
+#define LD_PDL_TRIGGER() pdl_launch_dependents()
+#else
+#define LD_PDL_TRIGGER() ((void)0)
+#endif
 
 // shared-memory writes of this thread -> visible to the async proxy (bulk copies)
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -133,6 +133,8 @@ __device__ __forceinline__ bool is_window_max(const uint32_t *A, int n_theta, in
 }
 
 __global__ void __launch_bounds__(PK_THREADS) peaks_band_kernel(const PeaksParams p) {
+  LD_PDL_TRIGGER();
+  pdl_wait();  // the previous kernel of the stream (acc, hint, flags) is complete
   __shared__ u64 buf[PK_BUF];
   __shared__ u64 top[LD_MAX_K];
   __shared__ int s_nbuf, s_ntop;
@@ -568,6 +570,8 @@ __device__ __forceinline__ T *pf_at(T *p, int rank) {  // p in CTA `rank` of the
 
 template <int NT, int G, int MINB>
 __global__ void __launch_bounds__(NT, MINB) peaks_fused_kernel(const PeaksParams p) {
+  LD_PDL_TRIGGER();
+  pdl_wait();  // the previous kernel of the stream (acc, hint, flags) is complete
   constexpr int NW = NT / 32;
   constexpr int S = PF_KEYS / NT;
   // window-test vectors in flight per lane (the register budget; 8 measured no faster)
@@ -992,6 +996,8 @@ constexpr int HF_WARPS = 8;
 #define LD_HF_CH 4  // chunks per warp in flight
 #endif
 __global__ void __launch_bounds__(32 * HF_WARPS, LD_HF_MINB) hint_from_acc_kernel(const HintFromAccParams p) {
+  LD_PDL_TRIGGER();
+  pdl_wait();  // the previous kernel of the stream (acc, hint, flags) is complete
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, f = blockIdx.y;
   if (f == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
     uint32_t *h = p.hdr;
@@ -1114,12 +1120,12 @@ cudaError_t launch_hint_from_acc(const uint32_t *acc, int batch, int n_theta, in
   const int want = (8 * sms + batch - 1) / batch;
   const int gx = std::max(1, std::min(want, (p.n_seg + HF_WARPS - 1) / HF_WARPS));
   dim3 grid(static_cast<unsigned>(gx), batch);
-  hint_from_acc_kernel<<<grid, 32 * HF_WARPS, 0, stream>>>(p);
-  note_launch();
-  return cudaGetLastError();
+  return launch_ex(hint_from_acc_kernel, grid, dim3(32 * HF_WARPS), 0, stream, 1, p);
 }
 
 __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksParams p) {
+  LD_PDL_TRIGGER();
+  pdl_wait();  // the previous kernel of the stream (acc, hint, flags) is complete
   __shared__ u64 buf[PK_BUF];
   __shared__ u64 top[LD_MAX_K];
   __shared__ int s_ntop;
@@ -1199,6 +1205,8 @@ __global__ void __launch_bounds__(PK_THREADS) peaks_merge_kernel(const PeaksPara
 // ---------------------------------------------------------------------------
 template <int HT>
 __global__ void __launch_bounds__(PT_MAX_THREADS) peaks_tile_kernel(const PeaksParams p) {
+  LD_PDL_TRIGGER();
+  pdl_wait();  // the previous kernel of the stream (acc, hint, flags) is complete
   extern __shared__ __align__(16) unsigned char psm[];
   constexpr int NV = PT_TR + 2 * HT;
   constexpr int PF = 2;  // prefilter radius in rho
@@ -1358,6 +1366,8 @@ __device__ __forceinline__ void stream_store(uint32_t *dst, const uint32_t (&v)[
 template <int HT, int CPT, int MINB>
 __global__ void __launch_bounds__(MINB == 2 ? PS_NT_MAX2 : PS_NT_MAX, MINB)
     peaks_stream_kernel(const PeaksParams p) {
+  LD_PDL_TRIGGER();
+  pdl_wait();  // the previous kernel of the stream (acc, hint, flags) is complete
   constexpr int NV = PS_G + 2 * HT;
   static_assert(PS_G * CPT <= 32, "survivor mask");
   extern __shared__ __align__(16) unsigned char psm[];
@@ -1841,6 +1851,8 @@ template <int HT>
 #define LD_PW_MINB 2
 #endif
 __global__ void __launch_bounds__(32 * PW_W, LD_PW_MINB) peaks_warp_kernel(const PeaksParams p) {
+  LD_PDL_TRIGGER();
+  pdl_wait();  // the previous kernel of the stream (acc, hint, flags) is complete
   extern __shared__ __align__(16) unsigned char psm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x * PW_W + warp, f = blockIdx.y;
@@ -2122,22 +2134,7 @@ static cudaError_t launch_fused_g(const PeaksParams &p, AttrOnce &attr, cudaStre
   auto kern = peaks_fused_kernel<NT, G, MINB>;
   cudaError_t e = ensure_smem_attr(attr, kern, static_cast<int>(PF_SMEM));
   if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.batch * G);
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = PF_SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = G;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, p);
-  note_launch();
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(p.batch * G), dim3(NT), PF_SMEM, stream, G, p);
 }
 
 static cudaError_t launch_fused(const PeaksParams &p, int sms, cudaStream_t stream) {
@@ -2172,9 +2169,7 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
   p.resolved = nullptr;
   if (n_cand <= 0) {  // no candidate rows: the merge writes sentinels and 0 peaks
     p.n_units = 0;
-    peaks_merge_kernel<<<p.batch, PK_THREADS, 0, stream>>>(p);
-    note_launch();
-    return cudaGetLastError();
+    return launch_ex(peaks_merge_kernel, dim3(p.batch), dim3(PK_THREADS), 0, stream, 1, p);
   }
   const bool dense_cheap = !force_band && !force_tile && !force_stream &&
       peaks_warp_plan(p.batch, n_cand, p.n_rho, p.half_theta, p.half_rho, p.k, sms, &p, &smem);
@@ -2217,31 +2212,30 @@ cudaError_t launch_peaks(const PeaksParams &p_in, uint32_t flags, cudaStream_t s
     cudaError_t e = ensure_smem_attr(g_warp_attr[p.half_theta], kern, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     dim3 g1((p.n_units + PW_W - 1) / PW_W, p.batch);
-    kern<<<g1, 32 * PW_W, smem, stream>>>(p);
+    e = launch_ex(kern, g1, dim3(32 * PW_W), smem, stream, 1, p);
+    if (e != cudaSuccess) return e;
   } else if (dense_stream) {
     StreamKernel kern = stream_kernel(p.half_theta, cpt);
     cudaError_t e = ensure_smem_attr(g_stream_attr[cpt == 4][p.half_theta], kern, 220 * 1024);
     if (e != cudaSuccess) return e;
     dim3 g1(p.n_units, p.batch);
-    kern<<<g1, p.st_nt, smem, stream>>>(p);
+    e = launch_ex(kern, g1, dim3(p.st_nt), smem, stream, 1, p);
+    if (e != cudaSuccess) return e;
   } else if (!force_band && !restricted &&
              peaks_tile_plan(p.n_theta, p.n_rho, p.half_theta, p.half_rho, p.k, &p, &smem)) {
     TileKernel kern = tile_kernel(p.half_theta);
     cudaError_t e = ensure_smem_attr(g_tile_attr[p.half_theta], kern, 200 * 1024);
     if (e != cudaSuccess) return e;
     dim3 g1(p.n_units, p.batch);
-    kern<<<g1, p.tch, smem, stream>>>(p);
+    e = launch_ex(kern, g1, dim3(p.tch), smem, stream, 1, p);
+    if (e != cudaSuccess) return e;
   } else {
     p.n_units = (n_cand + PK_ROWS - 1) / PK_ROWS;
     dim3 g1(p.n_units, p.batch);
-    peaks_band_kernel<<<g1, PK_THREADS, 0, stream>>>(p);
+    const cudaError_t e = launch_ex(peaks_band_kernel, g1, dim3(PK_THREADS), 0, stream, 1, p);
+    if (e != cudaSuccess) return e;
   }
-  note_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  peaks_merge_kernel<<<p.batch, PK_THREADS, 0, stream>>>(p);
-  note_launch();
-  return cudaGetLastError();
+  return launch_ex(peaks_merge_kernel, dim3(p.batch), dim3(PK_THREADS), 0, stream, 1, p);
 }
 
 }  // namespace ld

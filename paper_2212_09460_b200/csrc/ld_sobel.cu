@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
 
+  LD_PDL_TRIGGER();
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(SB_THREADS + 32, MINB)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();  // the previous kernel of the stream is done (frames, counts)
 
   if (warp == NCW) {  // ---------------- producer warp
     if (lane == 0) {
@@ -409,9 +411,7 @@ static cudaError_t launch_cfg(const CUtensorMap &tmap, const SobelParams &p, int
   static AttrOnce attr;
   const cudaError_t e = ensure_smem_attr(attr, kern, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<n_ctas, SB_THREADS + 32, smem, stream>>>(tmap, p);
-  note_launch();
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(n_ctas), dim3(SB_THREADS + 32), smem, stream, 1, tmap, p);
 }
 
 // Launch configuration: SR = 8 rows per thread strip (128-row tiles), 2 TMA
